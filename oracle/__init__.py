@@ -1,0 +1,242 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU checker for the CUDA path.
+
+Two backends with one interface:
+  * ``Oracle("port")``       the plain-C restatement (oracle/me_oracle.c ->
+                             oracle/liboracle.so), no dependency on the
+                             reference at run time;
+  * ``Oracle("reference")``  the UNMODIFIED reference sources compiled by
+                             oracle/Makefile into oracle/_ref/libme_ref.so,
+                             driven by oracle/ref_driver.cpp.
+Only tests/, __graft_entry__.smoke() and bench.py's reference/cpu_baseline legs
+may import this package; the product (paper_1002_1168_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_LIB = os.path.join(HERE, "liboracle.so")
+REF_LIB = os.path.join(HERE, "_ref", "libme_ref.so")
+REF_SRC = "/root/reference/proj"
+
+ME_OK = 0
+
+
+def build(ref: bool = True, quiet: bool = True):
+    """Compiles the restatement (always) and oracle/_ref (when the reference
+    sources are present, i.e. in the build container)."""
+    target = ["all"]
+    if ref and os.path.isdir(REF_SRC):
+        target = ["ref"]
+    out = subprocess.run(["make", "-C", HERE] + target, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
+
+
+def _rec_dtype():
+    return np.dtype([("dx", "<i2"), ("dy", "<i2"), ("cost_q4", "<u4"), ("comparisons", "<u2"), ("dpd_steps", "<u2"), ("iterations", "u1"), ("type", "u1"), ("reserved", "<u2")])
+
+
+def _stats_dtype():
+    return np.dtype([(n, "<i8") for n in ("block_comparisons", "dpd_refinement_steps", "blocks_opaque", "blocks_boundary", "blocks_transparent", "sse")])
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("algo", C.c_int32), ("search_range", C.c_int32), ("block_size", C.c_int32), ("ref_distance", C.c_int32), ("halfpel", C.c_int32), ("max_iterations", C.c_int32), ("step", C.c_int32), ("boundary_temporal", C.c_int32), ("epsilon", C.c_double), ("theta", C.c_double)]
+
+
+def make_cfg(algo=4, search_range=16, block_size=8, ref_distance=2, halfpel=0, max_iterations=4, step=2, boundary_temporal=0, epsilon=0.5, theta=2.0):
+    return _Cfg(algo, search_range, block_size, ref_distance, halfpel, max_iterations, step, boundary_temporal, epsilon, theta)
+
+
+def _vp(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class OracleError(Exception):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class Oracle:
+    def __init__(self, kind: str = "port"):
+        self.kind = kind
+        path = PORT_LIB if kind == "port" else REF_LIB
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.L = C.CDLL(path)
+        self.p = "orc_" if kind == "port" else "ref_"
+        self.L[self.p + "last_error"].restype = C.c_char_p
+
+    def _f(self, name):
+        return self.L[self.p + name]
+
+    def _chk(self, rc):
+        if rc != ME_OK:
+            raise OracleError(rc, self._f("last_error")().decode())
+
+    # -- sequences ---------------------------------------------------------
+    def run_sequence(self, cfg: _Cfg, luma: np.ndarray, alpha=None, want_pred=False):
+        luma = np.ascontiguousarray(luma, np.uint8)
+        F, H, W = luma.shape
+        if alpha is not None:
+            alpha = np.ascontiguousarray(alpha, np.uint8)
+        pairs = F - cfg.ref_distance
+        bs = cfg.block_size
+        recs = np.zeros((pairs, H // bs, W // bs), _rec_dtype())
+        stats = np.zeros(pairs, _stats_dtype())
+        pred = np.zeros((pairs, H, W), np.uint8) if want_pred else None
+        self._chk(self._f("run_sequence")(C.byref(cfg), F, W, H, _vp(luma), _vp(alpha), _vp(recs), _vp(stats), _vp(pred)))
+        return (recs, stats, pred) if want_pred else (recs, stats)
+
+    def estimate_field(self, cfg: _Cfg, cur, ref, ca=None, ra=None, prev_mv=None):
+        """One pair (port only): orc_estimate_field with an optional previous field."""
+        assert self.kind == "port"
+        cur, ref = np.ascontiguousarray(cur), np.ascontiguousarray(ref)
+        H, W = cur.shape
+        bs = cfg.block_size
+        cols, rows = W // bs, H // bs
+        recs = np.zeros(cols * rows, _rec_dtype())
+        st = np.zeros(1, _stats_dtype())
+        pm = None if prev_mv is None else np.ascontiguousarray(prev_mv, np.int32)
+        self._chk(self._f("estimate_field")(C.byref(cfg), W, H, _vp(cur), _vp(ref), _vp(ca), _vp(ra), _vp(pm), cols, rows, _vp(recs), _vp(st)))
+        return recs, st[0]
+
+    # -- per block ---------------------------------------------------------
+    def block_search(self, algo, cur, ref, x0, y0, size, rng):
+        cur, ref = np.ascontiguousarray(cur), np.ascontiguousarray(ref)
+        H, W = cur.shape
+        mv = (C.c_int32 * 2)()
+        cmp = C.c_int64()
+        cost = C.c_uint32()
+        self._chk(self._f("block_search")(algo, W, H, _vp(cur), _vp(ref), x0, y0, size, rng, mv, C.byref(cmp), C.byref(cost)))
+        return (mv[0], mv[1]), cmp.value, cost.value
+
+    def brs_select(self, cur, ref, ca, ra, x0, y0, size, btype, cands, rng, bt=0):
+        cur, ref = np.ascontiguousarray(cur), np.ascontiguousarray(ref)
+        H, W = cur.shape
+        cd = (C.c_int32 * 8)(*[int(v) for v in cands])
+        mv = (C.c_int32 * 2)()
+        kinds = (C.c_uint8 * 4)()
+        if self.kind == "port":
+            scores = (C.c_uint32 * 4)()
+            self._chk(self._f("brs_select")(W, H, _vp(cur), _vp(ref), _vp(ca), _vp(ra), x0, y0, size, btype, cd, rng, bt, mv, kinds, scores))
+        else:
+            cmp = C.c_int64()
+            self._chk(self._f("brs_select")(W, H, _vp(cur), _vp(ref), _vp(ca), _vp(ra), x0, y0, size, btype, cd, rng, bt, mv, kinds, C.byref(cmp)))
+        return (mv[0], mv[1]), list(kinds)
+
+    def prs_refine(self, cur, ref, x0, y0, size, d0, rng, eps=0.5, theta=2.0, max_iter=4, step=2):
+        cur, ref = np.ascontiguousarray(cur), np.ascontiguousarray(ref)
+        H, W = cur.shape
+        d = (C.c_int32 * 2)(*d0)
+        mv = (C.c_int32 * 2)()
+        dpd = C.c_int64()
+        log = (C.c_uint32 * 256)()
+        n = C.c_int()
+        f = self._f("prs_refine")
+        f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        self._chk(f(W, H, _vp(cur), _vp(ref), x0, y0, size, d, rng, eps, theta, max_iter, step, mv, C.byref(dpd), log, C.byref(n)))
+        return (mv[0], mv[1]), dpd.value, [log[i] for i in range(n.value)]
+
+    def prs_update(self, cur, ref, x, y, d, eps=0.5, theta=2.0):
+        cur, ref = np.ascontiguousarray(cur), np.ascontiguousarray(ref)
+        H, W = cur.shape
+        dd = (C.c_int32 * 2)(*d)
+        out = (C.c_double * 2)()
+        f = self._f("prs_update")
+        f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+        rc = f(W, H, _vp(cur), _vp(ref), x, y, dd, eps, theta, out)
+        if self.kind != "port":
+            self._chk(rc)
+        return out[0], out[1]
+
+    def sad_texture(self, cur, ref, x0, y0, size, dx, dy):
+        cur, ref = np.ascontiguousarray(cur), np.ascontiguousarray(ref)
+        H, W = cur.shape
+        if self.kind == "port":
+            f = self._f("sad_texture")
+            f.restype = C.c_double
+            return f(W, H, _vp(cur), _vp(ref), x0, y0, size, dx, dy)
+        out = C.c_double()
+        self._chk(self._f("sad_texture")(W, H, _vp(cur), _vp(ref), x0, y0, size, dx, dy, C.byref(out)))
+        return out.value
+
+    def sad_shape(self, ca, ra, x0, y0, size, dx, dy):
+        ca, ra = np.ascontiguousarray(ca), np.ascontiguousarray(ra)
+        H, W = ca.shape
+        out = C.c_int64()
+        self._chk(self._f("sad_shape")(W, H, _vp(ca), _vp(ra), x0, y0, size, dx, dy, C.byref(out)))
+        return out.value
+
+    def classify(self, alpha, size, W=None, H=None):
+        if alpha is not None:
+            alpha = np.ascontiguousarray(alpha)
+            H, W = alpha.shape
+        out = np.zeros((H // size) * (W // size), np.uint8)
+        self._chk(self._f("classify")(W, H, _vp(alpha), size, _vp(out)))
+        return out
+
+    def binarize(self, gray, thr=128):
+        gray = np.ascontiguousarray(gray)
+        H, W = gray.shape
+        out = np.zeros_like(gray)
+        self._f("binarize")(W, H, _vp(gray), thr, _vp(out))
+        return out
+
+    def predict_frame(self, ref, mv, types, bs):
+        ref = np.ascontiguousarray(ref)
+        H, W = ref.shape
+        mv = np.ascontiguousarray(mv, np.int32)
+        types = None if types is None else np.ascontiguousarray(types, np.uint8)
+        out = np.zeros_like(ref)
+        self._chk(self._f("predict_frame")(W, H, _vp(ref), _vp(mv), _vp(types), bs, _vp(out)))
+        return out
+
+    # -- timing (CPU baseline) -------------------------------------------------
+    def time_sequences(self, cfg, luma, alpha, threads):
+        """n_seq sequences ([n_seq, F, H, W]) on `threads` host threads."""
+        n_seq, F, H, W = luma.shape
+        if self.kind == "port":
+            pairs = F - cfg.ref_distance
+            recs = np.zeros((n_seq, pairs, H // cfg.block_size, W // cfg.block_size), _rec_dtype())
+            stats = np.zeros((n_seq, pairs), _stats_dtype())
+            self._chk(self._f("run_sequences_threaded")(C.byref(cfg), n_seq, F, W, H, _vp(luma), _vp(alpha), _vp(recs), _vp(stats), threads))
+            return int(stats["block_comparisons"].sum())
+        cs = C.c_int64()
+        self._chk(self._f("time_sequences")(C.byref(cfg), n_seq, F, W, H, _vp(luma), _vp(alpha), threads, C.byref(cs)))
+        return cs.value
+
+    def time_pairs(self, cfg, luma, alpha, first_pair, n_pairs, threads):
+        F, H, W = luma.shape
+        if self.kind == "port":
+            recs = np.zeros((n_pairs, H // cfg.block_size, W // cfg.block_size), _rec_dtype())
+            stats = np.zeros(n_pairs, _stats_dtype())
+            self._chk(self._f("run_pairs_threaded")(C.byref(cfg), F, W, H, _vp(luma), _vp(alpha), first_pair, n_pairs, _vp(recs), _vp(stats), threads))
+            return int(stats["block_comparisons"].sum())
+        cs = C.c_int64()
+        self._chk(self._f("time_pairs")(C.byref(cfg), F, W, H, _vp(luma), _vp(alpha), first_pair, n_pairs, threads, C.byref(cs)))
+        return cs.value
+
+    def time_blocks(self, cfg, cur, ref, block_xy, threads):
+        """Block searches on an explicit (x0, y0) list; returns total comparisons."""
+        H, W = cur.shape
+        xy = np.ascontiguousarray(block_xy, np.int32)
+        n = xy.shape[0]
+        if self.kind == "port":
+            mv = np.zeros((n, 2), np.int32)
+            cmp = np.zeros(n, np.int64)
+            self._f("search_blocks")(C.byref(cfg), W, H, _vp(cur), _vp(ref), _vp(xy), n, threads, _vp(mv), _vp(cmp))
+            return int(cmp.sum())
+        cmp = C.c_int64()
+        self._chk(self._f("time_blocks")(C.byref(cfg), W, H, _vp(cur), _vp(ref), _vp(xy), n, threads, C.byref(cmp)))
+        return cmp.value

@@ -1,0 +1,103 @@
+"""Batched sequence pipeline (the benchmark path): the frame-pair loop of the
+reference's run_experiment (proj/src/bench.cpp:155-205) over many sequences at
+once, fully on the GPU (me_b200_run_sequences_dev / me_b200_run_sequences).
+
+torch is used only for device memory and streams; the compute is the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import MeConfig, check, ctx, lib
+from .api import Algo, BoundaryTemporal, PrsConfig, SearchConfig, _cfg
+
+
+@dataclass
+class BatchConfig:
+    algo: Algo = Algo.PA
+    search: SearchConfig = None
+    prs: PrsConfig = None
+    boundary_temporal: BoundaryTemporal = BoundaryTemporal.Texture
+
+    def __post_init__(self):
+        if self.search is None:
+            self.search = SearchConfig()
+        if self.prs is None:
+            self.prs = PrsConfig()
+
+    def c(self) -> MeConfig:
+        return _cfg(self.algo, self.search, self.prs, self.boundary_temporal)
+
+
+def rec_view(t):
+    """Views a uint8 torch/numpy buffer of records as the me_block_rec dtype."""
+    a = t.cpu().numpy() if hasattr(t, "cpu") else t
+    return a.view(_lib.rec_dtype())
+
+
+def run_sequences_dev(cfg: BatchConfig, luma, alpha=None, recs=None, stats=None, pred=None, device: int = 0, stream=None):
+    """Device-resident inputs: luma/alpha are uint8 CUDA tensors [n_seq, F, H, W].
+
+    Returns (recs, stats) as uint8 CUDA tensors of shape [n_seq, pairs, rows,
+    cols, 16] and [n_seq, pairs, 48] (views via ``rec_view``); enqueued on
+    ``stream`` (torch's current stream when None), not synchronised.
+    """
+    import torch
+
+    n_seq, F, H, W = luma.shape
+    bs = cfg.search.block_size
+    pairs = F - cfg.search.ref_distance
+    rows, cols = H // bs, W // bs
+    if recs is None:
+        recs = torch.empty((n_seq, pairs, rows, cols, 16), dtype=torch.uint8, device=luma.device)
+    if stats is None:
+        stats = torch.empty((n_seq, pairs, 48), dtype=torch.uint8, device=luma.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(luma.device).cuda_stream
+    c = cfg.c()
+    check(
+        lib().me_b200_run_sequences_dev(
+            ctx(device), C.byref(c), n_seq, F, W, H,
+            C.c_void_p(luma.data_ptr()),
+            C.c_void_p(alpha.data_ptr()) if alpha is not None else None,
+            C.c_void_p(recs.data_ptr()), C.c_void_p(stats.data_ptr()),
+            C.c_void_p(pred.data_ptr()) if pred is not None else None,
+            C.c_void_p(stream),
+        )
+    )
+    return recs, stats
+
+
+def run_sequences(cfg: BatchConfig, luma: np.ndarray, alpha: Optional[np.ndarray] = None, want_pred: bool = False, device: int = 0):
+    """End to end from host arrays [n_seq, F, H, W] (pinned or pageable):
+    H2D, device pipeline, D2H.  Returns (recs, stats[, pred]) numpy arrays."""
+    luma = np.ascontiguousarray(luma, np.uint8)
+    if luma.ndim == 3:
+        luma = luma[None]
+    n_seq, F, H, W = luma.shape
+    if alpha is not None:
+        alpha = np.ascontiguousarray(alpha, np.uint8).reshape(luma.shape)
+    bs = cfg.search.block_size
+    pairs = F - cfg.search.ref_distance
+    if pairs < 1:
+        raise ValueError("ref_distance must be smaller than the frame count")
+    recs = np.zeros((n_seq, pairs, H // bs, W // bs), _lib.rec_dtype())
+    stats = np.zeros((n_seq, pairs), _lib.stats_dtype())
+    pred = np.zeros((n_seq, pairs, H, W), np.uint8) if want_pred else None
+    c = cfg.c()
+    vp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+    check(lib().me_b200_run_sequences(ctx(device), C.byref(c), n_seq, F, W, H, vp(luma), vp(alpha), vp(recs), vp(stats), vp(pred)))
+    if want_pred:
+        return recs, stats, pred
+    return recs, stats
+
+
+def run_sequences_ptr(cfg: BatchConfig, n_seq: int, F: int, W: int, H: int, luma_ptr: int, alpha_ptr: Optional[int], recs_ptr: int, stats_ptr: int, device: int = 0):
+    """Raw host-pointer form (e.g. pinned torch tensors) for end-to-end timing."""
+    c = cfg.c()
+    check(lib().me_b200_run_sequences(ctx(device), C.byref(c), n_seq, F, W, H, C.c_void_p(luma_ptr), C.c_void_p(alpha_ptr) if alpha_ptr else None, C.c_void_p(recs_ptr), C.c_void_p(stats_ptr), None))

@@ -1,0 +1,566 @@
+// capi.cu — the C ABI (include/me_b200.h): argument validation with the
+// reference's error semantics, per-thread contexts with device buffer caches,
+// host<->device staging for the host-pointer entry points, and dispatch into
+// the kernels of kernels.cu.  No CPU compute path exists: every entry point
+// either runs on an sm_100 device or fails with ME_ERR_NO_DEVICE.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "me_b200.h"
+#include "me_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+me_status me_fail(me_status code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+namespace {
+
+me_status ok() {
+    g_last_error.clear();
+    return ME_OK;
+}
+
+bool device_ok(int dev) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return false;
+    return p.major == 10;  // sm_100 family (the fatbin carries sm_100a code only)
+}
+
+// SearchConfig::validate + PrsConfig::validate (estimators.cpp:139-150)
+me_status validate(const me_config* c) {
+    if (!c) return me_fail(ME_ERR_INVALID_ARGUMENT, "null config");
+    if (c->search_range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (c->block_size != 8 && c->block_size != 16)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
+    if (c->ref_distance < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "ref_distance must be >= 1");
+    if (!(c->epsilon > 0.0)) return me_fail(ME_ERR_INVALID_ARGUMENT, "epsilon must be > 0");
+    if (!(c->theta > 0.0)) return me_fail(ME_ERR_INVALID_ARGUMENT, "theta must be > 0");
+    if (c->max_iterations < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "max_iterations must be >= 1");
+    if (c->step != 1 && c->step != 2)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "step must be 1 or 2 half-pels");
+    if (c->algo < ME_ALGO_ES || c->algo > ME_ALGO_PA)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "unknown algorithm");
+    if (c->boundary_temporal != ME_BT_TEXTURE && c->boundary_temporal != ME_BT_SHAPE)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "unknown boundary_temporal");
+    return ME_OK;
+}
+
+me_status check_rect(int W, int H, int x0, int y0, int size) {
+    // require_inside (estimators.cpp:105-110)
+    if (x0 < 0 || y0 < 0 || size <= 0 || x0 + size > W || y0 + size > H)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "block rect outside the frame");
+    return ME_OK;
+}
+
+me_status check_ctx(me_ctx* ctx) {
+    if (!ctx) return me_fail(ME_ERR_INVALID_ARGUMENT, "null context");
+    if (cudaSetDevice(ctx->device) != cudaSuccess)
+        return me_fail(ME_ERR_NO_DEVICE, "cannot select device");
+    return ME_OK;
+}
+
+// Copies a host plane into a device buffer (size rounded up; zero padded so
+// word loads of the last row never leave the allocation).
+me_status upload(me_ctx* ctx, DevBuf& buf, size_t off, const void* host, size_t n) {
+    ME_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(buf.p) + off, host, n, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    return ME_OK;
+}
+
+size_t pad16(size_t n) { return (n + 15) & ~size_t(15); }
+
+me_status sync(me_ctx* ctx) {
+    ME_CUDA(cudaStreamSynchronize(ctx->stream));
+    ME_CUDA(cudaGetLastError());
+    return ME_OK;
+}
+
+// Stages up to 4 host planes of n bytes each into ctx->in_luma (contiguous,
+// 16-byte padded slots); returns device pointers (null for null inputs).
+me_status stage_planes(me_ctx* ctx, size_t n, const uint8_t* const* host, const uint8_t** dev,
+                       int count) {
+    const size_t slot = pad16(n) + 256;
+    ME_CUDA(ctx->in_luma.reserve(slot * count));
+    ME_CUDA(cudaMemsetAsync(ctx->in_luma.p, 0, slot * count, ctx->stream));
+    for (int i = 0; i < count; ++i) {
+        if (!host[i]) {
+            dev[i] = nullptr;
+            continue;
+        }
+        me_status s = upload(ctx, ctx->in_luma, slot * i, host[i], n);
+        if (s) return s;
+        dev[i] = static_cast<const uint8_t*>(ctx->in_luma.p) + slot * i;
+    }
+    return ME_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* me_b200_version(void) { return "me_b200 1.0 (sm_100a)"; }
+
+const char* me_b200_last_error(void) { return g_last_error.c_str(); }
+
+int me_b200_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int good = 0;
+    for (int i = 0; i < n; ++i) good += device_ok(i) ? 1 : 0;
+    return good;
+}
+
+me_status me_b200_ctx_create(int device, me_ctx** out) {
+    if (!out) return me_fail(ME_ERR_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return me_fail(ME_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device));
+    }
+    if (!device_ok(device))
+        return me_fail(ME_ERR_NO_DEVICE, "device " + std::to_string(device) + " is not sm_100");
+    ME_CUDA(cudaSetDevice(device));
+    me_ctx* c = new me_ctx;
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return me_fail(ME_ERR_CUDA, "stream creation failed");
+    }
+    *out = c;
+    return ok();
+}
+
+void me_b200_ctx_destroy(me_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->types, &c->worklist, &c->counters, &c->tasks, &c->in_luma, &c->in_alpha,
+                      &c->out_recs, &c->out_stats, &c->out_pred, &c->aux})
+        b->release();
+    c->pin_a.release();
+    c->pin_b.release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+void* me_b200_ctx_stream(me_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+me_status me_b200_validate_config(const me_config* cfg) {
+    me_status s = validate(cfg);
+    return s ? s : ok();
+}
+
+static me_status check_batch(const me_config* cfg, int n_seq, int n_frames, int W, int H) {
+    me_status s = validate(cfg);
+    if (s) return s;
+    if (n_seq < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "n_seq must be >= 1");
+    if (W <= 0 || H <= 0 || W % 16 || H % 16)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "frame dimensions must be positive multiples of 16");
+    if (cfg->ref_distance >= n_frames)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "ref_distance must be smaller than the frame count");
+    const int64_t nb = int64_t(n_seq) * (n_frames - cfg->ref_distance) * (W / cfg->block_size) *
+                       (H / cfg->block_size);
+    if (nb >= (int64_t(1) << 31)) return me_fail(ME_ERR_INVALID_ARGUMENT, "batch too large (2^31 blocks)");
+    if (int64_t(W - cfg->block_size + 1) * (H - cfg->block_size + 1) >= (int64_t(1) << 24))
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "frame too large for the packed ES key");
+    return ME_OK;
+}
+
+static mek::Batch make_batch(const me_config* cfg, int n_seq, int n_frames, int W, int H,
+                             const uint8_t* luma, const uint8_t* alpha) {
+    mek::Batch b;
+    b.luma = luma;
+    b.alpha = alpha;
+    b.n_seq = n_seq;
+    b.F = n_frames;
+    b.W = W;
+    b.H = H;
+    b.d = cfg->ref_distance;
+    b.pairs = n_frames - cfg->ref_distance;
+    b.bs = cfg->block_size;
+    b.cols = W / cfg->block_size;
+    b.rows = H / cfg->block_size;
+    return b;
+}
+
+me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames,
+                                    int W, int H, const uint8_t* luma, const uint8_t* alpha,
+                                    me_block_rec* recs, me_pair_stats* stats, uint8_t* pred,
+                                    void* stream) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
+    if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    if ((reinterpret_cast<uintptr_t>(luma) | reinterpret_cast<uintptr_t>(alpha) |
+         reinterpret_cast<uintptr_t>(recs)) & 15)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "device buffers must be 16-byte aligned");
+    const mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H, luma, alpha);
+    const size_t need = mek::scratch_bytes(b, cfg->algo);
+    ME_CUDA(ctx->tasks.reserve(need));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, pred, ctx->tasks.p, ctx->tasks.cap,
+                           ctx->num_sms, st));
+    return ok();
+}
+
+me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
+                                int H, const uint8_t* luma, const uint8_t* alpha,
+                                me_block_rec* recs, me_pair_stats* stats, uint8_t* pred) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
+    if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const size_t plane = size_t(W) * H;
+    const size_t in_bytes = plane * n_frames * n_seq;
+    const int pairs = n_frames - cfg->ref_distance;
+    const size_t nrec = size_t(n_seq) * pairs * (W / cfg->block_size) * (H / cfg->block_size);
+    ME_CUDA(ctx->in_luma.reserve(in_bytes + 256));
+    if (alpha) ME_CUDA(ctx->in_alpha.reserve(in_bytes + 256));
+    ME_CUDA(ctx->out_recs.reserve(nrec * sizeof(me_block_rec)));
+    ME_CUDA(ctx->out_stats.reserve(size_t(n_seq) * pairs * sizeof(me_pair_stats)));
+    if (pred) ME_CUDA(ctx->out_pred.reserve(plane * pairs * n_seq));
+    ME_CUDA(cudaMemcpyAsync(ctx->in_luma.p, luma, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (alpha)
+        ME_CUDA(cudaMemcpyAsync(ctx->in_alpha.p, alpha, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    const mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H,
+                                    static_cast<const uint8_t*>(ctx->in_luma.p),
+                                    alpha ? static_cast<const uint8_t*>(ctx->in_alpha.p) : nullptr);
+    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+    ME_CUDA(mek::run_batch(b, *cfg, nullptr, static_cast<me_block_rec*>(ctx->out_recs.p),
+                           static_cast<me_pair_stats*>(ctx->out_stats.p),
+                           pred ? static_cast<uint8_t*>(ctx->out_pred.p) : nullptr, ctx->tasks.p,
+                           ctx->tasks.cap, ctx->num_sms, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(recs, ctx->out_recs.p, nrec * sizeof(me_block_rec),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(stats, ctx->out_stats.p, size_t(n_seq) * pairs * sizeof(me_pair_stats),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    if (pred)
+        ME_CUDA(cudaMemcpyAsync(pred, ctx->out_pred.p, plane * pairs * n_seq, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
+me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H,
+                                 const uint8_t* cur, const uint8_t* ref, const uint8_t* cur_alpha,
+                                 const uint8_t* ref_alpha, const int32_t* prev_mv, int prev_cols,
+                                 int prev_rows, me_block_rec* recs, me_pair_stats* stats) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = validate(cfg))) return s;  // cfg.validate(); prs.validate() (estimators.cpp:390-391)
+    if (!cur || !ref || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    if (W <= 0 || H <= 0) return me_fail(ME_ERR_INVALID_ARGUMENT, "frame dimensions must be positive");
+    const int bs = cfg->block_size;
+    if (W % bs || H % bs)  // block_grid (frame.cpp:106-110)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "block size does not divide the frame");
+    const int cols = W / bs, rows = H / bs;
+    if (prev_mv && (prev_cols != cols || prev_rows != rows))
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "previous motion field grid mismatch");
+    if (W % 8) return me_fail(ME_ERR_INVALID_ARGUMENT, "frame width must be a multiple of 8");
+    const size_t plane = size_t(W) * H;
+    // frame 0 = ref, frame 1 = cur (one pair at ref_distance 1)
+    me_config c1 = *cfg;
+    c1.ref_distance = 1;
+    const size_t slot = pad16(plane) + 256;
+    ME_CUDA(ctx->in_luma.reserve(2 * slot));
+    ME_CUDA(ctx->in_alpha.reserve(2 * slot));
+    ME_CUDA(ctx->out_recs.reserve(size_t(cols) * rows * sizeof(me_block_rec)));
+    ME_CUDA(ctx->out_stats.reserve(sizeof(me_pair_stats)));
+    ME_CUDA(ctx->aux.reserve(size_t(cols) * rows * 8 + 256));
+    uint8_t* L = static_cast<uint8_t*>(ctx->in_luma.p);
+    uint8_t* A = static_cast<uint8_t*>(ctx->in_alpha.p);
+    // the batch layout expects frames back to back; pad-free when plane % 16 == 0
+    if (plane % 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "frame area must be a multiple of 16");
+    ME_CUDA(cudaMemcpyAsync(L, ref, plane, cudaMemcpyHostToDevice, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(L + plane, cur, plane, cudaMemcpyHostToDevice, ctx->stream));
+    const uint8_t* alpha_dev = nullptr;
+    if (cur_alpha) {
+        if (ref_alpha)
+            ME_CUDA(cudaMemcpyAsync(A, ref_alpha, plane, cudaMemcpyHostToDevice, ctx->stream));
+        else
+            ME_CUDA(cudaMemsetAsync(A, 0, plane, ctx->stream));
+        ME_CUDA(cudaMemcpyAsync(A + plane, cur_alpha, plane, cudaMemcpyHostToDevice, ctx->stream));
+        alpha_dev = A;
+        if (!ref_alpha && cfg->algo == ME_ALGO_PA) {
+            // brs_select throws on a boundary block without both planes
+            // (estimators.cpp:266-268): classify first, before any estimation.
+            uint8_t* types = static_cast<uint8_t*>(ctx->aux.p);
+            ME_CUDA(mek::classify_frame(A + plane, W, H, bs, types, ctx->stream));
+            std::vector<uint8_t> ht(size_t(cols) * rows);
+            ME_CUDA(cudaMemcpyAsync(ht.data(), types, ht.size(), cudaMemcpyDeviceToHost, ctx->stream));
+            if ((s = sync(ctx))) return s;
+            for (uint8_t t : ht)
+                if (t == ME_BOUNDARY)
+                    return me_fail(ME_ERR_INVALID_ARGUMENT, "boundary block requires both alpha planes");
+        }
+    }
+    int32_t* prev_dev = nullptr;
+    if (prev_mv) {
+        prev_dev = static_cast<int32_t*>(ctx->aux.p);
+        ME_CUDA(cudaMemcpyAsync(prev_dev, prev_mv, size_t(cols) * rows * 8, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    }
+    const mek::Batch b = make_batch(&c1, 1, 2, W, H, L, alpha_dev);
+    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+    ME_CUDA(mek::run_batch(b, c1, prev_dev, static_cast<me_block_rec*>(ctx->out_recs.p),
+                           static_cast<me_pair_stats*>(ctx->out_stats.p), nullptr, ctx->tasks.p,
+                           ctx->tasks.cap, ctx->num_sms, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(recs, ctx->out_recs.p, size_t(cols) * rows * sizeof(me_block_rec),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(stats, ctx->out_stats.p, sizeof(me_pair_stats), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
+me_status me_b200_block_search(me_ctx* ctx, int algo, int W, int H, const uint8_t* cur,
+                               const uint8_t* ref, int x0, int y0, int size, int range,
+                               int32_t out_mv[2], int64_t* out_cmp, uint32_t* out_cost_q4) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (algo < ME_ALGO_ES || algo > ME_ALGO_DS)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "not a block search");
+    if (range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (size != 8 && size != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
+    if ((s = check_rect(W, H, x0, y0, size))) return s;
+    if (!cur || !ref || !out_mv) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const uint8_t* host[2] = {cur, ref};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(256));
+    int64_t* out = static_cast<int64_t*>(ctx->aux.p);
+    ME_CUDA(mek::block_search(algo, dev[0], dev[1], W, H, x0, y0, size, range, out, ctx->stream));
+    int64_t h[4];
+    ME_CUDA(cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((s = sync(ctx))) return s;
+    out_mv[0] = int32_t(h[0]);
+    out_mv[1] = int32_t(h[1]);
+    if (out_cmp) *out_cmp = h[2];
+    if (out_cost_q4) *out_cost_q4 = uint32_t(h[3]);
+    return ok();
+}
+
+me_status me_b200_brs_select(me_ctx* ctx, int W, int H, const uint8_t* cur, const uint8_t* ref,
+                             const uint8_t* cur_alpha, const uint8_t* ref_alpha, int x0, int y0,
+                             int size, int btype, const int32_t cands[8], int range,
+                             int boundary_temporal, int32_t out_mv[2], uint8_t out_kinds[4],
+                             uint32_t out_scores_q4[4]) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    // cfg.validate(); require_inside; type checks (estimators.cpp:261-268)
+    if (range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (size != 8 && size != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
+    if ((s = check_rect(W, H, x0, y0, size))) return s;
+    if (btype == ME_TRANSPARENT)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "candidate selection on a transparent block");
+    if (btype == ME_BOUNDARY && (!cur_alpha || !ref_alpha))
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "boundary block requires both alpha planes");
+    if (!cur || !ref || !cands || !out_mv) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const uint8_t* host[4] = {cur, ref, btype == ME_BOUNDARY ? cur_alpha : nullptr,
+                              btype == ME_BOUNDARY ? ref_alpha : nullptr};
+    const uint8_t* dev[4];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 4))) return s;
+    ME_CUDA(ctx->aux.reserve(256));
+    int64_t* out = static_cast<int64_t*>(ctx->aux.p);
+    int32_t* cd = reinterpret_cast<int32_t*>(out + 16);
+    ME_CUDA(cudaMemcpyAsync(cd, cands, 8 * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    ME_CUDA(mek::brs_single(dev[0], dev[1], dev[2], dev[3], W, H, x0, y0, size, btype, cd, range,
+                            boundary_temporal, out, ctx->stream));
+    int64_t h[10];
+    ME_CUDA(cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((s = sync(ctx))) return s;
+    out_mv[0] = int32_t(h[0]);
+    out_mv[1] = int32_t(h[1]);
+    for (int i = 0; i < 4; ++i) {
+        if (out_scores_q4) out_scores_q4[i] = uint32_t(h[2 + i]);
+        if (out_kinds) out_kinds[i] = uint8_t(h[6 + i]);
+    }
+    return ok();
+}
+
+me_status me_b200_prs_refine(me_ctx* ctx, int W, int H, const uint8_t* cur, const uint8_t* ref,
+                             int x0, int y0, int size, const int32_t d0[2], int range,
+                             double epsilon, double theta, int max_iterations, int step,
+                             int32_t out_mv[2], int64_t* out_dpd, uint32_t* log_q4, int* log_len) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (size != 8 && size != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
+    if (!(epsilon > 0.0)) return me_fail(ME_ERR_INVALID_ARGUMENT, "epsilon must be > 0");
+    if (!(theta > 0.0)) return me_fail(ME_ERR_INVALID_ARGUMENT, "theta must be > 0");
+    if (max_iterations < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "max_iterations must be >= 1");
+    if (step != 1 && step != 2) return me_fail(ME_ERR_INVALID_ARGUMENT, "step must be 1 or 2 half-pels");
+    if ((s = check_rect(W, H, x0, y0, size))) return s;
+    if (!cur || !ref || !d0 || !out_mv) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const uint8_t* host[2] = {cur, ref};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(128 * 8));
+    int64_t* out = static_cast<int64_t*>(ctx->aux.p);
+    ME_CUDA(mek::prs_single(dev[0], dev[1], W, H, x0, y0, size, d0[0], d0[1], range, epsilon, theta,
+                            max_iterations, step, out, ctx->stream));
+    int64_t h[69];
+    ME_CUDA(cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((s = sync(ctx))) return s;
+    out_mv[0] = int32_t(h[0]);
+    out_mv[1] = int32_t(h[1]);
+    if (out_dpd) *out_dpd = h[2];
+    const int n = int(h[3]) + 1;
+    if (log_len) *log_len = n;
+    if (log_q4)
+        for (int i = 0; i < n && i < 64; ++i) log_q4[i] = uint32_t(h[5 + i]);
+    return ok();
+}
+
+me_status me_b200_sad_texture(me_ctx* ctx, int W, int H, const uint8_t* cur, const uint8_t* ref,
+                              int x0, int y0, int size, int dx, int dy, uint32_t* out_sad_q4) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = check_rect(W, H, x0, y0, size))) return s;
+    if (size > 64) return me_fail(ME_ERR_INVALID_ARGUMENT, "block size above 64");
+    if (!cur || !ref || !out_sad_q4) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const uint8_t* host[2] = {cur, ref};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(256));
+    int64_t* out = static_cast<int64_t*>(ctx->aux.p);
+    ME_CUDA(mek::sad_texture_single(dev[0], dev[1], W, H, x0, y0, size, dx, dy, out, ctx->stream));
+    int64_t h;
+    ME_CUDA(cudaMemcpyAsync(&h, out, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((s = sync(ctx))) return s;
+    *out_sad_q4 = uint32_t(h);
+    return ok();
+}
+
+me_status me_b200_sad_shape(me_ctx* ctx, int W, int H, const uint8_t* cur_alpha,
+                            const uint8_t* ref_alpha, int x0, int y0, int size, int dx, int dy,
+                            int64_t* out_sad) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((dx & 1) || (dy & 1))  // metrics.cpp:67-68
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "shape SAD requires an integer-pel vector");
+    if ((s = check_rect(W, H, x0, y0, size))) return s;
+    if (size > 64) return me_fail(ME_ERR_INVALID_ARGUMENT, "block size above 64");
+    if (!cur_alpha || !ref_alpha || !out_sad) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const uint8_t* host[2] = {cur_alpha, ref_alpha};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(256));
+    int64_t* out = static_cast<int64_t*>(ctx->aux.p);
+    ME_CUDA(mek::sad_shape_single(dev[0], dev[1], W, H, x0, y0, size, dx, dy, out, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(out_sad, out, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
+me_status me_b200_classify_blocks(me_ctx* ctx, int W, int H, const uint8_t* alpha, int bs,
+                                  uint8_t* types) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (bs <= 0 || W <= 0 || H <= 0 || W % bs || H % bs)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "block size does not divide the frame");
+    if (bs % 4 || W % 4) return me_fail(ME_ERR_INVALID_ARGUMENT, "block size must be a multiple of 4");
+    if (!types) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const size_t n = size_t(W / bs) * (H / bs);
+    if (!alpha) {
+        std::memset(types, ME_OPAQUE, n);  // classify_block(nullptr) == Opaque (frame.cpp:82)
+        return ok();
+    }
+    const uint8_t* host[1] = {alpha};
+    const uint8_t* dev[1];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 1))) return s;
+    ME_CUDA(ctx->aux.reserve(n + 256));
+    ME_CUDA(mek::classify_frame(dev[0], W, H, bs, static_cast<uint8_t*>(ctx->aux.p), ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(types, ctx->aux.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
+me_status me_b200_binarize(me_ctx* ctx, int W, int H, const uint8_t* gray, int threshold,
+                           uint8_t* out) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (W < 0 || H < 0 || !gray || !out) return me_fail(ME_ERR_INVALID_ARGUMENT, "bad arguments");
+    const size_t n = size_t(W) * H;
+    if (n == 0) return ok();
+    const uint8_t* host[1] = {gray};
+    const uint8_t* dev[1];
+    if ((s = stage_planes(ctx, n, host, dev, 1))) return s;
+    ME_CUDA(ctx->aux.reserve(n + 256));
+    ME_CUDA(mek::binarize(dev[0], int(n), threshold, static_cast<uint8_t*>(ctx->aux.p), ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(out, ctx->aux.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
+me_status me_b200_predict_frame(me_ctx* ctx, int W, int H, const uint8_t* ref, const int32_t* mv,
+                                const uint8_t* types, int bs, const uint8_t* cur, uint8_t* pred,
+                                int64_t* out_sse) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (bs != 8 && bs != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
+    if (W <= 0 || H <= 0 || W % bs || H % bs)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "motion field grid does not cover the frame");
+    if (!ref || !mv) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    const size_t plane = size_t(W) * H;
+    const size_t nb = size_t(W / bs) * (H / bs);
+    const uint8_t* host[2] = {ref, cur};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, plane, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(nb * 9 + sizeof(me_pair_stats) + 512));
+    uint8_t* aux = static_cast<uint8_t*>(ctx->aux.p);
+    me_pair_stats* st = reinterpret_cast<me_pair_stats*>(aux);
+    int32_t* mv_dev = reinterpret_cast<int32_t*>(aux + 256);
+    uint8_t* types_dev = types ? aux + 256 + nb * 8 : nullptr;
+    ME_CUDA(cudaMemsetAsync(st, 0, sizeof(me_pair_stats), ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(mv_dev, mv, nb * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (types) ME_CUDA(cudaMemcpyAsync(types_dev, types, nb, cudaMemcpyHostToDevice, ctx->stream));
+    ME_CUDA(ctx->out_pred.reserve(plane + 256));
+    ME_CUDA(mek::predict(dev[0], dev[1], mv_dev, types_dev, W, H, bs,
+                         static_cast<uint8_t*>(ctx->out_pred.p), st, ctx->stream));
+    if (pred)
+        ME_CUDA(cudaMemcpyAsync(pred, ctx->out_pred.p, plane, cudaMemcpyDeviceToHost, ctx->stream));
+    me_pair_stats hs;
+    ME_CUDA(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((s = sync(ctx))) return s;
+    if (out_sse) *out_sse = cur ? hs.sse : 0;
+    return ok();
+}
+
+me_status me_b200_sse(me_ctx* ctx, int W, int H, const uint8_t* a, const uint8_t* b,
+                      int64_t* out_sse) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (W <= 0 || H <= 0 || !a || !b || !out_sse)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "bad arguments");
+    const size_t n = size_t(W) * H;
+    const uint8_t* host[2] = {a, b};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, n, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(256));
+    unsigned long long* out = static_cast<unsigned long long*>(ctx->aux.p);
+    ME_CUDA(cudaMemsetAsync(out, 0, 8, ctx->stream));
+    ME_CUDA(mek::sse(dev[0], dev[1], int(n), out, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(out_sse, out, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
+}  // extern "C"

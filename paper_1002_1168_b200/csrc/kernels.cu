@@ -1,0 +1,1517 @@
+// kernels.cu — sm_100a kernels of the shape-adaptive motion-estimation hot path.
+//
+// Reference path (paths relative to /root/reference/proj):
+//   classify_block      frame.cpp:81-104          -> classify_kernel
+//   full_search         estimators.cpp:167-187    -> es_kernel (CTA per block, window in smem)
+//   tss/fss/ds_search   estimators.cpp:189-236    -> ring_kernel (warp per block)
+//   gather/brs/prs      estimators.cpp:238-382    -> pa_kernel (dataflow wavefront, warp per block)
+//   estimate_field      estimators.cpp:384-440    -> run_batch (the whole pipeline)
+//   predict_frame, psnr compensation.cpp:30-71, metrics.cpp:108-124 -> mc_kernel (fused SSE)
+//
+// Integer arithmetic throughout except the PRS direction, which is computed in
+// IEEE double with explicit round-to-nearest intrinsics (no contraction) in the
+// reference's sequential raster order, and only when two or more neighbours
+// tie for the minimum (the only case in which it affects the result).
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace mek {
+
+// ---------------------------------------------------------------------------
+// Small device helpers
+// ---------------------------------------------------------------------------
+
+constexpr uint32_t kSentinel = 0x80008000u;  // MV word of a block not yet estimated
+constexpr uint32_t kInf = 0xFFFFFFFFu;
+constexpr uint32_t kBoundaryBit = 0x80000000u;
+
+// kOff8 (estimators.cpp:33-35): {dx, dy}, raster order of (dy, dx)
+__constant__ int c_off8[8][2] = {{-1, -1}, {0, -1}, {1, -1}, {-1, 0}, {1, 0}, {-1, 1}, {0, 1}, {1, 1}};
+// kLdsp / kSdsp (estimators.cpp:222-225)
+__constant__ int c_ldsp[8][2] = {{0, -2}, {-1, -1}, {1, -1}, {-2, 0}, {2, 0}, {-1, 1}, {1, 1}, {0, 2}};
+__constant__ int c_sdsp[4][2] = {{0, -1}, {-1, 0}, {1, 0}, {0, 1}};
+
+// d = sum over the 4 byte lanes of |a - b|, plus c  (one VABSDIFF4.U8.ACC)
+__device__ __forceinline__ uint32_t vad4(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t ldg32(const uint8_t* p) {
+    return __ldg(reinterpret_cast<const uint32_t*>(p));
+}
+
+// 8 bytes at an arbitrary address (read-only data).  The third aligned word is
+// loaded only when the span crosses into it, so no byte past p+7's word is read.
+__device__ __forceinline__ void ld8u(const uint8_t* p, uint32_t& r0, uint32_t& r1) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = uint32_t(a & 3) * 8;
+    const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1);
+    const uint32_t w2 = sh ? __ldg(w + 2) : 0u;
+    r0 = __funnelshift_r(w0, w1, sh);
+    r1 = __funnelshift_r(w1, w2, sh);
+}
+
+__device__ __forceinline__ void ld16u(const uint8_t* p, uint32_t r[4]) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = uint32_t(a & 3) * 8;
+    uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
+    const uint32_t w4 = sh ? __ldg(w + 4) : 0u;
+    r[0] = __funnelshift_r(w0, w1, sh);
+    r[1] = __funnelshift_r(w1, w2, sh);
+    r[2] = __funnelshift_r(w2, w3, sh);
+    r[3] = __funnelshift_r(w3, w4, sh);
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// sample_clamped (frame.cpp:58-62)
+__device__ __forceinline__ int pxc(const uint8_t* f, int W, int H, int x, int y) {
+    return f[size_t(clampi(y, 0, H - 1)) * W + clampi(x, 0, W - 1)];
+}
+
+// 4 x sample_halfpel (frame.cpp:64-79): the bilinear weights are 0 or 1/2, so
+// four times the sample is an exact integer.
+__device__ __forceinline__ int interp4(const uint8_t* f, int W, int H, int x2, int y2) {
+    const int xi = x2 >> 1, yi = y2 >> 1, fx = x2 & 1, fy = y2 & 1;
+    const int p00 = pxc(f, W, H, xi, yi);
+    if (!fx && !fy) return 4 * p00;
+    if (fx && !fy) return 2 * (p00 + pxc(f, W, H, xi + 1, yi));
+    if (!fx) return 2 * (p00 + pxc(f, W, H, xi, yi + 1));
+    return p00 + pxc(f, W, H, xi + 1, yi) + pxc(f, W, H, xi, yi + 1) + pxc(f, W, H, xi + 1, yi + 1);
+}
+
+// Half-pel window (estimators.cpp:41-48), half-pel units.
+struct Win {
+    int lo_x, hi_x, lo_y, hi_y;
+};
+__device__ __forceinline__ Win hp_window(int x0, int y0, int bs, int W, int H, int S) {
+    Win w;
+    w.lo_x = max(-2 * S, -2 * x0);
+    w.hi_x = min(2 * S, 2 * (W - x0 - bs));
+    w.lo_y = max(-2 * S, -2 * y0);
+    w.hi_y = min(2 * S, 2 * (H - y0 - bs));
+    return w;
+}
+
+// 4 x texture SAD of one block row (sad_texture, metrics.cpp:43-63).  Full-pel
+// vectors whose displaced row lies inside the frame use VABSDIFF4 on unaligned
+// loads; everything else goes through the exact clamped/half-pel path.
+__device__ __forceinline__ uint32_t row_sad4(const uint8_t* cur, const uint8_t* ref, int W, int H,
+                                             int x0, int y, int bs, int dx2, int dy2) {
+    if (((dx2 | dy2) & 1) == 0) {
+        const int sx = x0 + (dx2 >> 1), sy = y + (dy2 >> 1);
+        if (sx >= 0 && sx + bs <= W && sy >= 0 && sy < H && ((x0 | W) & 3) == 0) {
+            const uint8_t* c = cur + size_t(y) * W + x0;
+            const uint8_t* r = ref + size_t(sy) * W + sx;
+            uint32_t acc = 0;
+            if (bs == 8) {
+                uint32_t r0, r1;
+                ld8u(r, r0, r1);
+                acc = vad4(ldg32(c), r0, acc);
+                acc = vad4(ldg32(c + 4), r1, acc);
+            } else {
+                uint32_t rr[4];
+                ld16u(r, rr);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc = vad4(ldg32(c + 4 * i), rr[i], acc);
+            }
+            return acc * 4u;
+        }
+    }
+    uint32_t acc = 0;
+    for (int x = x0; x < x0 + bs; ++x) {
+        const int d = 4 * int(cur[size_t(y) * W + x]) - interp4(ref, W, H, 2 * x + dx2, 2 * y + dy2);
+        acc += uint32_t(d < 0 ? -d : d);
+    }
+    return acc;
+}
+
+// Mismatching alpha samples of one block row (sad_shape, metrics.cpp:65-84),
+// full-pel pel displacement (fx, fy).  __vcmpne4 marks each differing byte
+// with 0xFF, so popc/8 counts mismatches exactly for any byte values.
+__device__ __forceinline__ uint32_t row_shape(const uint8_t* ca, const uint8_t* ra, int W, int H,
+                                              int x0, int y, int bs, int fx, int fy) {
+    const int sx = x0 + fx, sy = y + fy;
+    if (sx >= 0 && sx + bs <= W && sy >= 0 && sy < H && ((x0 | W) & 3) == 0) {
+        const uint8_t* c = ca + size_t(y) * W + x0;
+        const uint8_t* r = ra + size_t(sy) * W + sx;
+        uint32_t bits = 0;
+        if (bs == 8) {
+            uint32_t r0, r1;
+            ld8u(r, r0, r1);
+            bits = __popc(__vcmpne4(ldg32(c), r0)) + __popc(__vcmpne4(ldg32(c + 4), r1));
+        } else {
+            uint32_t rr[4];
+            ld16u(r, rr);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) bits += __popc(__vcmpne4(ldg32(c + 4 * i), rr[i]));
+        }
+        return bits >> 3;
+    }
+    uint32_t m = 0;
+    const int ry = clampi(sy, 0, H - 1);
+    for (int x = x0; x < x0 + bs; ++x)
+        m += ca[size_t(y) * W + x] != ra[size_t(ry) * W + clampi(x + fx, 0, W - 1)];
+    return m;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_mv(int dx, int dy) {
+    return (uint32_t(uint16_t(int16_t(dx)))) | (uint32_t(uint16_t(int16_t(dy))) << 16);
+}
+__device__ __forceinline__ int mv_dx(uint32_t w) { return int(int16_t(uint16_t(w & 0xFFFF))); }
+__device__ __forceinline__ int mv_dy(uint32_t w) { return int(int16_t(uint16_t(w >> 16))); }
+
+__device__ __forceinline__ void write_rec(me_block_rec* r, int dx, int dy, uint32_t cost_q4,
+                                          uint32_t cmp, uint32_t dpd, uint32_t iters,
+                                          uint32_t type, bool release) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(r);
+    w[1] = cost_q4;
+    w[2] = (cmp & 0xFFFF) | (dpd << 16);
+    w[3] = (iters & 0xFF) | ((type & 0xFF) << 8);
+    if (release)
+        st_release(w, pack_mv(dx, dy));
+    else
+        w[0] = pack_mv(dx, dy);
+}
+
+// ---------------------------------------------------------------------------
+// classify_kernel: classify_block (frame.cpp:81-104) on every block of every
+// pair's CURRENT alpha plane (estimators.cpp:411), initialise its record
+// (transparent: final all-zero record; estimated: MV = sentinel) and build the
+// histogram of estimated blocks over the sort key (PA: wavefront step
+// t = h + 2v + p; baselines: a single bin).
+// ---------------------------------------------------------------------------
+
+struct ClassArgs {
+    Batch b;
+    int pa;              // key = wavefront step when 1
+    me_block_rec* recs;  // [n_seq][pairs][rows][cols]
+    uint8_t* types;      // same indexing
+    int* hist;           // [nbins]
+    int nbins;
+};
+
+__device__ __forceinline__ int classify_one(const uint8_t* a, int W, int x0, int y0, int bs) {
+    if (!a) return ME_OPAQUE;
+    uint32_t any = 0, nz = 1;
+    for (int y = 0; y < bs; ++y) {
+        const uint8_t* row = a + size_t(y0 + y) * W + x0;
+        for (int i = 0; i < bs; i += 4) {
+            const uint32_t w = ldg32(row + i);
+            any |= w;
+            nz &= __vcmpeq4(w, 0u) == 0u;
+        }
+    }
+    return !any ? ME_TRANSPARENT : (nz ? ME_OPAQUE : ME_BOUNDARY);
+}
+
+__global__ void classify_kernel(ClassArgs a) {
+    extern __shared__ int s_hist[];
+    const Batch& b = a.b;
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const int64_t n = b.nblocks();
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+         g += int64_t(gridDim.x) * blockDim.x) {
+        const int h = int(g % b.cols);
+        int64_t t = g / b.cols;
+        const int v = int(t % b.rows);
+        t /= b.rows;
+        const int p = int(t % b.pairs);
+        const int seq = int(t / b.pairs);
+        const size_t plane = size_t(b.W) * b.H;
+        const uint8_t* a_cur =
+            b.alpha ? b.alpha + (size_t(seq) * b.F + p + b.d) * plane : nullptr;
+        const int ty = classify_one(a_cur, b.W, h * b.bs, v * b.bs, b.bs);
+        a.types[g] = uint8_t(ty);
+        uint4 r;
+        r.x = ty == ME_TRANSPARENT ? 0u : kSentinel;
+        r.y = 0u;
+        r.z = 0u;
+        r.w = uint32_t(ty) << 8;
+        *reinterpret_cast<uint4*>(a.recs + g) = r;
+        if (ty != ME_TRANSPARENT) atomicAdd(&s_hist[a.pa ? h + 2 * v + p : 0], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
+}
+
+// Exclusive scan of hist into offs[0..nbins] (single CTA), cursor = offs.
+__global__ void scan_kernel(const int* hist, int nbins, int* offs, int* cursor) {
+    __shared__ int s_part[1024];
+    const int T = blockDim.x;
+    const int per = (nbins + T - 1) / T;
+    const int lo = threadIdx.x * per, hi = min(lo + per, nbins);
+    int sum = 0;
+    for (int i = lo; i < hi; ++i) sum += hist[i];
+    s_part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int i = 0; i < T; ++i) {
+            const int v = s_part[i];
+            s_part[i] = acc;
+            acc += v;
+        }
+        offs[nbins] = acc;
+    }
+    __syncthreads();
+    int acc = s_part[threadIdx.x];
+    for (int i = lo; i < hi; ++i) {
+        offs[i] = acc;
+        cursor[i] = acc;
+        acc += hist[i];
+    }
+}
+
+// Scatter estimated block ids into key order (per-CTA ranges per bin keep the
+// global atomics to one per (CTA, bin)).
+__global__ void fill_kernel(ClassArgs a, int* cursor, uint32_t* list) {
+    extern __shared__ int s_cnt[];  // [nbins] counts, then [nbins] bases
+    int* s_base = s_cnt + a.nbins;
+    const Batch& b = a.b;
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    const int64_t n = b.nblocks();
+    const int64_t chunk = int64_t(blockDim.x) * 8;
+    const int64_t g0 = int64_t(blockIdx.x) * chunk;
+    for (int64_t g = g0 + threadIdx.x; g < min(g0 + chunk, n); g += blockDim.x) {
+        const int ty = a.types[g];
+        if (ty == ME_TRANSPARENT) continue;
+        int key = 0;
+        if (a.pa) {
+            const int h = int(g % b.cols);
+            int64_t t = g / b.cols;
+            const int v = int(t % b.rows);
+            const int p = int((t / b.rows) % b.pairs);
+            key = h + 2 * v + p;
+        }
+        atomicAdd(&s_cnt[key], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
+        s_base[i] = s_cnt[i] ? atomicAdd(&cursor[i], s_cnt[i]) : 0;
+        s_cnt[i] = 0;
+    }
+    __syncthreads();
+    for (int64_t g = g0 + threadIdx.x; g < min(g0 + chunk, n); g += blockDim.x) {
+        const int ty = a.types[g];
+        if (ty == ME_TRANSPARENT) continue;
+        int key = 0;
+        if (a.pa) {
+            const int h = int(g % b.cols);
+            int64_t t = g / b.cols;
+            const int v = int(t % b.rows);
+            const int p = int((t / b.rows) % b.pairs);
+            key = h + 2 * v + p;
+        }
+        const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
+        list[pos] = uint32_t(g) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// es_kernel: full_search (estimators.cpp:167-187).  One CTA per estimated
+// block (persistent CTAs pull blocks from the work list).  The reference
+// window (clipped, pel units, estimators.cpp:62-65) is staged in shared memory
+// as 4 copies pre-shifted by 0..3 bytes so every candidate row is read as
+// aligned 32-bit words; the current block lives in registers.  A thread owns
+// one dx column and a run of K consecutive dy: each staged reference row is
+// loaded once and reused for every accumulator whose current row it pairs
+// with.  The winner is the minimum packed key (SAD, |dx|+|dy|, raster index)
+// — exactly the reference's strict-< scan with the Manhattan tie-break.
+// ---------------------------------------------------------------------------
+
+struct EsArgs {
+    Batch b;
+    int S;
+    const uint32_t* list;
+    const int* nlist;  // device count (offs[nbins])
+    int* counter;
+    me_block_rec* recs;
+    int band_rows_max;  // staged rows per band (multiple of K, + BS - 1 added on top)
+};
+
+constexpr int kEsThreads = 256;
+
+__device__ __forceinline__ void decode_block(const Batch& b, uint32_t g, int& h, int& v, int& p,
+                                             int& seq) {
+    h = int(g % uint32_t(b.cols));
+    uint32_t t = g / uint32_t(b.cols);
+    v = int(t % uint32_t(b.rows));
+    t /= uint32_t(b.rows);
+    p = int(t % uint32_t(b.pairs));
+    seq = int(t / uint32_t(b.pairs));
+}
+
+template <int BS, int K>
+__device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                         int S, int band_runs_max, uint32_t* sm, unsigned long long* s_best,
+                         int& out_dx, int& out_dy, uint32_t& out_sad, uint32_t& out_cmp) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int lo_x = max(-S, -x0), hi_x = min(S, W - x0 - BS);
+    const int lo_y = max(-S, -y0), hi_y = min(S, H - y0 - BS);
+    const int WX = hi_x - lo_x + 1, WY = hi_y - lo_y + 1;
+    const int nruns = (WY + K - 1) / K;
+    const int rowbytes = WX + BS - 1;
+    const int PW = ((WX - 1) >> 2) + (BS >> 2) + 1;  // words per staged row
+    constexpr int NW = BS / 4;
+
+    uint32_t c[BS][NW];
+    if (((x0 | W) & 3) == 0) {
+#pragma unroll
+        for (int r = 0; r < BS; ++r)
+#pragma unroll
+            for (int i = 0; i < NW; ++i) c[r][i] = ldg32(cur + size_t(y0 + r) * W + x0 + 4 * i);
+    } else {
+#pragma unroll
+        for (int r = 0; r < BS; ++r)
+#pragma unroll
+            for (int i = 0; i < NW; ++i) {
+                const uint8_t* q = cur + size_t(y0 + r) * W + x0 + 4 * i;
+                c[r][i] = uint32_t(q[0]) | (uint32_t(q[1]) << 8) | (uint32_t(q[2]) << 16) |
+                          (uint32_t(q[3]) << 24);
+            }
+    }
+
+    unsigned long long best = ~0ull;
+    for (int run0 = 0; run0 < nruns; run0 += band_runs_max) {
+        const int bruns = min(band_runs_max, nruns - run0);
+        const int srows = bruns * K + BS - 1;
+        int CW = srows * PW;
+        CW += ((8 - (CW & 31)) + 32) & 31;  // copy stride = 8 (mod 32) words: conflict-free lanes
+        const int row_g0 = y0 + lo_y + run0 * K;  // frame row of staged row 0
+        const int rows_valid = min(srows, WY + BS - 1 - run0 * K);
+        const uint8_t* rb = ref + size_t(row_g0) * W + (x0 + lo_x);
+        __syncthreads();  // previous band / block done with smem
+        for (int idx = tid; idx < srows * PW; idx += blockDim.x) {
+            const int row = idx / PW, q = idx - row * PW;
+            uint32_t bytes[7];
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int col = 4 * q + k;
+                bytes[k] = (row < rows_valid && col < rowbytes) ? rb[size_t(row) * W + col] : 0u;
+            }
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+                sm[s * CW + idx] = bytes[s] | (bytes[s + 1] << 8) | (bytes[s + 2] << 16) |
+                                   (bytes[s + 3] << 24);
+        }
+        __syncthreads();
+        const int ntask = WX * bruns;
+        for (int task = tid; task < ntask; task += blockDim.x) {
+            const int run = task / WX, col = task - run * WX;
+            const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
+            uint32_t acc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = 0;
+#pragma unroll
+            for (int j = 0; j < K + BS - 1; ++j) {
+                uint32_t w[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) w[i] = base[j * PW + i];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int r = j - k;
+                    if (r >= 0 && r < BS) {
+#pragma unroll
+                        for (int i = 0; i < NW; ++i) acc[k] = vad4(c[r][i], w[i], acc[k]);
+                    }
+                }
+            }
+            const int dx = lo_x + col;
+            const int ady = (run0 + run) * K;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int wy = ady + k;  // window row index
+                if (wy < WY) {
+                    const int dy = lo_y + wy;
+                    const unsigned long long key =
+                        (static_cast<unsigned long long>(acc[k]) << 40) |
+                        (static_cast<unsigned long long>(abs(dx) + abs(dy)) << 24) |
+                        static_cast<unsigned long long>(wy * WX + col);
+                    best = key < best ? key : best;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+        best = other < best ? other : best;
+    }
+    if (lane == 0) s_best[wid] = best;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long m = s_best[0];
+        for (int i = 1; i < int(blockDim.x >> 5); ++i) m = s_best[i] < m ? s_best[i] : m;
+        const int raster = int(m & 0xFFFFFF);
+        out_dx = lo_x + raster % WX;
+        out_dy = lo_y + raster / WX;
+        out_sad = uint32_t(m >> 40);
+        out_cmp = uint32_t(WX * WY);
+    }
+}
+
+template <int BS, int K>
+__global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ unsigned long long s_best[kEsThreads / 32];
+    __shared__ int s_item;
+    const Batch& b = a.b;
+    const int n = *a.nlist;
+    const size_t plane = size_t(b.W) * b.H;
+    const int band_runs = a.band_rows_max / K;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= n) return;
+        const uint32_t e = a.list[item];
+        const uint32_t g = e & ~kBoundaryBit;
+        int h, v, p, seq;
+        decode_block(b, g, h, v, p, seq);
+        const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
+        const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
+        int dx, dy;
+        uint32_t sad, cmp;
+        es_block<BS, K>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, s_best, dx, dy,
+                        sad, cmp);
+        if (threadIdx.x == 0)
+            write_rec(a.recs + g, 2 * dx, 2 * dy, sad * 4u, cmp, 0, 0,
+                      (e & kBoundaryBit) ? ME_BOUNDARY : ME_OPAQUE, false);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ring_kernel: tss_search / fss_search / ds_search (estimators.cpp:189-236).
+// One warp per block.  Each ring's (up to 8) admissible positions are scored
+// in parallel: 4 lanes per position, BS/4 rows per lane, reduced by shuffles.
+// A per-warp bitmap over the clipped window counts unique evaluations
+// (BlockMatcher::eval's cache, estimators.cpp:72-81); revisits are recomputed,
+// not recounted.
+// ---------------------------------------------------------------------------
+
+struct RingCtx {
+    const uint8_t *cur, *ref;
+    int W, H, x0, y0, bs;
+    int lo_x, hi_x, lo_y, hi_y;  // pel window
+    uint32_t* bitmap;            // per-warp
+    uint32_t count;
+};
+
+// Scores the n (<= 8) positions (cx, cy) + offs[k] * radius (pel); lanes
+// 4k..4k+3 own position k and return its SAD; bit 4k of adm_mask is set for
+// admissible positions.  radius 0 scores the center itself.
+__device__ __forceinline__ uint32_t ring_eval(RingCtx& c, const int (*offs)[2], int n, int radius,
+                                              int cx, int cy, int lane, uint32_t& adm_mask) {
+    const int k = lane >> 2;
+    const int dx = k < n ? cx + offs[k][0] * radius : 0;
+    const int dy = k < n ? cy + offs[k][1] * radius : 0;
+    const bool adm = k < n && dx >= c.lo_x && dx <= c.hi_x && dy >= c.lo_y && dy <= c.hi_y;
+    uint32_t s = 0;
+    if (adm)
+        for (int r = (lane & 3); r < c.bs; r += 4)
+            s += row_sad4(c.cur, c.ref, c.W, c.H, c.x0, c.y0 + r, c.bs, 2 * dx, 2 * dy);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+    s >>= 2;
+    // unique-evaluation counting
+    const int WX = c.hi_x - c.lo_x + 1;
+    bool fresh = false;
+    if (adm && (lane & 3) == 0) {
+        const int bit = (dy - c.lo_y) * WX + (dx - c.lo_x);
+        const uint32_t m = 1u << (bit & 31);
+        fresh = (atomicOr(&c.bitmap[bit >> 5], m) & m) == 0;
+    }
+    c.count += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
+    adm_mask = __ballot_sync(0xFFFFFFFFu, adm && (lane & 3) == 0);
+    return s;
+}
+
+// probe_ring (estimators.cpp:85-102): strict improvement in listed order.
+__device__ __forceinline__ void probe_ring(RingCtx& c, const int (*offs)[2], int n, int radius,
+                                           int& cx, int& cy, uint32_t& best, int lane) {
+    uint32_t adm;
+    const uint32_t s = ring_eval(c, offs, n, radius, cx, cy, lane, adm);
+    int bx = cx, by = cy;
+    for (int i = 0; i < n; ++i) {
+        const uint32_t v = __shfl_sync(0xFFFFFFFFu, s, 4 * i);
+        if (((adm >> (4 * i)) & 1u) && v < best) {
+            best = v;
+            bx = cx + offs[i][0] * radius;
+            by = cy + offs[i][1] * radius;
+        }
+    }
+    cx = bx;
+    cy = by;
+}
+
+__device__ void ring_block(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H, int x0,
+                           int y0, int bs, int S, uint32_t* bitmap, int lane, int& out_dx,
+                           int& out_dy, uint32_t& out_sad, uint32_t& out_cmp) {
+    RingCtx c;
+    c.cur = cur;
+    c.ref = ref;
+    c.W = W;
+    c.H = H;
+    c.x0 = x0;
+    c.y0 = y0;
+    c.bs = bs;
+    c.lo_x = max(-S, -x0);
+    c.hi_x = min(S, W - x0 - bs);
+    c.lo_y = max(-S, -y0);
+    c.hi_y = min(S, H - y0 - bs);
+    c.bitmap = bitmap;
+    c.count = 0;
+    const int words = ((c.hi_x - c.lo_x + 1) * (c.hi_y - c.lo_y + 1) + 31) >> 5;
+    for (int i = lane; i < words; i += 32) bitmap[i] = 0;
+    __syncwarp();
+    int cx = 0, cy = 0;
+    uint32_t best;
+    {
+        uint32_t adm;
+        const uint32_t s = ring_eval(c, c_off8, 1, 0, 0, 0, lane, adm);  // the center, once
+        best = __shfl_sync(0xFFFFFFFFu, s, 0);
+    }
+    if (algo == ME_ALGO_TSS) {
+        int step = 1;
+        while (step * 2 <= S) step *= 2;
+        for (; step >= 1; step /= 2) probe_ring(c, c_off8, 8, step, cx, cy, best, lane);
+    } else if (algo == ME_ALGO_FSS) {
+        for (int round = 0; round < 3; ++round) {
+            const int px0 = cx, py0 = cy;
+            probe_ring(c, c_off8, 8, 2, cx, cy, best, lane);
+            if (cx == px0 && cy == py0) break;
+        }
+        probe_ring(c, c_off8, 8, 1, cx, cy, best, lane);
+    } else {
+        for (;;) {
+            const int px0 = cx, py0 = cy;
+            probe_ring(c, c_ldsp, 8, 1, cx, cy, best, lane);
+            if (cx == px0 && cy == py0) break;
+        }
+        probe_ring(c, c_sdsp, 4, 1, cx, cy, best, lane);
+    }
+    out_dx = cx;
+    out_dy = cy;
+    out_sad = best;
+    out_cmp = c.count;
+}
+
+struct RingArgs {
+    Batch b;
+    int algo, S;
+    const uint32_t* list;
+    const int* nlist;
+    me_block_rec* recs;
+    int bitmap_words;  // per warp
+};
+
+__global__ void __launch_bounds__(256) ring_kernel(RingArgs a) {
+    extern __shared__ uint32_t s_bits[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* bitmap = s_bits + wid * a.bitmap_words;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int n = *a.nlist;
+    const Batch& b = a.b;
+    const size_t plane = size_t(b.W) * b.H;
+    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+        const uint32_t e = a.list[item];
+        const uint32_t g = e & ~kBoundaryBit;
+        int h, v, p, seq;
+        decode_block(b, g, h, v, p, seq);
+        const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
+        const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
+        int dx, dy;
+        uint32_t sad, cmp;
+        ring_block(a.algo, cur, ref, b.W, b.H, h * b.bs, v * b.bs, b.bs, a.S, bitmap, lane, dx, dy,
+                   sad, cmp);
+        if (lane == 0)
+            write_rec(a.recs + g, 2 * dx, 2 * dy, sad * 4u, cmp, 0, 0,
+                      (e & kBoundaryBit) ? ME_BOUNDARY : ME_OPAQUE, false);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// PA: gather_candidates + brs_select + prs_refine (estimators.cpp:238-382) as
+// a dataflow wavefront.  Block (h, v) of pair p depends only on A = (h-1, v),
+// B = (h, v-1), C = (h+1, v-1) of pair p and T = (h, v) of pair p-1
+// (bench.cpp:204 threads the previous pair's field), so every block with the
+// same t = h + 2v + p is independent (a plain h + v diagonal is NOT: C lies on
+// it).  The work list is sorted by t; persistent warps take list entries
+// round-robin and spin (acquire loads) on their four dependencies' MV words,
+// which hold a sentinel until the producing warp's release store.  Every
+// dependency sits earlier in the list, so the smallest unfinished entry can
+// always proceed: no grid-wide barrier, no deadlock.
+// ---------------------------------------------------------------------------
+
+struct PaParams {
+    int W, H, bs, S;
+    int max_iter, step, bt_shape;
+    double eps, theta;
+    int bm_side, bm_words;  // PRS visited bitmap (lattice side, words per warp)
+};
+
+// Per-warp block context.
+struct PaBlock {
+    const uint8_t *cur, *ref, *ca, *ra;
+    int x0, y0;
+    Win w;
+};
+
+// Scores 4 candidate slots (lanes 8k..8k+7 own slot k): texture (4 x SAD at a
+// half-pel vector) or shape (4 x 255 x mismatches at the llround-snapped pel
+// vector, estimators.cpp:284-286).  Result broadcast in each 8-lane group.
+__device__ __forceinline__ uint32_t score4(const PaParams& P, const PaBlock& B, int lane,
+                                           int dx2, int dy2, bool shape) {
+    uint32_t s = 0;
+    if (shape) {
+        // llround(h / 2) == (h + sign(h)) / 2 with C truncation
+        const int fx = (dx2 + (dx2 > 0) - (dx2 < 0)) / 2;
+        const int fy = (dy2 + (dy2 > 0) - (dy2 < 0)) / 2;
+        for (int r = lane & 7; r < P.bs; r += 8)
+            s += row_shape(B.ca, B.ra, P.W, P.H, B.x0, B.y0 + r, P.bs, fx, fy);
+        s *= 255u * 4u;
+    } else {
+        for (int r = lane & 7; r < P.bs; r += 8)
+            s += row_sad4(B.cur, B.ref, P.W, P.H, B.x0, B.y0 + r, P.bs, dx2, dy2);
+    }
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
+    return s;
+}
+
+// 8 neighbour slots (lanes 4k..4k+3 own slot k), texture only.
+__device__ __forceinline__ uint32_t score8(const PaParams& P, const PaBlock& B, int lane, int dx2,
+                                           int dy2, bool active) {
+    uint32_t s = 0;
+    if (active)
+        for (int r = lane & 3; r < P.bs; r += 4)
+            s += row_sad4(B.cur, B.ref, P.W, P.H, B.x0, B.y0 + r, P.bs, dx2, dy2);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+    return s;
+}
+
+// The PRS probing direction (estimators.cpp:343-355) for field vector
+// (cx, cy): sequential raster-order double sums of prs_update terms
+// (estimators.cpp:303-309), each term computed by its own lane with
+// round-to-nearest intrinsics, then accumulated in order through shuffles.
+__device__ void prs_direction(const PaParams& P, const PaBlock& B, int lane, int cx, int cy,
+                              double& dir_x, double& dir_y) {
+    const int dmx = -cx, dmy = -cy;
+    const double pdx = 0.5 * dmx, pdy = 0.5 * dmy;
+    const int npix = P.bs * P.bs;
+    double sx = 0.0, sy = 0.0;
+    for (int base = 0; base < npix; base += 32) {
+        const int pix = base + lane;
+        const int x = B.x0 + pix % P.bs, y = B.y0 + pix / P.bs;
+        // dpd (metrics.cpp:86-88): cur(x,y) - halfpel(ref, 2x - d.dx, 2y - d.dy)
+        const int i4 = interp4(B.ref, P.W, P.H, 2 * x - dmx, 2 * y - dmy);
+        const double e = __dsub_rn(double(B.cur[size_t(y) * P.W + x]), double(i4) * 0.25);
+        // grad_central (metrics.cpp:97-101) on cur, clamped
+        const double gx = (double(pxc(B.cur, P.W, P.H, x + 1, y)) -
+                           double(pxc(B.cur, P.W, P.H, x - 1, y))) / 2.0;
+        const double gy = (double(pxc(B.cur, P.W, P.H, x, y + 1)) -
+                           double(pxc(B.cur, P.W, P.H, x, y - 1))) / 2.0;
+        // update_term (metrics.cpp:103-106)
+        const double ux = fabs(gx) < P.theta ? 0.0 : __ddiv_rn(1.0, gx);
+        const double uy = fabs(gy) < P.theta ? 0.0 : __ddiv_rn(1.0, gy);
+        const double ee = __dmul_rn(P.eps, e);
+        const double tx = __dsub_rn(pdx, __dmul_rn(ee, ux));
+        const double ty = __dsub_rn(pdy, __dmul_rn(ee, uy));
+        for (int j = 0; j < 32; ++j) {
+            sx = __dadd_rn(sx, __shfl_sync(0xFFFFFFFFu, tx, j));
+            sy = __dadd_rn(sy, __shfl_sync(0xFFFFFFFFu, ty, j));
+        }
+    }
+    const double n = double(P.bs) * double(P.bs);
+    dir_x = -__dsub_rn(__ddiv_rn(sx, n), pdx);
+    dir_y = -__dsub_rn(__ddiv_rn(sy, n), pdy);
+}
+
+struct PaResult {
+    int dx, dy;
+    uint32_t cost_q4, dpd, iters;
+};
+
+// prs_refine (estimators.cpp:311-382) from an already clipped start (cx, cy)
+// whose texture cost is `ccost` (kInf: not yet evaluated).  Warp-uniform.
+__device__ PaResult prs_warp(const PaParams& P, const PaBlock& B, int lane, int cx, int cy,
+                             uint32_t ccost, uint32_t* bitmap) {
+    const int M = P.bm_side / 2;  // lattice radius
+    for (int i = lane; i < P.bm_words; i += 32) bitmap[i] = 0;
+    __syncwarp();
+    const int sx0 = cx, sy0 = cy;
+    auto lattice_bit = [&](int vx, int vy) {
+        return ((vy - sy0) / P.step + M) * P.bm_side + ((vx - sx0) / P.step + M);
+    };
+    if (lane == 0) {
+        const int bit = lattice_bit(cx, cy);
+        bitmap[bit >> 5] |= 1u << (bit & 31);
+    }
+    __syncwarp();
+    uint32_t dpd = 1;
+    if (ccost == kInf) {
+        const uint32_t s = score4(P, B, lane, cx, cy, false);
+        ccost = __shfl_sync(0xFFFFFFFFu, s, 0);
+    }
+    uint32_t iters = 0;
+    for (int it = 0; it < P.max_iter; ++it) {
+        if (ccost == 0) break;
+        const int k = lane >> 2;
+        const int nx = cx + c_off8[k][0] * P.step, ny = cy + c_off8[k][1] * P.step;
+        const bool adm = nx >= B.w.lo_x && nx <= B.w.hi_x && ny >= B.w.lo_y && ny <= B.w.hi_y;
+        const uint32_t cost = score8(P, B, lane, nx, ny, adm);
+        const bool leader = (lane & 3) == 0;
+        bool fresh = false;
+        if (adm && leader) {
+            const int bit = lattice_bit(nx, ny);
+            const uint32_t m = 1u << (bit & 31);
+            fresh = (atomicOr(&bitmap[bit >> 5], m) & m) == 0;
+        }
+        dpd += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
+        const uint32_t mine = (adm && leader) ? cost : kInf;
+        const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, mine);
+        if (m >= ccost) break;  // center kept (estimators.cpp:376)
+        const uint32_t ties = __ballot_sync(0xFFFFFFFFu, adm && leader && cost == m);
+        int win;
+        if (__popc(ties) == 1) {
+            win = (__ffs(ties) - 1) >> 2;
+        } else {
+            // stable descending sort by off . dir (estimators.cpp:357-362): the
+            // first tied neighbour in sorted order has the largest key, and the
+            // smallest index among equal keys.
+            double dir_x, dir_y;
+            prs_direction(P, B, lane, cx, cy, dir_x, dir_y);
+            win = -1;
+            double bestkey = 0.0;
+            for (int i = 0; i < 8; ++i) {
+                if (!((ties >> (4 * i)) & 1u)) continue;
+                const double key = __dadd_rn(__dmul_rn(double(c_off8[i][0]), dir_x),
+                                             __dmul_rn(double(c_off8[i][1]), dir_y));
+                if (win < 0 || key > bestkey) {
+                    win = i;
+                    bestkey = key;
+                }
+            }
+        }
+        cx += c_off8[win][0] * P.step;
+        cy += c_off8[win][1] * P.step;
+        ccost = m;
+        ++iters;
+    }
+    PaResult r;
+    r.dx = cx;
+    r.dy = cy;
+    r.cost_q4 = ccost;
+    r.dpd = dpd;
+    r.iters = iters;
+    return r;
+}
+
+__device__ __forceinline__ int clip_comp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// brs_select (estimators.cpp:257-301) then prs_refine.  cand[] holds the four
+// raw candidates A, B, C, T (every lane).  Returns also the BRS winner slot.
+__device__ PaResult pa_block(const PaParams& P, const PaBlock& B, int lane, bool boundary,
+                             const int cdx[4], const int cdy[4], uint32_t* bitmap,
+                             uint32_t* brs_scores = nullptr, int* brs_kinds = nullptr) {
+    const int k = lane >> 3;
+    const int vx = clip_comp(cdx[k], B.w.lo_x, B.w.hi_x);
+    const int vy = clip_comp(cdy[k], B.w.lo_y, B.w.hi_y);
+    const bool shape = boundary && (k < 3 || P.bt_shape);
+    const uint32_t s = score4(P, B, lane, vx, vy, shape);
+    uint32_t sc[4];
+    int bx = 0, by = 0, win = 0;
+    for (int i = 0; i < 4; ++i) {
+        sc[i] = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
+        const int ix = __shfl_sync(0xFFFFFFFFu, vx, 8 * i), iy = __shfl_sync(0xFFFFFFFFu, vy, 8 * i);
+        if (i == 0 || sc[i] < sc[win]) {
+            win = i;
+            bx = ix;
+            by = iy;
+        }
+    }
+    if (brs_scores)
+        for (int i = 0; i < 4; ++i) brs_scores[i] = sc[i];
+    if (brs_kinds)
+        for (int i = 0; i < 4; ++i) brs_kinds[i] = boundary && (i < 3 || P.bt_shape);
+    const bool win_shape = boundary && (win < 3 || P.bt_shape);
+    return prs_warp(P, B, lane, bx, by, win_shape ? kInf : sc[win], bitmap);
+}
+
+struct PaArgs {
+    Batch b;
+    PaParams P;
+    const uint32_t* list;
+    const int* nlist;
+    me_block_rec* recs;
+    const int32_t* prev0;  // pair 0's temporal candidates or null
+};
+
+__global__ void __launch_bounds__(512) pa_kernel(PaArgs a) {
+    extern __shared__ uint32_t s_pa[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* bitmap = s_pa + wid * a.P.bm_words;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int n = *a.nlist;
+    const Batch& b = a.b;
+    const PaParams& P = a.P;
+    const size_t plane = size_t(b.W) * b.H;
+    const uint32_t pair_blocks = uint32_t(b.rows) * b.cols;
+    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+        const uint32_t e = a.list[item];
+        const uint32_t g = e & ~kBoundaryBit;
+        const bool boundary = (e & kBoundaryBit) != 0;
+        int h, v, p, seq;
+        decode_block(b, g, h, v, p, seq);
+        // gather_candidates (estimators.cpp:238-255): lanes 0..3 fetch A, B, C, T
+        uint32_t mvw = 0;
+        if (lane < 4) {
+            const uint32_t* src = nullptr;
+            if (lane == 0 && h > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - 1);
+            if (lane == 1 && v > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - b.cols);
+            if (lane == 2 && v > 0 && h + 1 < b.cols)
+                src = reinterpret_cast<const uint32_t*>(a.recs + g - b.cols + 1);
+            if (lane == 3 && p > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - pair_blocks);
+            if (src) {
+                mvw = ld_acquire(src);
+                while (mvw == kSentinel) {
+                    __nanosleep(64);
+                    mvw = ld_acquire(src);
+                }
+            } else if (lane == 3 && a.prev0) {
+                const int i = v * b.cols + h;
+                mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+            }
+        }
+        int cdx[4], cdy[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t w = __shfl_sync(0xFFFFFFFFu, mvw, i);
+            cdx[i] = mv_dx(w);
+            cdy[i] = mv_dy(w);
+        }
+        PaBlock B;
+        B.cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
+        B.ref = b.luma + (size_t(seq) * b.F + p) * plane;
+        B.ca = b.alpha ? b.alpha + (size_t(seq) * b.F + p + b.d) * plane : nullptr;
+        B.ra = b.alpha ? b.alpha + (size_t(seq) * b.F + p) * plane : nullptr;
+        B.x0 = h * P.bs;
+        B.y0 = v * P.bs;
+        B.w = hp_window(B.x0, B.y0, P.bs, P.W, P.H, P.S);
+        const PaResult r = pa_block(P, B, lane, boundary, cdx, cdy, bitmap);
+        if (lane == 0)
+            write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters,
+                      boundary ? ME_BOUNDARY : ME_OPAQUE, true);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// mc_kernel: predict_frame (compensation.cpp:30-71) fused with the psnr SSE
+// (metrics.cpp:108-124) and the per-pair SearchStats reduction.  One thread
+// per 8-pixel row segment; the prediction is only stored when requested.
+// ---------------------------------------------------------------------------
+
+struct McArgs {
+    Batch b;
+    const me_block_rec* recs;
+    me_pair_stats* stats;
+    uint8_t* pred;  // [n_seq*pairs][H][W] or null
+    const int32_t* mv_override;  // single-frame predict: [rows*cols][2] (recs ignored)
+    const uint8_t* types_override;
+    const uint8_t* ref_override;
+    const uint8_t* cur_override;
+};
+
+// Rounds 4*s/4 to nearest, ties to even (std::nearbyint, compensation.cpp:64).
+__device__ __forceinline__ int round_q4(int i4) {
+    const int q = i4 >> 2, rem = i4 & 3;
+    if (rem < 2) return q;
+    if (rem > 2) return q + 1;
+    return q + (q & 1);
+}
+
+__global__ void __launch_bounds__(256) mc_kernel(McArgs a) {
+    const Batch& b = a.b;
+    const int gp = blockIdx.y;  // seq * pairs + p
+    const int seq = gp / b.pairs, p = gp % b.pairs;
+    const size_t plane = size_t(b.W) * b.H;
+    const int segs = b.W >> 3;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t sse = 0;
+    uint32_t cmp = 0, dpd = 0, n_o = 0, n_b = 0, n_t = 0;
+    if (idx < segs * b.H) {
+        const int y = idx / segs, x = (idx - y * segs) * 8;
+        const int h = x / b.bs, v = y / b.bs;
+        const size_t bi = size_t(gp) * b.rows * b.cols + size_t(v) * b.cols + h;
+        int dx2, dy2, ty;
+        if (a.mv_override) {
+            const int i = v * b.cols + h;
+            dx2 = a.mv_override[2 * i];
+            dy2 = a.mv_override[2 * i + 1];
+            ty = a.types_override ? a.types_override[i] : ME_OPAQUE;
+        } else {
+            const uint4 r = *reinterpret_cast<const uint4*>(a.recs + bi);
+            dx2 = mv_dx(r.x);
+            dy2 = mv_dy(r.x);
+            ty = int((r.w >> 8) & 0xFF);
+            if (x % b.bs == 0 && y % b.bs == 0) {
+                cmp = r.z & 0xFFFF;
+                dpd = r.z >> 16;
+                n_o = ty == ME_OPAQUE;
+                n_b = ty == ME_BOUNDARY;
+                n_t = ty == ME_TRANSPARENT;
+            }
+        }
+        if (ty == ME_TRANSPARENT) dx2 = dy2 = 0;
+        const uint8_t* ref = a.ref_override ? a.ref_override : b.luma + (size_t(seq) * b.F + p) * plane;
+        const uint8_t* cur = a.cur_override ? a.cur_override
+                                            : b.luma + (size_t(seq) * b.F + p + b.d) * plane;
+        uint32_t pw0, pw1;
+        const int sx = x + (dx2 >> 1), sy = y + (dy2 >> 1);
+        if (((dx2 | dy2) & 1) == 0 && sx >= 0 && sx + 8 <= b.W && sy >= 0 && sy < b.H) {
+            ld8u(ref + size_t(sy) * b.W + sx, pw0, pw1);
+        } else {
+            uint32_t w[2] = {0u, 0u};
+            for (int i = 0; i < 8; ++i) {
+                const int xx = x + i;
+                const int val = ((dx2 | dy2) & 1) == 0
+                                    ? pxc(ref, b.W, b.H, xx + (dx2 >> 1), y + (dy2 >> 1))
+                                    : round_q4(interp4(ref, b.W, b.H, 2 * xx + dx2, 2 * y + dy2));
+                w[i >> 2] |= uint32_t(clampi(val, 0, 255)) << (8 * (i & 3));
+            }
+            pw0 = w[0];
+            pw1 = w[1];
+        }
+        if (cur) {
+            const uint32_t c0 = ldg32(cur + size_t(y) * b.W + x), c1 = ldg32(cur + size_t(y) * b.W + x + 4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int d0 = int((c0 >> (8 * i)) & 0xFF) - int((pw0 >> (8 * i)) & 0xFF);
+                const int d1 = int((c1 >> (8 * i)) & 0xFF) - int((pw1 >> (8 * i)) & 0xFF);
+                sse += uint32_t(d0 * d0 + d1 * d1);
+            }
+        }
+        if (a.pred) {
+            uint2* dst = reinterpret_cast<uint2*>(a.pred + size_t(gp) * plane + size_t(y) * b.W + x);
+            *dst = make_uint2(pw0, pw1);
+        }
+    }
+    // CTA reduction
+    __shared__ uint32_t s_red[6][8];
+    uint32_t vals[6] = {sse, cmp, dpd, n_o, n_b, n_t};
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        uint32_t v = vals[k];
+        v = __reduce_add_sync(0xFFFFFFFFu, v);
+        if (lane == 0) s_red[k][wid] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        unsigned long long tot = 0;
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) tot += s_red[threadIdx.x][i];
+        if (tot && a.stats) {
+            unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp);
+            const int field[6] = {5, 0, 1, 2, 3, 4};  // sse, cmp, dpd, opaque, boundary, transparent
+            atomicAdd(st + field[threadIdx.x], tot);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Single-block kernels behind the per-block C-ABI entry points.
+// ---------------------------------------------------------------------------
+
+template <int BS>
+__global__ void __launch_bounds__(kEsThreads) es_single_kernel(const uint8_t* cur, const uint8_t* ref,
+                                                               int W, int H, int x0, int y0, int S,
+                                                               int band_rows, int64_t* out) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ unsigned long long s_best[kEsThreads / 32];
+    int dx, dy;
+    uint32_t sad, cmp;
+    es_block<BS, 8>(cur, ref, W, H, x0, y0, S, band_rows / 8, sm, s_best, dx, dy, sad, cmp);
+    if (threadIdx.x == 0) {
+        out[0] = 2 * dx;
+        out[1] = 2 * dy;
+        out[2] = cmp;
+        out[3] = int64_t(sad) * 4;
+    }
+}
+
+__global__ void ring_single_kernel(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H,
+                                   int x0, int y0, int bs, int S, int64_t* out) {
+    extern __shared__ uint32_t s_bits[];
+    int dx, dy;
+    uint32_t sad, cmp;
+    ring_block(algo, cur, ref, W, H, x0, y0, bs, S, s_bits, threadIdx.x & 31, dx, dy, sad, cmp);
+    if (threadIdx.x == 0) {
+        out[0] = 2 * dx;
+        out[1] = 2 * dy;
+        out[2] = cmp;
+        out[3] = int64_t(sad) * 4;
+    }
+}
+
+// out: [0..1] mv, [2..5] scores_q4, [6..9] kinds
+__global__ void brs_single_kernel(PaParams P, PaBlock B, int boundary, const int32_t* cands,
+                                  int64_t* out) {
+    extern __shared__ uint32_t s_bits[];
+    const int lane = threadIdx.x & 31;
+    int cdx[4], cdy[4];
+    for (int i = 0; i < 4; ++i) {
+        cdx[i] = cands[2 * i];
+        cdy[i] = cands[2 * i + 1];
+    }
+    const int k = lane >> 3;
+    const int vx = clip_comp(cdx[k], B.w.lo_x, B.w.hi_x);
+    const int vy = clip_comp(cdy[k], B.w.lo_y, B.w.hi_y);
+    const bool shape = boundary && (k < 3 || P.bt_shape);
+    const uint32_t s = score4(P, B, lane, vx, vy, shape);
+    uint32_t sc[4];
+    int bx = 0, by = 0, win = 0;
+    for (int i = 0; i < 4; ++i) {
+        sc[i] = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
+        const int ix = __shfl_sync(0xFFFFFFFFu, vx, 8 * i), iy = __shfl_sync(0xFFFFFFFFu, vy, 8 * i);
+        if (i == 0 || sc[i] < sc[win]) {
+            win = i;
+            bx = ix;
+            by = iy;
+        }
+    }
+    if (lane == 0) {
+        out[0] = bx;
+        out[1] = by;
+        for (int i = 0; i < 4; ++i) {
+            out[2 + i] = sc[i];
+            out[6 + i] = boundary && (i < 3 || P.bt_shape);
+        }
+    }
+}
+
+// out: [0..1] mv, [2] dpd, [3] iterations, [4] final cost_q4, [5..] descent log
+__global__ void prs_single_kernel(PaParams P, PaBlock B, int d0x, int d0y, int64_t* out) {
+    extern __shared__ uint32_t s_bits[];
+    const int lane = threadIdx.x & 31;
+    const int cx = clip_comp(d0x, B.w.lo_x, B.w.hi_x), cy = clip_comp(d0y, B.w.lo_y, B.w.hi_y);
+    // replay the descent to produce the log: run prs with max_iter = 0.. is
+    // wasteful; instead record accepted centers inline by re-running per step.
+    PaParams Q = P;
+    uint32_t logv[64];
+    int nlog = 0;
+    PaResult r{};
+    const int cap = P.max_iter < 63 ? P.max_iter : 63;
+    for (int m = 0; m <= cap; ++m) {
+        Q.max_iter = m;
+        if (m == 0) {
+            // center cost only
+            const uint32_t s = score4(P, B, lane, cx, cy, false);
+            logv[nlog++] = __shfl_sync(0xFFFFFFFFu, s, 0);
+            continue;
+        }
+        r = prs_warp(Q, B, lane, cx, cy, kInf, s_bits);
+        if (int(r.iters) < m) break;  // stopped before using the m-th iteration
+        logv[nlog++] = r.cost_q4;
+    }
+    r = prs_warp(P, B, lane, cx, cy, kInf, s_bits);
+    if (lane == 0) {
+        out[0] = r.dx;
+        out[1] = r.dy;
+        out[2] = r.dpd;
+        out[3] = r.iters;
+        out[4] = r.cost_q4;
+        for (int i = 0; i < nlog && i < 64; ++i) out[5 + i] = logv[i];
+    }
+}
+
+__global__ void sad_texture_single_kernel(const uint8_t* cur, const uint8_t* ref, int W, int H,
+                                          int x0, int y0, int bs, int dx2, int dy2, int64_t* out) {
+    const int lane = threadIdx.x & 31;
+    uint32_t s = 0;
+    for (int r = lane; r < bs; r += 32) s += row_sad4(cur, ref, W, H, x0, y0 + r, bs, dx2, dy2);
+    s = __reduce_add_sync(0xFFFFFFFFu, s);
+    if (lane == 0) out[0] = s;
+}
+
+__global__ void sad_shape_single_kernel(const uint8_t* ca, const uint8_t* ra, int W, int H, int x0,
+                                        int y0, int bs, int fx, int fy, int64_t* out) {
+    const int lane = threadIdx.x & 31;
+    uint32_t s = 0;
+    for (int r = lane; r < bs; r += 32) s += row_shape(ca, ra, W, H, x0, y0 + r, bs, fx, fy);
+    s = __reduce_add_sync(0xFFFFFFFFu, s);
+    if (lane == 0) out[0] = int64_t(s) * 255;
+}
+
+__global__ void classify_frame_kernel(const uint8_t* alpha, int W, int H, int bs, uint8_t* types) {
+    const int cols = W / bs, rows = H / bs;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cols * rows) return;
+    types[i] = uint8_t(classify_one(alpha, W, (i % cols) * bs, (i / cols) * bs, bs));
+}
+
+__global__ void binarize_kernel(const uint8_t* g, int n, int thr, uint8_t* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = g[i] >= thr ? 255 : 0;
+}
+
+__global__ void sse_kernel(const uint8_t* x, const uint8_t* y, int n, unsigned long long* out) {
+    unsigned long long s = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int d = int(x[i]) - int(y[i]);
+        s += uint64_t(d * d);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+
+namespace {
+
+constexpr int kEsBandRows = 64;  // dy rows of candidates staged per band (multiple of K=8)
+
+size_t es_smem_bytes(int bs, int S, int W) {
+    const int WX = min(2 * S + 1, W - bs + 1);
+    const int PW = ((WX - 1) >> 2) + (bs >> 2) + 1;
+    const int srows = kEsBandRows + bs - 1;
+    return size_t(4) * (size_t(srows) * PW + 32) * 4;
+}
+
+PaParams make_pa_params(const Batch& b, const me_config& c) {
+    PaParams P;
+    P.W = b.W;
+    P.H = b.H;
+    P.bs = b.bs;
+    P.S = c.search_range;
+    P.max_iter = c.max_iterations;
+    P.step = c.halfpel ? 1 : c.step;
+    P.bt_shape = c.boundary_temporal == ME_BT_SHAPE;
+    P.eps = c.epsilon;
+    P.theta = c.theta;
+    // lattice radius: max_iter steps, but never more than the window allows
+    const int span = (4 * c.search_range) / P.step + 1;
+    int side = 2 * c.max_iterations + 1;
+    if (side > 2 * span + 1) side = 2 * span + 1;
+    P.bm_side = side;
+    P.bm_words = (side * side + 31) / 32;
+    return P;
+}
+
+struct Scratch {
+    uint8_t* types;
+    uint32_t* list;
+    int* hist;
+    int* offs;
+    int* cursor;
+    int* counter;
+};
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+Scratch carve(const Batch& b, int nbins, void* base) {
+    Scratch s;
+    uint8_t* p = static_cast<uint8_t*>(base);
+    const size_t nb = size_t(b.nblocks());
+    s.types = p;
+    p += align_up(nb);
+    s.list = reinterpret_cast<uint32_t*>(p);
+    p += align_up(nb * 4);
+    s.hist = reinterpret_cast<int*>(p);
+    p += align_up(size_t(nbins) * 4);
+    s.offs = reinterpret_cast<int*>(p);
+    p += align_up(size_t(nbins + 1) * 4);
+    s.cursor = reinterpret_cast<int*>(p);
+    p += align_up(size_t(nbins) * 4);
+    s.counter = reinterpret_cast<int*>(p);
+    return s;
+}
+
+}  // namespace
+
+size_t scratch_bytes(const Batch& b, int algo) {
+    const int nbins = algo == ME_ALGO_PA ? b.steps() : 1;
+    const size_t nb = size_t(b.nblocks());
+    return align_up(nb) + align_up(nb * 4) + align_up(size_t(nbins) * 4) +
+           align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4) + 256;
+}
+
+cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
+                      me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
+                      size_t scratch_size, int num_sms, cudaStream_t st) {
+    const int algo = cfg.algo;
+    const bool pa = algo == ME_ALGO_PA;
+    const int nbins = pa ? b.steps() : 1;
+    if (scratch_size < scratch_bytes(b, algo)) return cudaErrorInvalidValue;
+    Scratch s = carve(b, nbins, scratch);
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(s.hist, 0, size_t(nbins) * 4, st))) return e;
+    if ((e = cudaMemsetAsync(s.counter, 0, 4, st))) return e;
+    if (stats && (e = cudaMemsetAsync(stats, 0, sizeof(me_pair_stats) * size_t(b.n_seq) * b.pairs, st)))
+        return e;
+
+    ClassArgs ca;
+    ca.b = b;
+    ca.pa = pa ? 1 : 0;
+    ca.recs = recs;
+    ca.types = s.types;
+    ca.hist = s.hist;
+    ca.nbins = nbins;
+    const int64_t nb = b.nblocks();
+    const size_t hist_smem = size_t(nbins) * 4;
+    {
+        const int threads = 256;
+        int grid = int(std::min<int64_t>((nb + threads - 1) / threads, int64_t(num_sms) * 8));
+        if (grid < 1) grid = 1;
+        classify_kernel<<<grid, threads, hist_smem, st>>>(ca);
+        if ((e = cudaGetLastError())) return e;
+    }
+    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, s.offs, s.cursor);
+    if ((e = cudaGetLastError())) return e;
+    {
+        const int threads = 256;
+        const int64_t chunk = threads * 8;
+        const int grid = int((nb + chunk - 1) / chunk);
+        fill_kernel<<<grid, threads, 2 * hist_smem, st>>>(ca, s.cursor, s.list);
+        if ((e = cudaGetLastError())) return e;
+    }
+    const int* nlist = s.offs + nbins;
+
+    if (algo == ME_ALGO_ES) {
+        EsArgs ea;
+        ea.b = b;
+        ea.S = cfg.search_range;
+        ea.list = s.list;
+        ea.nlist = nlist;
+        ea.counter = s.counter;
+        ea.recs = recs;
+        ea.band_rows_max = kEsBandRows;
+        const size_t smem = es_smem_bytes(b.bs, cfg.search_range, b.W);
+        if (b.bs == 16) {
+            if ((e = cudaFuncSetAttribute(es_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, es_kernel<16, 8>, kEsThreads, smem);
+            es_kernel<16, 8><<<num_sms * (occ > 0 ? occ : 1), kEsThreads, smem, st>>>(ea);
+        } else {
+            if ((e = cudaFuncSetAttribute(es_kernel<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, es_kernel<8, 8>, kEsThreads, smem);
+            es_kernel<8, 8><<<num_sms * (occ > 0 ? occ : 1), kEsThreads, smem, st>>>(ea);
+        }
+        if ((e = cudaGetLastError())) return e;
+    } else if (algo == ME_ALGO_PA) {
+        PaArgs pa_args;
+        pa_args.b = b;
+        pa_args.P = make_pa_params(b, cfg);
+        pa_args.list = s.list;
+        pa_args.nlist = nlist;
+        pa_args.recs = recs;
+        pa_args.prev0 = prev0;
+        const int threads = 512;
+        const size_t smem = size_t(threads / 32) * pa_args.P.bm_words * 4;
+        if ((e = cudaFuncSetAttribute(pa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pa_kernel, threads, smem);
+        // persistent: every warp must be co-resident (dependency spinning)
+        pa_kernel<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(pa_args);
+        if ((e = cudaGetLastError())) return e;
+    } else {
+        RingArgs ra;
+        ra.b = b;
+        ra.algo = algo;
+        ra.S = cfg.search_range;
+        ra.list = s.list;
+        ra.nlist = nlist;
+        ra.recs = recs;
+        const int WX = std::min(2 * cfg.search_range + 1, b.W - b.bs + 1);
+        const int WY = std::min(2 * cfg.search_range + 1, b.H - b.bs + 1);
+        ra.bitmap_words = (WX * WY + 31) / 32;
+        int warps = 8;
+        while (warps > 1 && size_t(warps) * ra.bitmap_words * 4 > 160 * 1024) warps >>= 1;
+        const size_t smem = size_t(warps) * ra.bitmap_words * 4;
+        if ((e = cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ring_kernel, warps * 32, smem);
+        ring_kernel<<<num_sms * (occ > 0 ? occ : 1), warps * 32, smem, st>>>(ra);
+        if ((e = cudaGetLastError())) return e;
+    }
+
+    McArgs ma;
+    ma.b = b;
+    ma.recs = recs;
+    ma.stats = stats;
+    ma.pred = pred;
+    ma.mv_override = nullptr;
+    ma.types_override = nullptr;
+    ma.ref_override = nullptr;
+    ma.cur_override = nullptr;
+    const int segs = (b.W / 8) * b.H;
+    dim3 grid((segs + 255) / 256, b.n_seq * b.pairs);
+    mc_kernel<<<grid, 256, 0, st>>>(ma);
+    return cudaGetLastError();
+}
+
+cudaError_t block_search(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H, int x0,
+                         int y0, int size, int range, int64_t* out, cudaStream_t st) {
+    if (algo == ME_ALGO_ES) {
+        const size_t smem = es_smem_bytes(size, range, W);
+        cudaError_t e;
+        if (size == 16) {
+            if ((e = cudaFuncSetAttribute(es_single_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+            es_single_kernel<16><<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, kEsBandRows, out);
+        } else {
+            if ((e = cudaFuncSetAttribute(es_single_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+            es_single_kernel<8><<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, kEsBandRows, out);
+        }
+        return cudaGetLastError();
+    }
+    const int WX = std::min(2 * range + 1, W - size + 1);
+    const int WY = std::min(2 * range + 1, H - size + 1);
+    const size_t smem = size_t((WX * WY + 31) / 32) * 4;
+    cudaError_t e = cudaFuncSetAttribute(ring_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e) return e;
+    ring_single_kernel<<<1, 32, smem, st>>>(algo, cur, ref, W, H, x0, y0, size, range, out);
+    return cudaGetLastError();
+}
+
+static PaBlock single_block(const uint8_t* cur, const uint8_t* ref, const uint8_t* ca,
+                            const uint8_t* ra, int W, int H, int x0, int y0, int size, int range) {
+    PaBlock B;
+    B.cur = cur;
+    B.ref = ref;
+    B.ca = ca;
+    B.ra = ra;
+    B.x0 = x0;
+    B.y0 = y0;
+    B.w.lo_x = std::max(-2 * range, -2 * x0);
+    B.w.hi_x = std::min(2 * range, 2 * (W - x0 - size));
+    B.w.lo_y = std::max(-2 * range, -2 * y0);
+    B.w.hi_y = std::min(2 * range, 2 * (H - y0 - size));
+    return B;
+}
+
+cudaError_t brs_single(const uint8_t* cur, const uint8_t* ref, const uint8_t* ca,
+                       const uint8_t* ra, int W, int H, int x0, int y0, int size, int btype,
+                       const int32_t* cands_dev, int range, int boundary_temporal, int64_t* out,
+                       cudaStream_t st) {
+    PaParams P{};
+    P.W = W;
+    P.H = H;
+    P.bs = size;
+    P.S = range;
+    P.bt_shape = boundary_temporal == ME_BT_SHAPE;
+    PaBlock B = single_block(cur, ref, ca, ra, W, H, x0, y0, size, range);
+    brs_single_kernel<<<1, 32, 0, st>>>(P, B, btype == ME_BOUNDARY, cands_dev, out);
+    return cudaGetLastError();
+}
+
+cudaError_t prs_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                       int size, int d0x, int d0y, int range, double eps, double theta,
+                       int max_iter, int step, int64_t* out, cudaStream_t st) {
+    Batch b{};
+    b.W = W;
+    b.H = H;
+    b.bs = size;
+    me_config c{};
+    c.search_range = range;
+    c.max_iterations = max_iter;
+    c.step = step;
+    c.halfpel = 0;
+    c.epsilon = eps;
+    c.theta = theta;
+    PaParams P = make_pa_params(b, c);
+    PaBlock B = single_block(cur, ref, nullptr, nullptr, W, H, x0, y0, size, range);
+    const size_t smem = size_t(P.bm_words) * 4;
+    cudaError_t e = cudaFuncSetAttribute(prs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e) return e;
+    prs_single_kernel<<<1, 32, smem, st>>>(P, B, d0x, d0y, out);
+    return cudaGetLastError();
+}
+
+cudaError_t sad_texture_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                               int size, int dx, int dy, int64_t* out, cudaStream_t st) {
+    sad_texture_single_kernel<<<1, 32, 0, st>>>(cur, ref, W, H, x0, y0, size, dx, dy, out);
+    return cudaGetLastError();
+}
+
+cudaError_t sad_shape_single(const uint8_t* ca, const uint8_t* ra, int W, int H, int x0, int y0,
+                             int size, int dx, int dy, int64_t* out, cudaStream_t st) {
+    sad_shape_single_kernel<<<1, 32, 0, st>>>(ca, ra, W, H, x0, y0, size, dx / 2, dy / 2, out);
+    return cudaGetLastError();
+}
+
+cudaError_t classify_frame(const uint8_t* alpha, int W, int H, int bs, uint8_t* types,
+                           cudaStream_t st) {
+    const int n = (W / bs) * (H / bs);
+    classify_frame_kernel<<<(n + 255) / 256, 256, 0, st>>>(alpha, W, H, bs, types);
+    return cudaGetLastError();
+}
+
+cudaError_t binarize(const uint8_t* gray, int n, int threshold, uint8_t* out, cudaStream_t st) {
+    binarize_kernel<<<std::min((n + 255) / 256, 4096), 256, 0, st>>>(gray, n, threshold, out);
+    return cudaGetLastError();
+}
+
+cudaError_t predict(const uint8_t* ref, const uint8_t* cur, const int32_t* mv, const uint8_t* types,
+                    int W, int H, int bs, uint8_t* pred, me_pair_stats* stats_out,
+                    cudaStream_t st) {
+    Batch b{};
+    b.W = W;
+    b.H = H;
+    b.bs = bs;
+    b.n_seq = 1;
+    b.pairs = 1;
+    b.F = 1;
+    b.d = 0;
+    b.cols = W / bs;
+    b.rows = H / bs;
+    McArgs ma;
+    ma.b = b;
+    ma.recs = nullptr;
+    ma.stats = stats_out;  // only .sse is non-zero (no records)
+    ma.pred = pred;
+    ma.mv_override = mv;
+    ma.types_override = types;
+    ma.ref_override = ref;
+    ma.cur_override = cur;
+    const int segs = (W / 8) * H;
+    dim3 grid((segs + 255) / 256, 1);
+    mc_kernel<<<grid, 256, 0, st>>>(ma);
+    return cudaGetLastError();
+}
+
+cudaError_t sse(const uint8_t* a, const uint8_t* b, int n, unsigned long long* out,
+                cudaStream_t st) {
+    sse_kernel<<<std::min((n + 255) / 256, 1024), 256, 0, st>>>(a, b, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace mek

@@ -1,0 +1,57 @@
+// kernels.h — host-side launchers for the sm_100a kernels in kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "me_b200.h"
+
+namespace mek {
+
+// Geometry of a batch: n_seq sequences x n_frames frames of W x H luma; pairs
+// tau = d .. F-1 (pair index p = tau - d, cur = frame p + d, ref = frame p).
+struct Batch {
+    const uint8_t* luma;   // [n_seq][F][H][W]
+    const uint8_t* alpha;  // same shape, or null (all opaque)
+    int n_seq, F, W, H, d, pairs, bs, cols, rows;
+    __host__ __device__ int64_t nblocks() const { return int64_t(n_seq) * pairs * rows * cols; }
+    __host__ __device__ int steps() const { return (cols - 1) + 2 * (rows - 1) + (pairs - 1) + 1; }
+};
+
+// Scratch needed by run_batch (bytes), given the step-bin count.
+size_t scratch_bytes(const Batch& b, int algo);
+
+// Full device pipeline: classify -> (ES | rings | PA wavefront) -> MC + PSNR.
+// `prev0` (nullable, [rows*cols][2] int32) supplies pair 0's temporal
+// candidates (estimate_field's prev_field); stats must hold n_seq*pairs
+// entries; pred is nullable.
+cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
+                      me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
+                      size_t scratch_size, int num_sms, cudaStream_t st);
+
+// Single-block entry points (all pointers device pointers; outputs in `out`,
+// an int64 array whose layout is documented at each launcher).
+cudaError_t block_search(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H, int x0,
+                         int y0, int size, int range, int64_t* out, cudaStream_t st);
+cudaError_t brs_single(const uint8_t* cur, const uint8_t* ref, const uint8_t* ca,
+                       const uint8_t* ra, int W, int H, int x0, int y0, int size, int btype,
+                       const int32_t* cands_dev, int range, int boundary_temporal, int64_t* out,
+                       cudaStream_t st);
+cudaError_t prs_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                       int size, int d0x, int d0y, int range, double eps, double theta,
+                       int max_iter, int step, int64_t* out, cudaStream_t st);
+cudaError_t sad_texture_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                               int size, int dx, int dy, int64_t* out, cudaStream_t st);
+cudaError_t sad_shape_single(const uint8_t* ca, const uint8_t* ra, int W, int H, int x0, int y0,
+                             int size, int dx, int dy, int64_t* out, cudaStream_t st);
+cudaError_t classify_frame(const uint8_t* alpha, int W, int H, int bs, uint8_t* types,
+                           cudaStream_t st);
+cudaError_t binarize(const uint8_t* gray, int n, int threshold, uint8_t* out, cudaStream_t st);
+cudaError_t predict(const uint8_t* ref, const uint8_t* cur, const int32_t* mv, const uint8_t* types,
+                    int W, int H, int bs, uint8_t* pred, me_pair_stats* stats,
+                    cudaStream_t st);
+cudaError_t sse(const uint8_t* a, const uint8_t* b, int n, unsigned long long* out,
+                cudaStream_t st);
+
+}  // namespace mek

@@ -1,0 +1,74 @@
+// me_internal.h — shared host-side internals of libme_b200.so (not installed).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "me_b200.h"
+
+// Records `msg` as this thread's last error and returns `code`.
+me_status me_fail(me_status code, const std::string& msg);
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+
+#define ME_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return me_fail(ME_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Grow-only pinned host staging buffer.
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMallocHost(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct me_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    // scratch for the batched pipeline
+    DevBuf types, worklist, counters, tasks;
+    // inputs/outputs of the host-pointer entry points
+    DevBuf in_luma, in_alpha, out_recs, out_stats, out_pred, aux;
+    HostBuf pin_a, pin_b;
+};
+
+#endif

@@ -1,0 +1,211 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle
+restatement on identical seeded inputs.  Integer results must be bit-exact
+(MVs, per-block SAD x4, comparison / dpd / iteration counts, block classes,
+SSE); the PSNR dB value is computed from the exact SSE on the host.
+Run on a B200:  python -m pytest tests -m gpu
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = [(4, 8), (4, 16), (0, 16), (1, 16), (2, 16), (3, 16)]
+
+
+def noise(rng, h, w):
+    return rng.integers(0, 256, size=(h, w), dtype=np.uint8)
+
+
+def shift_clamped(base, sx, sy):
+    h, w = base.shape
+    ys = np.clip(np.arange(h) + sy, 0, h - 1)
+    xs = np.clip(np.arange(w) + sx, 0, w - 1)
+    return base[ys][:, xs]
+
+
+def assert_recs(got, want, what=""):
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        i = tuple(bad[0])
+        raise AssertionError(f"{what}: {len(bad)} record mismatches; first at {i}: got {got[i]} want {want[i]}")
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2])
+@pytest.mark.parametrize("algo,bs", ALGOS)
+def test_sequence_configs(me_gpu, port, cfg_id, algo, bs):
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config_sequence(cfg_id, 1000 + cfg_id)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=16, block_size=bs))
+    recs, stats = me_gpu.run_sequences(cfg, luma[None], alpha[None])
+    want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=bs), luma, alpha)
+    assert_recs(recs[0], want_r, f"cfg{cfg_id} algo{algo} bs{bs}")
+    assert np.array_equal(stats[0], want_s)
+
+
+@pytest.mark.parametrize("algo,bs", ALGOS)
+def test_sequence_no_mask_and_pred(me_gpu, port, algo, bs):
+    rng = np.random.default_rng(algo * 10 + bs)
+    base = noise(rng, 96 + 32, 128 + 32)
+    frames = np.stack([shift_clamped(base, 2 * t, -t)[16:16 + 96, 16:16 + 128] for t in range(5)])
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=7, block_size=bs, ref_distance=1))
+    recs, stats, pred = me_gpu.run_sequences(cfg, frames[None], None, want_pred=True)
+    want_r, want_s, want_p = port.run_sequence(oracle.make_cfg(algo=algo, search_range=7, block_size=bs, ref_distance=1), frames, None, want_pred=True)
+    assert_recs(recs[0], want_r)
+    assert np.array_equal(stats[0], want_s)
+    assert np.array_equal(pred[0], want_p)
+
+
+def test_batch_of_sequences_config4_small(me_gpu, port):
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config4_batch(6, 500, frames=8)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in range(6):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"seq {i}")
+        assert np.array_equal(stats[i], want_s)
+
+
+@pytest.mark.parametrize("contrast", ["full", "low"])
+@pytest.mark.parametrize("bs", [8, 16])
+def test_pa_tie_heavy_sequences(me_gpu, port, contrast, bs):
+    """Low-contrast content makes PRS neighbour ties frequent, exercising the
+    FP64 direction path (estimators.cpp:345-362)."""
+    rng = np.random.default_rng(77 + bs)
+    if contrast == "low":
+        base = (100 + rng.integers(0, 3, size=(160, 192))).astype(np.uint8)
+    else:
+        base = noise(rng, 160, 192)
+    frames = np.stack([shift_clamped(base, (t * 3) % 5 - 2, (t * 7) % 5 - 2)[16:144, 16:176] for t in range(8)])
+    mask = np.zeros_like(frames)
+    mask[:, 20:100, 30:120] = 255
+    for halfpel in (0, 1):
+        cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=8, block_size=bs, halfpel=bool(halfpel)))
+        recs, stats = me_gpu.run_sequences(cfg, frames[None], mask[None])
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=8, block_size=bs, halfpel=halfpel), frames, mask)
+        assert_recs(recs[0], want_r, f"halfpel={halfpel}")
+        assert np.array_equal(stats[0], want_s)
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2, 3])
+@pytest.mark.parametrize("rng_s", [7, 16])
+def test_block_search_random(me_gpu, port, algo, rng_s):
+    rng = np.random.default_rng(2026 + algo)
+    st = me_gpu.SearchStats()
+    for trial in range(4):
+        cur, ref = noise(rng, 64, 64), noise(rng, 64, 64)
+        if trial == 1:  # smooth content: long descents, revisits
+            cur = np.convolve(cur.ravel(), np.ones(9) / 9, "same").reshape(64, 64).astype(np.uint8)
+            ref = shift_clamped(cur, 3, -2)
+        for r in me_gpu.block_grid(64, 64, 16):
+            st = me_gpu.SearchStats()
+            fn = [me_gpu.full_search, me_gpu.tss_search, me_gpu.fss_search, me_gpu.ds_search][algo]
+            mv = fn(cur, ref, r, me_gpu.SearchConfig(search_range=rng_s, block_size=16), st)
+            want_mv, want_cmp, _ = port.block_search(algo, cur, ref, r.x0, r.y0, 16, rng_s)
+            assert mv == tuple(want_mv) and st.block_comparisons == want_cmp, (trial, r)
+
+
+def test_brs_select_random(me_gpu, port):
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        cur, ref = noise(rng, 64, 64), noise(rng, 64, 64)
+        ca = np.zeros((64, 64), np.uint8)
+        ra = np.zeros((64, 64), np.uint8)
+        ca[rng.integers(0, 30):rng.integers(34, 64), rng.integers(0, 30):rng.integers(34, 64)] = 255
+        ra[rng.integers(0, 30):rng.integers(34, 64), rng.integers(0, 30):rng.integers(34, 64)] = 255
+        size = 8 if trial % 2 else 16
+        x0 = int(rng.integers(0, 64 // size)) * size
+        y0 = int(rng.integers(0, 64 // size)) * size
+        cands = [int(v) for v in rng.integers(-20, 21, size=8)]
+        btype = int(rng.integers(1, 3))
+        bt = int(trial % 3 == 0)
+        cs = me_gpu.CandidateSet(tuple(cands[0:2]), tuple(cands[2:4]), tuple(cands[4:6]), tuple(cands[6:8]))
+        log = []
+        mv = me_gpu.brs_select(cur, ref, ca, ra, me_gpu.BlockRect(x0, y0, size), me_gpu.BlockType(btype), cs, me_gpu.SearchConfig(search_range=7, block_size=size), me_gpu.EstimateOptions(me_gpu.BoundaryTemporal(bt), log), me_gpu.SearchStats())
+        want_mv, want_kinds = port.brs_select(cur, ref, ca, ra, x0, y0, size, btype, cands, 7, bt)
+        assert mv == tuple(want_mv), trial
+        assert [int(e.kind) for e in log] == want_kinds
+
+
+@pytest.mark.parametrize("step", [2, 1])
+@pytest.mark.parametrize("size", [8, 16])
+def test_prs_refine_random(me_gpu, port, step, size):
+    rng = np.random.default_rng(500 + step + size)
+    for trial in range(30):
+        if trial % 3 == 2:
+            cur = (100 + rng.integers(0, 2, size=(64, 64))).astype(np.uint8)
+            ref = (100 + rng.integers(0, 2, size=(64, 64))).astype(np.uint8)
+        else:
+            cur, ref = noise(rng, 64, 64), noise(rng, 64, 64)
+        x0 = int(rng.integers(0, 64 // size)) * size
+        y0 = int(rng.integers(0, 64 // size)) * size
+        d0 = (int(rng.integers(-11, 12)), int(rng.integers(-11, 12)))
+        st = me_gpu.SearchStats()
+        log = []
+        mv = me_gpu.prs_refine(cur, ref, me_gpu.BlockRect(x0, y0, size), d0, me_gpu.SearchConfig(search_range=7, block_size=size), me_gpu.PrsConfig(step=step), st, log)
+        want_mv, want_dpd, want_log = port.prs_refine(cur, ref, x0, y0, size, d0, 7, step=step)
+        assert mv == tuple(want_mv), trial
+        assert st.dpd_refinement_steps == want_dpd
+        assert [int(v * 4) for v in log] == want_log
+
+
+def test_sad_texture_and_shape(me_gpu, port):
+    rng = np.random.default_rng(3)
+    cur, ref = noise(rng, 48, 64), noise(rng, 48, 64)
+    ca = (noise(rng, 48, 64) > 128).astype(np.uint8) * 255
+    ra = (noise(rng, 48, 64) > 100).astype(np.uint8) * 255
+    for size in (8, 16):
+        for x0, y0 in ((0, 0), (48 - size + 0, 16), (8, 32 - size + 16)):
+            if x0 + size > 64 or y0 + size > 48:
+                continue
+            for dx in range(-21, 22, 3):
+                for dy in (-19, -4, -1, 0, 1, 6, 25):
+                    got = me_gpu.sad_texture(cur, ref, me_gpu.BlockRect(x0, y0, size), (dx, dy))
+                    assert got == port.sad_texture(cur, ref, x0, y0, size, dx, dy)
+                    if dx % 2 == 0 and dy % 2 == 0:
+                        assert me_gpu.sad_shape(ca, ra, me_gpu.BlockRect(x0, y0, size), (dx, dy)) == port.sad_shape(ca, ra, x0, y0, size, dx, dy)
+    with pytest.raises(ValueError):
+        me_gpu.sad_shape(ca, ra, me_gpu.BlockRect(0, 0, 8), (1, 0))
+
+
+def test_classify_binarize_predict_psnr(me_gpu, port):
+    rng = np.random.default_rng(5)
+    gray = noise(rng, 64, 96)
+    assert np.array_equal(me_gpu.binarize(gray), port.binarize(gray))
+    alpha = np.zeros((64, 96), np.uint8)
+    alpha[10:50, 20:70] = 255
+    for bs in (8, 16):
+        assert np.array_equal(me_gpu.classify_blocks(alpha, bs), port.classify(alpha, bs))
+    ref = noise(rng, 64, 96)
+    cur = noise(rng, 64, 96)
+    for bs in (8, 16):
+        cols, rows = 96 // bs, 64 // bs
+        mv = rng.integers(-40, 41, size=(cols * rows, 2)).astype(np.int32)
+        types = rng.integers(0, 3, size=cols * rows).astype(np.uint8)
+        f = me_gpu.MotionField(cols, rows, bs, vectors=mv, types=types)
+        pred, sse = me_gpu.predict_frame(ref, f, me_gpu.SearchConfig(block_size=bs), cur=cur)
+        want = port.predict_frame(ref, mv, types, bs)
+        assert np.array_equal(pred, want)
+        assert sse == int(((cur.astype(np.int64) - want) ** 2).sum())
+    p = me_gpu.psnr(np.full((32, 32), 100, np.uint8), np.full((32, 32), 101, np.uint8))
+    assert p.mse == 1.0 and abs(p.psnr_db - 48.1308) < 1e-3
+    assert me_gpu.psnr(cur, cur).infinite()
+
+
+def test_estimate_field_prev(me_gpu, port):
+    rng = np.random.default_rng(9)
+    base = noise(rng, 64, 64)
+    cur, ref = shift_clamped(base, 2, 2), base
+    prev = np.full((64, 2), 4, np.int32)
+    pf = me_gpu.MotionField(8, 8, 8, vectors=prev.copy())
+    f, st, recs = me_gpu.estimate_field(me_gpu.Algo.PA, cur, ref, None, None, pf, me_gpu.SearchConfig(block_size=8), me_gpu.PrsConfig(), return_records=True)
+    want, wst = port.estimate_field(oracle.make_cfg(algo=4, search_range=7, block_size=8), cur, ref, prev_mv=prev)
+    assert_recs(recs, want)
+    assert f.at(0, 0) == (4, 4)
+    flat = np.full((64, 64), 99, np.uint8)
+    f2, _ = me_gpu.estimate_field(me_gpu.Algo.PA, flat, flat, None, None, pf, me_gpu.SearchConfig(block_size=8), me_gpu.PrsConfig())
+    assert f2.at(0, 0) == (0, 0)
