@@ -112,6 +112,14 @@ void me_b200_ctx_destroy(me_ctx* ctx);
 /* The cudaStream_t the host-pointer entry points of this context run on. */
 void* me_b200_ctx_stream(me_ctx* ctx);
 
+/* Per-kernel CUDA-event timing of the batched pipeline (off by default).
+ * When enabled, every run records events on its stream around each stage;
+ * me_b200_ctx_stage_ms waits for the last run and writes the stage durations
+ * (ms) in the order ME_STAGE_* into out[n] (n <= ME_NUM_STAGES). */
+enum { ME_STAGE_CLASSIFY = 0, ME_STAGE_SORT = 1, ME_STAGE_SEARCH = 2, ME_STAGE_MC_PSNR = 3, ME_NUM_STAGES = 4 };
+me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable);
+me_status me_b200_ctx_stage_ms(me_ctx* ctx, float* out, int n);
+
 /* SearchConfig::validate + PrsConfig::validate (estimators.cpp:139-150). */
 me_status me_b200_validate_config(const me_config* cfg);
 

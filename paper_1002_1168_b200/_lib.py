@@ -128,6 +128,8 @@ SIGNATURES = {
     "me_b200_ctx_destroy": (None, [P]),
     "me_b200_ctx_stream": (P, [P]),
     "me_b200_validate_config": (I, [C.POINTER(MeConfig)]),
+    "me_b200_ctx_set_profiling": (I, [P, I]),
+    "me_b200_ctx_stage_ms": (I, [P, C.POINTER(C.c_float), I]),
     "me_b200_run_sequences_dev": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P, P]),
     "me_b200_run_sequences": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P]),
     "me_b200_estimate_field": (I, [P, C.POINTER(MeConfig), I, I, P, P, P, P, P, I, I, P, P]),

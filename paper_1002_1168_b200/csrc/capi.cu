@@ -151,6 +151,8 @@ void me_b200_ctx_destroy(me_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
     for (DevBuf* b : {&c->types, &c->worklist, &c->counters, &c->tasks, &c->in_luma, &c->in_alpha,
                       &c->out_recs, &c->out_stats, &c->out_pred, &c->aux})
         b->release();
@@ -161,6 +163,27 @@ void me_b200_ctx_destroy(me_ctx* c) {
 }
 
 void* me_b200_ctx_stream(me_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (enable && !ctx->ev[0])
+        for (auto& e : ctx->ev) ME_CUDA(cudaEventCreate(&e));
+    ctx->profiling = enable != 0;
+    ctx->ev_valid = false;
+    return ok();
+}
+
+me_status me_b200_ctx_stage_ms(me_ctx* ctx, float* out, int n) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!ctx->profiling || !ctx->ev_valid)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "no profiled run on this context");
+    ME_CUDA(cudaEventSynchronize(ctx->ev[4]));
+    for (int i = 0; i < n && i < ME_NUM_STAGES; ++i)
+        ME_CUDA(cudaEventElapsedTime(&out[i], ctx->ev[i], ctx->ev[i + 1]));
+    return ok();
+}
 
 me_status me_b200_validate_config(const me_config* cfg) {
     me_status s = validate(cfg);
@@ -216,7 +239,8 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
     ME_CUDA(ctx->tasks.reserve(need));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, pred, ctx->tasks.p, ctx->tasks.cap,
-                           ctx->num_sms, st));
+                           ctx->num_sms, st, ctx->events()));
+    ctx->ev_valid = ctx->profiling;
     return ok();
 }
 
@@ -246,7 +270,8 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     ME_CUDA(mek::run_batch(b, *cfg, nullptr, static_cast<me_block_rec*>(ctx->out_recs.p),
                            static_cast<me_pair_stats*>(ctx->out_stats.p),
                            pred ? static_cast<uint8_t*>(ctx->out_pred.p) : nullptr, ctx->tasks.p,
-                           ctx->tasks.cap, ctx->num_sms, ctx->stream));
+                           ctx->tasks.cap, ctx->num_sms, ctx->stream, ctx->events()));
+    ctx->ev_valid = ctx->profiling;
     ME_CUDA(cudaMemcpyAsync(recs, ctx->out_recs.p, nrec * sizeof(me_block_rec),
                             cudaMemcpyDeviceToHost, ctx->stream));
     ME_CUDA(cudaMemcpyAsync(stats, ctx->out_stats.p, size_t(n_seq) * pairs * sizeof(me_pair_stats),

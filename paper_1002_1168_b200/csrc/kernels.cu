@@ -1266,7 +1266,7 @@ size_t scratch_bytes(const Batch& b, int algo) {
 
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
-                      size_t scratch_size, int num_sms, cudaStream_t st) {
+                      size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events) {
     const int algo = cfg.algo;
     const bool pa = algo == ME_ALGO_PA;
     const int nbins = pa ? b.steps() : 1;
@@ -1278,6 +1278,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     if (stats && (e = cudaMemsetAsync(stats, 0, sizeof(me_pair_stats) * size_t(b.n_seq) * b.pairs, st)))
         return e;
 
+    if (events) cudaEventRecord(events[0], st);
     ClassArgs ca;
     ca.b = b;
     ca.pa = pa ? 1 : 0;
@@ -1294,6 +1295,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         classify_kernel<<<grid, threads, hist_smem, st>>>(ca);
         if ((e = cudaGetLastError())) return e;
     }
+    if (events) cudaEventRecord(events[1], st);
     scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, s.offs, s.cursor);
     if ((e = cudaGetLastError())) return e;
     {
@@ -1304,6 +1306,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         if ((e = cudaGetLastError())) return e;
     }
     const int* nlist = s.offs + nbins;
+    if (events) cudaEventRecord(events[2], st);
 
     if (algo == ME_ALGO_ES) {
         EsArgs ea;
@@ -1364,6 +1367,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         if ((e = cudaGetLastError())) return e;
     }
 
+    if (events) cudaEventRecord(events[3], st);
     McArgs ma;
     ma.b = b;
     ma.recs = recs;
@@ -1376,6 +1380,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     const int segs = (b.W / 8) * b.H;
     dim3 grid((segs + 255) / 256, b.n_seq * b.pairs);
     mc_kernel<<<grid, 256, 0, st>>>(ma);
+    if (events) cudaEventRecord(events[4], st);
     return cudaGetLastError();
 }
 

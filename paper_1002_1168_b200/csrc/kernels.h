@@ -26,9 +26,12 @@ size_t scratch_bytes(const Batch& b, int algo);
 // `prev0` (nullable, [rows*cols][2] int32) supplies pair 0's temporal
 // candidates (estimate_field's prev_field); stats must hold n_seq*pairs
 // entries; pred is nullable.
+// `events` (nullable) = 5 events recorded before classify, before the sort,
+// before the search, before MC+PSNR and at the end.
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
-                      size_t scratch_size, int num_sms, cudaStream_t st);
+                      size_t scratch_size, int num_sms, cudaStream_t st,
+                      cudaEvent_t* events = nullptr);
 
 // Single-block entry points (all pointers device pointers; outputs in `out`,
 // an int64 array whose layout is documented at each launcher).

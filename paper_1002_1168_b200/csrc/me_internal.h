@@ -69,6 +69,11 @@ struct me_ctx {
     // inputs/outputs of the host-pointer entry points
     DevBuf in_luma, in_alpha, out_recs, out_stats, out_pred, aux;
     HostBuf pin_a, pin_b;
+    // stage timing
+    bool profiling = false;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool ev_valid = false;
+    cudaEvent_t* events() { return profiling ? ev : nullptr; }
 };
 
 #endif
