@@ -201,6 +201,12 @@ static me_status check_batch(const me_config* cfg, int n_seq, int n_frames, int 
     const int64_t nb = int64_t(n_seq) * (n_frames - cfg->ref_distance) * (W / cfg->block_size) *
                        (H / cfg->block_size);
     if (nb >= (int64_t(1) << 31)) return me_fail(ME_ERR_INVALID_ARGUMENT, "batch too large (2^31 blocks)");
+    if (n_seq >= 65536 || n_frames - cfg->ref_distance >= 65536 || H / cfg->block_size >= 32768 ||
+        W / cfg->block_size >= 65536)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "batch geometry exceeds the work-list encoding");
+    if (cfg->algo == ME_ALGO_PA && (W / cfg->block_size - 1) + 2 * (H / cfg->block_size - 1) +
+                                           (n_frames - cfg->ref_distance) > 12000)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "wavefront longer than 12000 steps");
     if (int64_t(W - cfg->block_size + 1) * (H - cfg->block_size + 1) >= (int64_t(1) << 24))
         return me_fail(ME_ERR_INVALID_ARGUMENT, "frame too large for the packed ES key");
     return ME_OK;

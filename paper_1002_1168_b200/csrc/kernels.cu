@@ -163,13 +163,76 @@ __device__ __forceinline__ uint32_t row_shape(const uint8_t* ca, const uint8_t* 
     return m;
 }
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+// Rounds 4*s/4 to nearest, ties to even (std::nearbyint, compensation.cpp:64).
+__device__ __forceinline__ int round_q4(int i4) {
+    const int q = i4 >> 2, rem = i4 & 3;
+    if (rem < 2) return q;
+    if (rem > 2) return q + 1;
+    return q + (q & 1);
+}
+
+// Sum of squared differences of 4 byte lanes (IDP4A on the packed |a-b|).
+__device__ __forceinline__ uint32_t sq4(uint32_t a, uint32_t b, uint32_t acc) {
+    const uint32_t d = __vabsdiffu4(a, b);
+    return __dp4a(d, d, acc);
+}
+
+// Squared error of one block row of cur against its motion-compensated
+// prediction (predict_frame, compensation.cpp:42-66): clamped full-pel copy or
+// half-pel bilinear rounded half to even.
+__device__ uint32_t row_sse(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y,
+                            int bs, int dx2, int dy2) {
+    uint32_t s = 0;
+    for (int x = x0; x < x0 + bs; ++x) {
+        const int p = ((dx2 | dy2) & 1) == 0 ? pxc(ref, W, H, x + (dx2 >> 1), y + (dy2 >> 1))
+                                             : round_q4(interp4(ref, W, H, 2 * x + dx2, 2 * y + dy2));
+        const int d = int(cur[size_t(y) * W + x]) - p;
+        s += uint32_t(d * d);
+    }
+    return s;
+}
+
+// Same for a full-pel vector (pels) whose displaced row lies inside the frame
+// and a word-aligned current row.
+__device__ __forceinline__ uint32_t row_sse_fp(const uint8_t* cur, const uint8_t* ref, int W, int x0,
+                                               int y, int bs, int dx, int dy) {
+    const uint8_t* c = cur + size_t(y) * W + x0;
+    const uint8_t* r = ref + size_t(y + dy) * W + x0 + dx;
+    uint32_t s = 0;
+    if (bs == 8) {
+        uint32_t r0, r1;
+        ld8u(r, r0, r1);
+        s = sq4(ldg32(c), r0, s);
+        s = sq4(ldg32(c + 4), r1, s);
+    } else {
+        uint32_t rr[4];
+        ld16u(r, rr);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s = sq4(ldg32(c + 4 * i), rr[i], s);
+    }
+    return s;
+}
+
+// Per-pair SearchStats + SSE accumulation (me_pair_stats field order).
+__device__ __forceinline__ void add_stats(me_pair_stats* st, uint32_t sse, uint32_t cmp,
+                                          uint32_t dpd, int type) {
+    unsigned long long* s = reinterpret_cast<unsigned long long*>(st);
+    if (sse) atomicAdd(s + 5, static_cast<unsigned long long>(sse));
+    if (cmp) atomicAdd(s + 0, static_cast<unsigned long long>(cmp));
+    if (dpd) atomicAdd(s + 1, static_cast<unsigned long long>(dpd));
+    atomicAdd(s + (type == ME_OPAQUE ? 2 : (type == ME_BOUNDARY ? 3 : 4)), 1ull);
+}
+
+// The MV word is the whole payload a dependent block needs, and it is a single
+// 32-bit word: relaxed gpu-scope accesses suffice (no acquire fence, which
+// would invalidate the SM's L1 on every poll).
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t pack_mv(int dx, int dy) {
@@ -186,7 +249,7 @@ __device__ __forceinline__ void write_rec(me_block_rec* r, int dx, int dy, uint3
     w[2] = (cmp & 0xFFFF) | (dpd << 16);
     w[3] = (iters & 0xFF) | ((type & 0xFF) << 8);
     if (release)
-        st_release(w, pack_mv(dx, dy));
+        st_relaxed(w, pack_mv(dx, dy));
     else
         w[0] = pack_mv(dx, dy);
 }
@@ -206,6 +269,8 @@ struct ClassArgs {
     uint8_t* types;      // same indexing
     int* hist;           // [nbins]
     int nbins;
+    me_pair_stats* stats;  // [n_seq][pairs]: transparent blocks' count and SSE
+    int skew;              // PA: key = h + 2v + p + skew * seq (staggers the sequences)
 };
 
 __device__ __forceinline__ int classify_one(const uint8_t* a, int W, int x0, int y0, int bs) {
@@ -213,41 +278,88 @@ __device__ __forceinline__ int classify_one(const uint8_t* a, int W, int x0, int
     uint32_t any = 0, nz = 1;
     for (int y = 0; y < bs; ++y) {
         const uint8_t* row = a + size_t(y0 + y) * W + x0;
-        for (int i = 0; i < bs; i += 4) {
-            const uint32_t w = ldg32(row + i);
-            any |= w;
-            nz &= __vcmpeq4(w, 0u) == 0u;
+        for (int i = 0; i < bs; i += 8) {
+            const uint2 w = *reinterpret_cast<const uint2*>(row + i);
+            any |= w.x | w.y;
+            nz &= (__vcmpeq4(w.x, 0u) | __vcmpeq4(w.y, 0u)) == 0u;
         }
     }
     return !any ? ME_TRANSPARENT : (nz ? ME_OPAQUE : ME_BOUNDARY);
 }
 
-__global__ void classify_kernel(ClassArgs a) {
+// SSE of a block predicted with the zero vector (transparent blocks,
+// compensation.cpp:45): cur block vs the co-located ref block.
+__device__ __forceinline__ uint32_t block_sse0(const uint8_t* cur, const uint8_t* ref, int W,
+                                               int x0, int y0, int bs) {
+    uint32_t s = 0;
+    for (int y = 0; y < bs; ++y) {
+        const size_t o = size_t(y0 + y) * W + x0;
+        for (int i = 0; i < bs; i += 8) {
+            const uint2 c = __ldg(reinterpret_cast<const uint2*>(cur + o + i));
+            const uint2 r = __ldg(reinterpret_cast<const uint2*>(ref + o + i));
+            s = sq4(c.x, r.x, s);
+            s = sq4(c.y, r.y, s);
+        }
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
     extern __shared__ int s_hist[];
     const Batch& b = a.b;
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const int64_t n = b.nblocks();
-    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
-         g += int64_t(gridDim.x) * blockDim.x) {
-        const int h = int(g % b.cols);
-        int64_t t = g / b.cols;
-        const int v = int(t % b.rows);
-        t /= b.rows;
-        const int p = int(t % b.pairs);
-        const int seq = int(t / b.pairs);
-        const size_t plane = size_t(b.W) * b.H;
-        const uint8_t* a_cur =
-            b.alpha ? b.alpha + (size_t(seq) * b.F + p + b.d) * plane : nullptr;
-        const int ty = classify_one(a_cur, b.W, h * b.bs, v * b.bs, b.bs);
-        a.types[g] = uint8_t(ty);
-        uint4 r;
-        r.x = ty == ME_TRANSPARENT ? 0u : kSentinel;
-        r.y = 0u;
-        r.z = 0u;
-        r.w = uint32_t(ty) << 8;
-        *reinterpret_cast<uint4*>(a.recs + g) = r;
-        if (ty != ME_TRANSPARENT) atomicAdd(&s_hist[a.pa ? h + 2 * v + p : 0], 1);
+    const size_t plane = size_t(b.W) * b.H;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    // uniform trip count so whole warps reach the warp-level reductions
+    for (int64_t g0 = int64_t(blockIdx.x) * blockDim.x; g0 < n; g0 += stride) {
+        const int64_t g = g0 + threadIdx.x;
+        uint32_t sse = 0, n_t = 0;
+        int64_t gp = -1;
+        if (g < n) {
+            const int h = int(g % b.cols);
+            int64_t t = g / b.cols;
+            const int v = int(t % b.rows);
+            gp = t / b.rows;  // seq * pairs + p
+            const int p = int(gp % b.pairs);
+            const int seq = int(gp / b.pairs);
+            const size_t fcur = size_t(seq) * b.F + p + b.d, fref = size_t(seq) * b.F + p;
+            const uint8_t* a_cur = b.alpha ? b.alpha + fcur * plane : nullptr;
+            const int ty = classify_one(a_cur, b.W, h * b.bs, v * b.bs, b.bs);
+            a.types[g] = uint8_t(ty);
+            uint4 r;
+            r.x = ty == ME_TRANSPARENT ? 0u : kSentinel;
+            r.y = 0u;
+            r.z = 0u;
+            r.w = uint32_t(ty) << 8;
+            *reinterpret_cast<uint4*>(a.recs + g) = r;
+            if (ty != ME_TRANSPARENT) {
+                atomicAdd(&s_hist[a.pa ? h + 2 * v + p + a.skew * seq : 0], 1);
+            } else if (a.stats) {
+                sse = block_sse0(b.luma + fcur * plane, b.luma + fref * plane, b.W, h * b.bs,
+                                 v * b.bs, b.bs);
+                n_t = 1;
+            }
+        }
+        if (a.stats) {
+            const int64_t gp0 = __shfl_sync(0xFFFFFFFFu, gp, 0);
+            const bool uniform = __all_sync(0xFFFFFFFFu, gp == gp0 || gp < 0);
+            if (uniform) {
+                const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, sse);
+                const uint32_t wn = __reduce_add_sync(0xFFFFFFFFu, n_t);
+                if (lane == 0 && wn) {
+                    unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp0);
+                    if (ws) atomicAdd(st + 5, static_cast<unsigned long long>(ws));
+                    atomicAdd(st + 4, static_cast<unsigned long long>(wn));
+                }
+            } else if (n_t) {
+                unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp);
+                if (sse) atomicAdd(st + 5, static_cast<unsigned long long>(sse));
+                atomicAdd(st + 4, 1ull);
+            }
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x)
@@ -284,7 +396,20 @@ __global__ void scan_kernel(const int* hist, int nbins, int* offs, int* cursor) 
 
 // Scatter estimated block ids into key order (per-CTA ranges per bin keep the
 // global atomics to one per (CTA, bin)).
-__global__ void fill_kernel(ClassArgs a, int* cursor, uint32_t* list) {
+__device__ __forceinline__ void split_block(const Batch& b, int64_t g, int& h, int& v, int& p,
+                                            int& seq) {
+    h = int(g % b.cols);
+    int64_t t = g / b.cols;
+    v = int(t % b.rows);
+    t /= b.rows;
+    p = int(t % b.pairs);
+    seq = int(t / b.pairs);
+}
+
+// Scatter estimated blocks into key order as decoded list entries
+// {h | v << 16 | boundary << 31, p | seq << 16} (per-CTA ranges per bin keep
+// the global atomics to one per (CTA, bin)).
+__global__ void fill_kernel(ClassArgs a, int* cursor, uint2* list) {
     extern __shared__ int s_cnt[];  // [nbins] counts, then [nbins] bases
     int* s_base = s_cnt + a.nbins;
     const Batch& b = a.b;
@@ -294,17 +419,10 @@ __global__ void fill_kernel(ClassArgs a, int* cursor, uint32_t* list) {
     const int64_t chunk = int64_t(blockDim.x) * 8;
     const int64_t g0 = int64_t(blockIdx.x) * chunk;
     for (int64_t g = g0 + threadIdx.x; g < min(g0 + chunk, n); g += blockDim.x) {
-        const int ty = a.types[g];
-        if (ty == ME_TRANSPARENT) continue;
-        int key = 0;
-        if (a.pa) {
-            const int h = int(g % b.cols);
-            int64_t t = g / b.cols;
-            const int v = int(t % b.rows);
-            const int p = int((t / b.rows) % b.pairs);
-            key = h + 2 * v + p;
-        }
-        atomicAdd(&s_cnt[key], 1);
+        if (a.types[g] == ME_TRANSPARENT) continue;
+        int h, v, p, seq;
+        split_block(b, g, h, v, p, seq);
+        atomicAdd(&s_cnt[a.pa ? h + 2 * v + p + a.skew * seq : 0], 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
@@ -315,16 +433,12 @@ __global__ void fill_kernel(ClassArgs a, int* cursor, uint32_t* list) {
     for (int64_t g = g0 + threadIdx.x; g < min(g0 + chunk, n); g += blockDim.x) {
         const int ty = a.types[g];
         if (ty == ME_TRANSPARENT) continue;
-        int key = 0;
-        if (a.pa) {
-            const int h = int(g % b.cols);
-            int64_t t = g / b.cols;
-            const int v = int(t % b.rows);
-            const int p = int((t / b.rows) % b.pairs);
-            key = h + 2 * v + p;
-        }
+        int h, v, p, seq;
+        split_block(b, g, h, v, p, seq);
+        const int key = a.pa ? h + 2 * v + p + a.skew * seq : 0;
         const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
-        list[pos] = uint32_t(g) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u);
+        list[pos] = make_uint2(uint32_t(h) | (uint32_t(v) << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u),
+                               uint32_t(p) | (uint32_t(seq) << 16));
     }
 }
 
@@ -343,23 +457,25 @@ __global__ void fill_kernel(ClassArgs a, int* cursor, uint32_t* list) {
 struct EsArgs {
     Batch b;
     int S;
-    const uint32_t* list;
+    const uint2* list;
     const int* nlist;  // device count (offs[nbins])
     int* counter;
     me_block_rec* recs;
     int band_rows_max;  // staged rows per band (multiple of K, + BS - 1 added on top)
+    me_pair_stats* stats;
 };
 
 constexpr int kEsThreads = 256;
 
-__device__ __forceinline__ void decode_block(const Batch& b, uint32_t g, int& h, int& v, int& p,
-                                             int& seq) {
-    h = int(g % uint32_t(b.cols));
-    uint32_t t = g / uint32_t(b.cols);
-    v = int(t % uint32_t(b.rows));
-    t /= uint32_t(b.rows);
-    p = int(t % uint32_t(b.pairs));
-    seq = int(t / uint32_t(b.pairs));
+// Unpacks a work-list entry; returns the global block index g.
+__device__ __forceinline__ uint32_t decode_entry(const Batch& b, uint2 e, int& h, int& v, int& p,
+                                                 int& seq, bool& boundary) {
+    h = int(e.x & 0xFFFF);
+    v = int((e.x >> 16) & 0x7FFF);
+    boundary = (e.x & kBoundaryBit) != 0;
+    p = int(e.y & 0xFFFF);
+    seq = int(e.y >> 16);
+    return ((uint32_t(seq) * b.pairs + p) * b.rows + v) * b.cols + h;
 }
 
 template <int BS, int K>
@@ -476,6 +592,7 @@ __global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ unsigned long long s_best[kEsThreads / 32];
     __shared__ int s_item;
+    __shared__ int s_res[4];
     const Batch& b = a.b;
     const int n = *a.nlist;
     const size_t plane = size_t(b.W) * b.H;
@@ -486,19 +603,35 @@ __global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
         __syncthreads();
         const int item = s_item;
         if (item >= n) return;
-        const uint32_t e = a.list[item];
-        const uint32_t g = e & ~kBoundaryBit;
         int h, v, p, seq;
-        decode_block(b, g, h, v, p, seq);
+        bool boundary;
+        const uint32_t g = decode_entry(b, a.list[item], h, v, p, seq, boundary);
         const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
         const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
         int dx, dy;
         uint32_t sad, cmp;
         es_block<BS, K>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, s_best, dx, dy,
                         sad, cmp);
-        if (threadIdx.x == 0)
-            write_rec(a.recs + g, 2 * dx, 2 * dy, sad * 4u, cmp, 0, 0,
-                      (e & kBoundaryBit) ? ME_BOUNDARY : ME_OPAQUE, false);
+        if (threadIdx.x == 0) {
+            s_res[0] = dx;
+            s_res[1] = dy;
+            s_res[2] = int(sad);
+            s_res[3] = int(cmp);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // fused predict_frame + psnr SSE of this block at its vector
+            const int lane = threadIdx.x;
+            const int rdx = s_res[0], rdy = s_res[1];
+            uint32_t sse = lane < BS ? row_sse_fp(cur, ref, b.W, h * BS, v * BS + lane, BS, rdx, rdy) : 0u;
+            sse = __reduce_add_sync(0xFFFFFFFFu, sse);
+            if (lane == 0) {
+                const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+                write_rec(a.recs + g, 2 * rdx, 2 * rdy, uint32_t(s_res[2]) * 4u, uint32_t(s_res[3]), 0, 0,
+                          ty, false);
+                if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, uint32_t(s_res[3]), 0, ty);
+            }
+        }
     }
 }
 
@@ -621,10 +754,11 @@ __device__ void ring_block(int algo, const uint8_t* cur, const uint8_t* ref, int
 struct RingArgs {
     Batch b;
     int algo, S;
-    const uint32_t* list;
+    const uint2* list;
     const int* nlist;
     me_block_rec* recs;
     int bitmap_words;  // per warp
+    me_pair_stats* stats;
 };
 
 __global__ void __launch_bounds__(256) ring_kernel(RingArgs a) {
@@ -636,19 +770,22 @@ __global__ void __launch_bounds__(256) ring_kernel(RingArgs a) {
     const Batch& b = a.b;
     const size_t plane = size_t(b.W) * b.H;
     for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
-        const uint32_t e = a.list[item];
-        const uint32_t g = e & ~kBoundaryBit;
         int h, v, p, seq;
-        decode_block(b, g, h, v, p, seq);
+        bool boundary;
+        const uint32_t g = decode_entry(b, a.list[item], h, v, p, seq, boundary);
         const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
         const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
         int dx, dy;
         uint32_t sad, cmp;
         ring_block(a.algo, cur, ref, b.W, b.H, h * b.bs, v * b.bs, b.bs, a.S, bitmap, lane, dx, dy,
                    sad, cmp);
-        if (lane == 0)
-            write_rec(a.recs + g, 2 * dx, 2 * dy, sad * 4u, cmp, 0, 0,
-                      (e & kBoundaryBit) ? ME_BOUNDARY : ME_OPAQUE, false);
+        uint32_t sse = lane < b.bs ? row_sse_fp(cur, ref, b.W, h * b.bs, v * b.bs + lane, b.bs, dx, dy) : 0u;
+        sse = __reduce_add_sync(0xFFFFFFFFu, sse);
+        if (lane == 0) {
+            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+            write_rec(a.recs + g, 2 * dx, 2 * dy, sad * 4u, cmp, 0, 0, ty, false);
+            if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, cmp, 0, ty);
+        }
         __syncwarp();
     }
 }
@@ -840,94 +977,347 @@ __device__ PaResult pa_block(const PaParams& P, const PaBlock& B, int lane, bool
                              const int cdx[4], const int cdy[4], uint32_t* bitmap,
                              uint32_t* brs_scores = nullptr, int* brs_kinds = nullptr) {
     const int k = lane >> 3;
-    const int vx = clip_comp(cdx[k], B.w.lo_x, B.w.hi_x);
-    const int vy = clip_comp(cdy[k], B.w.lo_y, B.w.hi_y);
+    int rx = cdx[0], ry = cdy[0];
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+        if (k == i) {
+            rx = cdx[i];
+            ry = cdy[i];
+        }
+    const int vx = clip_comp(rx, B.w.lo_x, B.w.hi_x);
+    const int vy = clip_comp(ry, B.w.lo_y, B.w.hi_y);
     const bool shape = boundary && (k < 3 || P.bt_shape);
     const uint32_t s = score4(P, B, lane, vx, vy, shape);
-    uint32_t sc[4];
+    uint32_t best = 0;
     int bx = 0, by = 0, win = 0;
     for (int i = 0; i < 4; ++i) {
-        sc[i] = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
+        const uint32_t si = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
         const int ix = __shfl_sync(0xFFFFFFFFu, vx, 8 * i), iy = __shfl_sync(0xFFFFFFFFu, vy, 8 * i);
-        if (i == 0 || sc[i] < sc[win]) {
+        if (brs_scores) brs_scores[i] = si;
+        if (i == 0 || si < best) {
             win = i;
+            best = si;
             bx = ix;
             by = iy;
         }
     }
-    if (brs_scores)
-        for (int i = 0; i < 4; ++i) brs_scores[i] = sc[i];
     if (brs_kinds)
         for (int i = 0; i < 4; ++i) brs_kinds[i] = boundary && (i < 3 || P.bt_shape);
     const bool win_shape = boundary && (win < 3 || P.bt_shape);
-    return prs_warp(P, B, lane, bx, by, win_shape ? kInf : sc[win], bitmap);
+    return prs_warp(P, B, lane, bx, by, win_shape ? kInf : best, bitmap);
 }
 
 struct PaArgs {
     Batch b;
     PaParams P;
-    const uint32_t* list;
+    const uint2* list;
     const int* nlist;
     me_block_rec* recs;
     const int32_t* prev0;  // pair 0's temporal candidates or null
+    me_pair_stats* stats;
+    int fast;              // integer-pel patch fast path allowed (step 2, max_iter <= 4)
+    int warp_words;        // shared words per warp
 };
 
-__global__ void __launch_bounds__(512) pa_kernel(PaArgs a) {
+// Fast path geometry: with step 2 (integer pel) and at most R = 4 PRS
+// iterations, every position prs_refine can evaluate lies within +/-4 pels of
+// the BRS winner, so one (BS+8)^2 reference patch per candidate, staged once
+// in shared memory, holds all the data the block needs: the BRS texture
+// scores, every PRS neighbour cost (evaluated lazily, exactly the positions
+// the reference visits) and the final prediction SSE.
+template <int BS>
+struct PaFast {
+    static constexpr int R = 4;
+    static constexpr int L = 2 * R + 1;          // lattice side
+    static constexpr int PR = BS + 2 * R;        // patch rows
+    static constexpr int PB = BS + 2 * R;        // patch bytes per row
+    static constexpr int PWW = PB / 4 + 1;       // words per row (+1: unaligned reads)
+    static constexpr int NW = BS / 4;            // words per block row
+    static constexpr int PATCH_WORDS = PR * PWW;
+    static constexpr int CUR_WORDS = BS * NW;
+    static constexpr int WORDS = 4 * PATCH_WORDS + CUR_WORDS + 4;  // patches, cur block, visited
+};
+
+// Loads patch row r of candidate centre (cx, cy) (pels) into smem words;
+// rows/columns outside the frame are edge-replicated (only inadmissible
+// positions ever read them).
+template <int BS>
+__device__ __forceinline__ void load_patch_row(const uint8_t* ref, int W, int H, int x0, int y0,
+                                               int cx, int cy, int r, uint32_t* dst) {
+    using F = PaFast<BS>;
+    const int y = clampi(y0 + cy - F::R + r, 0, H - 1);
+    const int xs = x0 + cx - F::R;
+    const uint8_t* row = ref + size_t(y) * W;
+    if (xs >= 0 && xs + F::PB <= W) {
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(row + xs);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~uintptr_t(3));
+        const uint32_t sh = uint32_t(ad & 3) * 8;
+        uint32_t prev = __ldg(w);
+#pragma unroll
+        for (int i = 0; i < F::PB / 4; ++i) {
+            const uint32_t nxt = (i + 1 < F::PB / 4 || sh) ? __ldg(w + i + 1) : 0u;
+            dst[i] = __funnelshift_r(prev, nxt, sh);
+            prev = nxt;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < F::PB / 4; ++i) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v |= uint32_t(row[clampi(xs + 4 * i + k, 0, W - 1)]) << (8 * k);
+            dst[i] = v;
+        }
+    }
+    dst[F::PB / 4] = 0u;
+}
+
+// SAD of block row r against the patch at lattice offset (i, j) in [0, 2R]^2.
+template <int BS>
+__device__ __forceinline__ uint32_t patch_row_sad(const uint32_t* pw, const uint32_t* cw, int i, int j,
+                                                  int r) {
+    using F = PaFast<BS>;
+    const uint32_t* row = pw + (j + r) * F::PWW + (i >> 2);
+    const uint32_t* c = cw + r * F::NW;
+    const uint32_t sh = uint32_t(i & 3) * 8;
+    uint32_t acc = 0, w0 = row[0];
+#pragma unroll
+    for (int k = 0; k < F::NW; ++k) {
+        const uint32_t w1 = row[k + 1];
+        acc = vad4(c[k], __funnelshift_r(w0, w1, sh), acc);
+        w0 = w1;
+    }
+    return acc;
+}
+
+// gather_candidates (estimators.cpp:238-255): lane i < 4 returns candidate i's
+// MV word (A, B, C, T), waiting for dependencies still in flight.
+__device__ __forceinline__ uint32_t fetch_candidate(const PaArgs& a, uint32_t g, int h, int v, int p,
+                                                    int lane) {
+    const Batch& b = a.b;
+    uint32_t mvw = 0;
+    if (lane < 4) {
+        const uint32_t* src = nullptr;
+        if (lane == 0 && h > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - 1);
+        if (lane == 1 && v > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - b.cols);
+        if (lane == 2 && v > 0 && h + 1 < b.cols)
+            src = reinterpret_cast<const uint32_t*>(a.recs + g - b.cols + 1);
+        if (lane == 3 && p > 0)
+            src = reinterpret_cast<const uint32_t*>(a.recs + g - uint32_t(b.rows) * b.cols);
+        if (src) {
+            mvw = ld_relaxed(src);
+            while (mvw == kSentinel) {
+                __nanosleep(32);
+                mvw = ld_relaxed(src);
+            }
+        } else if (lane == 3 && a.prev0) {
+            const int i = v * b.cols + h;
+            mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+        }
+    }
+    return mvw;
+}
+
+// Integer-pel fast path for one block (warp-cooperative): brs_select +
+// prs_refine decisions identical to the reference; also returns the block's
+// prediction SSE.  The current block is already in smem (cw).
+template <int BS>
+__device__ PaResult pa_fast_block(const PaParams& P, const PaBlock& B, int lane, bool boundary,
+                                  int myvx, int myvy, uint32_t* ws, uint32_t& sse_out) {
+    // myvx/myvy: clipped (even) candidate (lane >> 3) of this lane, half-pel
+    using F = PaFast<BS>;
+    uint32_t* patch = ws;                        // [4][PR][PWW]
+    const uint32_t* cw = ws + 4 * F::PATCH_WORDS;  // [BS][NW]
+    uint32_t* vis = ws + 4 * F::PATCH_WORDS + F::CUR_WORDS;  // [3] lattice bitmap
+    // --- stage the four candidate patches -----------------------------------
+    const int c = lane >> 3, sub = lane & 7;
+    const int ccx = myvx >> 1, ccy = myvy >> 1;  // pels
+    for (int r = sub; r < F::PR; r += 8)
+        load_patch_row<BS>(B.ref, P.W, P.H, B.x0, B.y0, ccx, ccy, r,
+                           patch + c * F::PATCH_WORDS + r * F::PWW);
+    // shape scores (boundary blocks) read the alpha planes directly
+    const bool shape = boundary && (c < 3 || P.bt_shape);
+    uint32_t s = 0;
+    if (shape)
+        for (int r = sub; r < BS; r += 8)
+            s += row_shape(B.ca, B.ra, P.W, P.H, B.x0, B.y0 + r, BS, ccx, ccy) * (255u * 4u);
+    if (lane < 3) vis[lane] = 0u;
+    __syncwarp();
+    if (!shape)
+        for (int r = sub; r < BS; r += 8)
+            s += 4u * patch_row_sad<BS>(patch + c * F::PATCH_WORDS, cw, F::R, F::R, r);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
+    // brs_select: strict <, so A, B, C, T win ties in that order (estimators.cpp:295)
+    uint32_t best = __shfl_sync(0xFFFFFFFFu, s, 0);
+    int win = 0;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+        const uint32_t si = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
+        if (si < best) {
+            best = si;
+            win = i;
+        }
+    }
+    const bool win_shape = boundary && (win < 3 || P.bt_shape);
+    const int wx = __shfl_sync(0xFFFFFFFFu, myvx, 8 * win), wy = __shfl_sync(0xFFFFFFFFu, myvy, 8 * win);
+    const uint32_t* pw = patch + win * F::PATCH_WORDS;
+    // --- prs_refine (estimators.cpp:311-382) ---------------------------------
+    int ci = F::R, cj = F::R;
+    uint32_t ccost = best;
+    if (win_shape) {  // the centre's texture cost was not computed by BRS
+        uint32_t t = 0;
+        for (int r = lane; r < BS; r += 32) t += patch_row_sad<BS>(pw, cw, ci, cj, r);
+        ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
+    }
+    if (lane == 0) {
+        const int bit = F::R * F::L + F::R;
+        vis[bit >> 5] |= 1u << (bit & 31);
+    }
+    __syncwarp();
+    uint32_t dpd = 1, iters = 0;
+    const int k = lane >> 2, q = lane & 3;
+    const bool leader = q == 0;
+    for (int it = 0; it < P.max_iter; ++it) {
+        if (ccost == 0) break;  // already a global minimum (:341)
+        const int ni = ci + c_off8[k][0], nj = cj + c_off8[k][1];
+        const int vx = wx + 2 * (ni - F::R), vy = wy + 2 * (nj - F::R);
+        const bool adm = vx >= B.w.lo_x && vx <= B.w.hi_x && vy >= B.w.lo_y && vy <= B.w.hi_y;
+        uint32_t part = 0;
+        if (adm)
+            for (int r = q; r < BS; r += 4) part += patch_row_sad<BS>(pw, cw, ni, nj, r);
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
+        const uint32_t cost = 4u * part;
+        bool fresh = false;
+        if (adm && leader) {  // unique aggregate evaluations (:321-332)
+            const int bit = nj * F::L + ni;
+            const uint32_t m = 1u << (bit & 31);
+            fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
+        }
+        dpd += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
+        const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, (adm && leader) ? cost : kInf);
+        if (m >= ccost) break;  // centre kept (:376)
+        const uint32_t ties = __ballot_sync(0xFFFFFFFFu, adm && leader && cost == m);
+        int w;
+        if (__popc(ties) == 1) {
+            w = (__ffs(ties) - 1) >> 2;
+        } else {
+            // stable descending sort by off . dir (:357-362): the first tied
+            // neighbour in sorted order has the largest key, lowest index on equal keys
+            double dir_x, dir_y;
+            prs_direction(P, B, lane, wx + 2 * (ci - F::R), wy + 2 * (cj - F::R), dir_x, dir_y);
+            w = -1;
+            double bestkey = 0.0;
+            for (int o = 0; o < 8; ++o) {
+                if (!((ties >> (4 * o)) & 1u)) continue;
+                const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x),
+                                             __dmul_rn(double(c_off8[o][1]), dir_y));
+                if (w < 0 || key > bestkey) {
+                    w = o;
+                    bestkey = key;
+                }
+            }
+        }
+        ci += c_off8[w][0];
+        cj += c_off8[w][1];
+        ccost = m;
+        ++iters;
+    }
+    // --- fused predict_frame + psnr SSE at the final vector ------------------
+    uint32_t sse = 0;
+    for (int r = lane; r < BS; r += 32) {
+        const uint32_t* row = pw + (cj + r) * F::PWW + (ci >> 2);
+        const uint32_t sh = uint32_t(ci & 3) * 8;
+        uint32_t w0 = row[0];
+#pragma unroll
+        for (int kk = 0; kk < F::NW; ++kk) {
+            const uint32_t w1 = row[kk + 1];
+            sse = sq4(cw[r * F::NW + kk], __funnelshift_r(w0, w1, sh), sse);
+            w0 = w1;
+        }
+    }
+    sse_out = __reduce_add_sync(0xFFFFFFFFu, sse);
+    PaResult res;
+    res.dx = wx + 2 * (ci - F::R);
+    res.dy = wy + 2 * (cj - F::R);
+    res.cost_q4 = ccost;
+    res.dpd = dpd;
+    res.iters = iters;
+    return res;
+}
+
+template <int BS>
+__global__ void __launch_bounds__(512, BS == 8 ? 2 : 1) pa_kernel(PaArgs a) {
     extern __shared__ uint32_t s_pa[];
+    using F = PaFast<BS>;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t* bitmap = s_pa + wid * a.P.bm_words;
+    uint32_t* ws = s_pa + wid * a.warp_words;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     const int n = *a.nlist;
     const Batch& b = a.b;
     const PaParams& P = a.P;
     const size_t plane = size_t(b.W) * b.H;
-    const uint32_t pair_blocks = uint32_t(b.rows) * b.cols;
-    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
-        const uint32_t e = a.list[item];
-        const uint32_t g = e & ~kBoundaryBit;
-        const bool boundary = (e & kBoundaryBit) != 0;
+    int item = blockIdx.x * (blockDim.x >> 5) + wid;
+    uint2 e = item < n ? a.list[item] : make_uint2(0u, 0u);
+    for (; item < n; item += nwarps) {
+        const uint2 e_next = item + nwarps < n ? a.list[item + nwarps] : make_uint2(0u, 0u);  // prefetch
         int h, v, p, seq;
-        decode_block(b, g, h, v, p, seq);
-        // gather_candidates (estimators.cpp:238-255): lanes 0..3 fetch A, B, C, T
-        uint32_t mvw = 0;
-        if (lane < 4) {
-            const uint32_t* src = nullptr;
-            if (lane == 0 && h > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - 1);
-            if (lane == 1 && v > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - b.cols);
-            if (lane == 2 && v > 0 && h + 1 < b.cols)
-                src = reinterpret_cast<const uint32_t*>(a.recs + g - b.cols + 1);
-            if (lane == 3 && p > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - pair_blocks);
-            if (src) {
-                mvw = ld_acquire(src);
-                while (mvw == kSentinel) {
-                    __nanosleep(64);
-                    mvw = ld_acquire(src);
-                }
-            } else if (lane == 3 && a.prev0) {
-                const int i = v * b.cols + h;
-                mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+        bool boundary;
+        const uint32_t g = decode_entry(b, e, h, v, p, seq, boundary);
+        PaBlock B;
+        const size_t fc = size_t(seq) * b.F + p + b.d, fr = size_t(seq) * b.F + p;
+        B.cur = b.luma + fc * plane;
+        B.ref = b.luma + fr * plane;
+        B.ca = b.alpha ? b.alpha + fc * plane : nullptr;
+        B.ra = b.alpha ? b.alpha + fr * plane : nullptr;
+        B.x0 = h * BS;
+        B.y0 = v * BS;
+        B.w = hp_window(B.x0, B.y0, BS, P.W, P.H, P.S);
+        // round A: current block into smem + candidate MVs, concurrently
+        if (a.fast && lane < BS) {
+            uint32_t* dst = ws + 4 * F::PATCH_WORDS + lane * F::NW;
+            const uint8_t* src = B.cur + size_t(B.y0 + lane) * b.W + B.x0;
+            if (BS == 8) {
+                const uint2 w = __ldg(reinterpret_cast<const uint2*>(src));
+                dst[0] = w.x;
+                dst[1] = w.y;
+            } else {
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(src));
+                dst[0] = w.x;
+                dst[1] = w.y;
+                dst[2] = w.z;
+                dst[3] = w.w;
             }
         }
-        int cdx[4], cdy[4];
+        const uint32_t mvw = fetch_candidate(a, g, h, v, p, lane);
+        const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, lane >> 3);
+        const int myvx = clip_comp(mv_dx(mine), B.w.lo_x, B.w.hi_x);  // clip_to_window (:275-276)
+        const int myvy = clip_comp(mv_dy(mine), B.w.lo_y, B.w.hi_y);
+        const bool odd = __any_sync(0xFFFFFFFFu, ((myvx | myvy) & 1) != 0);
+        PaResult r;
+        uint32_t sse;
+        if (a.fast && !odd) {
+            r = pa_fast_block<BS>(P, B, lane, boundary, myvx, myvy, ws, sse);
+        } else {
+            int rdx[4], rdy[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t w = __shfl_sync(0xFFFFFFFFu, mvw, i);
-            cdx[i] = mv_dx(w);
-            cdy[i] = mv_dy(w);
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t w = __shfl_sync(0xFFFFFFFFu, mvw, i);
+                rdx[i] = mv_dx(w);
+                rdy[i] = mv_dy(w);
+            }
+            r = pa_block(P, B, lane, boundary, rdx, rdy, ws);
+            uint32_t s = lane < BS ? row_sse(B.cur, B.ref, P.W, P.H, B.x0, B.y0 + lane, BS, r.dx, r.dy) : 0u;
+            sse = __reduce_add_sync(0xFFFFFFFFu, s);
         }
-        PaBlock B;
-        B.cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
-        B.ref = b.luma + (size_t(seq) * b.F + p) * plane;
-        B.ca = b.alpha ? b.alpha + (size_t(seq) * b.F + p + b.d) * plane : nullptr;
-        B.ra = b.alpha ? b.alpha + (size_t(seq) * b.F + p) * plane : nullptr;
-        B.x0 = h * P.bs;
-        B.y0 = v * P.bs;
-        B.w = hp_window(B.x0, B.y0, P.bs, P.W, P.H, P.S);
-        const PaResult r = pa_block(P, B, lane, boundary, cdx, cdy, bitmap);
-        if (lane == 0)
-            write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters,
-                      boundary ? ME_BOUNDARY : ME_OPAQUE, true);
+        if (lane == 0) {
+            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+            write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters, ty, true);
+            if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, 4, r.dpd, ty);
+        }
         __syncwarp();
+        e = e_next;
     }
 }
 
@@ -947,14 +1337,6 @@ struct McArgs {
     const uint8_t* ref_override;
     const uint8_t* cur_override;
 };
-
-// Rounds 4*s/4 to nearest, ties to even (std::nearbyint, compensation.cpp:64).
-__device__ __forceinline__ int round_q4(int i4) {
-    const int q = i4 >> 2, rem = i4 & 3;
-    if (rem < 2) return q;
-    if (rem > 2) return q + 1;
-    return q + (q & 1);
-}
 
 __global__ void __launch_bounds__(256) mc_kernel(McArgs a) {
     const Batch& b = a.b;
@@ -1228,7 +1610,7 @@ PaParams make_pa_params(const Batch& b, const me_config& c) {
 
 struct Scratch {
     uint8_t* types;
-    uint32_t* list;
+    uint2* list;
     int* hist;
     int* offs;
     int* cursor;
@@ -1243,8 +1625,8 @@ Scratch carve(const Batch& b, int nbins, void* base) {
     const size_t nb = size_t(b.nblocks());
     s.types = p;
     p += align_up(nb);
-    s.list = reinterpret_cast<uint32_t*>(p);
-    p += align_up(nb * 4);
+    s.list = reinterpret_cast<uint2*>(p);
+    p += align_up(nb * 8);
     s.hist = reinterpret_cast<int*>(p);
     p += align_up(size_t(nbins) * 4);
     s.offs = reinterpret_cast<int*>(p);
@@ -1257,10 +1639,17 @@ Scratch carve(const Batch& b, int nbins, void* base) {
 
 }  // namespace
 
+// Sequence stagger of the PA wavefront keys (key = t + skew * seq): spreads the
+// ramp-up/ramp-down of the per-sequence wavefronts so dependent blocks sit
+// further apart in the work list.
+int pa_skew(const Batch& b) { return b.steps() + (b.n_seq - 1) <= 8192 ? 1 : 0; }
+
+int pa_bins(const Batch& b) { return b.steps() + pa_skew(b) * (b.n_seq - 1); }
+
 size_t scratch_bytes(const Batch& b, int algo) {
-    const int nbins = algo == ME_ALGO_PA ? b.steps() : 1;
+    const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
     const size_t nb = size_t(b.nblocks());
-    return align_up(nb) + align_up(nb * 4) + align_up(size_t(nbins) * 4) +
+    return align_up(nb) + align_up(nb * 8) + align_up(size_t(nbins) * 4) +
            align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4) + 256;
 }
 
@@ -1269,7 +1658,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
                       size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events) {
     const int algo = cfg.algo;
     const bool pa = algo == ME_ALGO_PA;
-    const int nbins = pa ? b.steps() : 1;
+    const int nbins = pa ? pa_bins(b) : 1;
     if (scratch_size < scratch_bytes(b, algo)) return cudaErrorInvalidValue;
     Scratch s = carve(b, nbins, scratch);
     cudaError_t e;
@@ -1286,6 +1675,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     ca.types = s.types;
     ca.hist = s.hist;
     ca.nbins = nbins;
+    ca.stats = stats;
+    ca.skew = pa_skew(b);
     const int64_t nb = b.nblocks();
     const size_t hist_smem = size_t(nbins) * 4;
     {
@@ -1317,6 +1708,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         ea.counter = s.counter;
         ea.recs = recs;
         ea.band_rows_max = kEsBandRows;
+        ea.stats = stats;
         const size_t smem = es_smem_bytes(b.bs, cfg.search_range, b.W);
         if (b.bs == 16) {
             if ((e = cudaFuncSetAttribute(es_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
@@ -1338,13 +1730,18 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         pa_args.nlist = nlist;
         pa_args.recs = recs;
         pa_args.prev0 = prev0;
+        pa_args.stats = stats;
+        pa_args.fast = (pa_args.P.step == 2 && cfg.max_iterations <= 4) ? 1 : 0;
         const int threads = 512;
-        const size_t smem = size_t(threads / 32) * pa_args.P.bm_words * 4;
-        if ((e = cudaFuncSetAttribute(pa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+        const int fast_words = b.bs == 8 ? PaFast<8>::WORDS : PaFast<16>::WORDS;
+        pa_args.warp_words = std::max(fast_words, pa_args.P.bm_words);
+        const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
+        auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pa_kernel, threads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         // persistent: every warp must be co-resident (dependency spinning)
-        pa_kernel<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(pa_args);
+        kern<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(pa_args);
         if ((e = cudaGetLastError())) return e;
     } else {
         RingArgs ra;
@@ -1354,6 +1751,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         ra.list = s.list;
         ra.nlist = nlist;
         ra.recs = recs;
+        ra.stats = stats;
         const int WX = std::min(2 * cfg.search_range + 1, b.W - b.bs + 1);
         const int WY = std::min(2 * cfg.search_range + 1, b.H - b.bs + 1);
         ra.bitmap_words = (WX * WY + 31) / 32;
@@ -1368,18 +1766,22 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     }
 
     if (events) cudaEventRecord(events[3], st);
-    McArgs ma;
-    ma.b = b;
-    ma.recs = recs;
-    ma.stats = stats;
-    ma.pred = pred;
-    ma.mv_override = nullptr;
-    ma.types_override = nullptr;
-    ma.ref_override = nullptr;
-    ma.cur_override = nullptr;
-    const int segs = (b.W / 8) * b.H;
-    dim3 grid((segs + 255) / 256, b.n_seq * b.pairs);
-    mc_kernel<<<grid, 256, 0, st>>>(ma);
+    if (pred) {
+        // the SSE and stats are already fused into the classify and search
+        // kernels; this pass only materialises the prediction when asked to
+        McArgs ma;
+        ma.b = b;
+        ma.recs = recs;
+        ma.stats = nullptr;
+        ma.pred = pred;
+        ma.mv_override = nullptr;
+        ma.types_override = nullptr;
+        ma.ref_override = nullptr;
+        ma.cur_override = nullptr;
+        const int segs = (b.W / 8) * b.H;
+        dim3 grid((segs + 255) / 256, b.n_seq * b.pairs);
+        mc_kernel<<<grid, 256, 0, st>>>(ma);
+    }
     if (events) cudaEventRecord(events[4], st);
     return cudaGetLastError();
 }
