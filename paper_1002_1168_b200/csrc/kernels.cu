@@ -15,7 +15,11 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "kernels.h"
 
@@ -270,7 +274,7 @@ struct ClassArgs {
     int* hist;           // [nbins]
     int nbins;
     me_pair_stats* stats;  // [n_seq][pairs]: transparent blocks' count and SSE
-    int skew;              // PA: key = h + 2v + p + skew * seq (staggers the sequences)
+    int key_a, key_s;      // PA: key = key_a * (h + 2v + p) + key_s * seq (sequence stagger)
 };
 
 __device__ __forceinline__ int classify_one(const uint8_t* a, int W, int x0, int y0, int bs) {
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             r.w = uint32_t(ty) << 8;
             *reinterpret_cast<uint4*>(a.recs + g) = r;
             if (ty != ME_TRANSPARENT) {
-                atomicAdd(&s_hist[a.pa ? h + 2 * v + p + a.skew * seq : 0], 1);
+                atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
             } else if (a.stats) {
                 sse = block_sse0(b.luma + fcur * plane, b.luma + fref * plane, b.W, h * b.bs,
                                  v * b.bs, b.bs);
@@ -367,13 +371,20 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
 }
 
 // Exclusive scan of hist into offs[0..nbins] (single CTA), cursor = offs.
-__global__ void scan_kernel(const int* hist, int nbins, int* offs, int* cursor) {
+// Each bin is padded to a multiple of `pad` entries (invalid markers), so a
+// warp that claims `pad` aligned entries never straddles two bins.
+constexpr uint32_t kInvalidEntry = 0xFFFFFFFFu;
+constexpr int kTasksPerWarpMax = 4;  // PA: 8-lane groups (BS 8) -> 4 blocks per warp
+
+__global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
+                            uint2* list) {
     __shared__ int s_part[1024];
     const int T = blockDim.x;
     const int per = (nbins + T - 1) / T;
     const int lo = threadIdx.x * per, hi = min(lo + per, nbins);
+    auto padded = [&](int v) { return (v + pad - 1) / pad * pad; };
     int sum = 0;
-    for (int i = lo; i < hi; ++i) sum += hist[i];
+    for (int i = lo; i < hi; ++i) sum += padded(hist[i]);
     s_part[threadIdx.x] = sum;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -390,7 +401,8 @@ __global__ void scan_kernel(const int* hist, int nbins, int* offs, int* cursor) 
     for (int i = lo; i < hi; ++i) {
         offs[i] = acc;
         cursor[i] = acc;
-        acc += hist[i];
+        for (int k = hist[i]; k < padded(hist[i]); ++k) list[acc + k] = make_uint2(kInvalidEntry, kInvalidEntry);
+        acc += padded(hist[i]);
     }
 }
 
@@ -422,7 +434,7 @@ __global__ void fill_kernel(ClassArgs a, int* cursor, uint2* list) {
         if (a.types[g] == ME_TRANSPARENT) continue;
         int h, v, p, seq;
         split_block(b, g, h, v, p, seq);
-        atomicAdd(&s_cnt[a.pa ? h + 2 * v + p + a.skew * seq : 0], 1);
+        atomicAdd(&s_cnt[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
@@ -435,7 +447,7 @@ __global__ void fill_kernel(ClassArgs a, int* cursor, uint2* list) {
         if (ty == ME_TRANSPARENT) continue;
         int h, v, p, seq;
         split_block(b, g, h, v, p, seq);
-        const int key = a.pa ? h + 2 * v + p + a.skew * seq : 0;
+        const int key = a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0;
         const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
         list[pos] = make_uint2(uint32_t(h) | (uint32_t(v) << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u),
                                uint32_t(p) | (uint32_t(seq) << 16));
@@ -1007,6 +1019,82 @@ __device__ PaResult pa_block(const PaParams& P, const PaBlock& B, int lane, bool
     return prs_warp(P, B, lane, bx, by, win_shape ? kInf : best, bitmap);
 }
 
+
+// ---------------------------------------------------------------------------
+// PA fast path (one block per warp).  With PRS on the integer grid (step 2)
+// and at most R = 4 iterations, every position prs_refine can evaluate lies
+// within +/-4 pels of the BRS winner.  So a block needs exactly one round of
+// global loads — a (BS+8)^2 reference patch per distinct candidate, staged in
+// shared memory — after which the BRS scores, all 81 lattice costs around the
+// winner (computed eagerly, in parallel) and the final SSE come from shared
+// memory, and the PRS walk itself is a chain of table lookups.  The wavefront's
+// critical path is a chain of blocks, so per-block latency is what this
+// layout minimises.
+// ---------------------------------------------------------------------------
+
+template <int BS>
+struct WPatch {
+    static constexpr int R = 4;
+    static constexpr int L = 2 * R + 1;     // lattice side (9)
+    static constexpr int NP = L * L;        // 81 lattice positions
+    static constexpr int PR = BS + 2 * R;   // patch rows
+    static constexpr int PB = BS + 2 * R;   // patch bytes per row
+    static constexpr int PWW = PB / 4 + 1;  // words per row (+1 pad for unaligned reads)
+    static constexpr int WORDS = PR * PWW;
+    static constexpr int WARP_WORDS = 4 * WORDS + NP + 3;
+};
+
+// Loads patch row r (0..PR-1) of the candidate at pel offset (cx, cy) into
+// dst.  Rows / columns outside the frame are edge-replicated (only
+// inadmissible positions ever read them).
+template <int BS>
+__device__ __forceinline__ void stage_patch_row(const uint8_t* ref, int W, int H, int x0, int y0,
+                                                int cx, int cy, int r, uint32_t* dst) {
+    using F = WPatch<BS>;
+    constexpr int PW = F::PB / 4;
+    const int y = clampi(y0 + cy - F::R + r, 0, H - 1);
+    const int xs = x0 + cx - F::R;
+    const uint8_t* row = ref + size_t(y) * W;
+    uint32_t w[PW];
+    if (xs >= 0 && xs + F::PB <= W) {
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(row + xs);
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(ad & ~uintptr_t(3));
+        const uint32_t sh = uint32_t(ad & 3) * 8;
+        uint32_t prev = __ldg(aw);
+#pragma unroll
+        for (int i = 0; i < PW; ++i) {
+            const uint32_t nxt = (i + 1 < PW || sh) ? __ldg(aw + i + 1) : 0u;
+            w[i] = __funnelshift_r(prev, nxt, sh);
+            prev = nxt;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PW; ++i) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v |= uint32_t(row[clampi(xs + 4 * i + k, 0, W - 1)]) << (8 * k);
+            w[i] = v;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PW; ++i) dst[i] = w[i];
+    dst[PW] = 0u;
+}
+
+// BS/4 words of a patch row starting at byte offset i (0..2R).
+template <int BS>
+__device__ __forceinline__ void patch_words(const uint32_t* row, int i, uint32_t (&o)[BS / 4]) {
+    const uint32_t* p = row + (i >> 2);
+    const uint32_t sh = uint32_t(i & 3) * 8;
+    uint32_t w0 = p[0];
+#pragma unroll
+    for (int k = 0; k < BS / 4; ++k) {
+        const uint32_t w1 = p[k + 1];
+        o[k] = __funnelshift_r(w0, w1, sh);
+        w0 = w1;
+    }
+}
+
 struct PaArgs {
     Batch b;
     PaParams P;
@@ -1015,82 +1103,20 @@ struct PaArgs {
     me_block_rec* recs;
     const int32_t* prev0;  // pair 0's temporal candidates or null
     me_pair_stats* stats;
-    int fast;              // integer-pel patch fast path allowed (step 2, max_iter <= 4)
+    int fast;              // patch fast path allowed (step 2, max_iter <= 4)
     int warp_words;        // shared words per warp
+    int poll_ns;           // dependency poll interval
+    unsigned long long* trace;  // debug: per entry {claimed, deps ready, done, smid} (ns)
 };
 
-// Fast path geometry: with step 2 (integer pel) and at most R = 4 PRS
-// iterations, every position prs_refine can evaluate lies within +/-4 pels of
-// the BRS winner, so one (BS+8)^2 reference patch per candidate, staged once
-// in shared memory, holds all the data the block needs: the BRS texture
-// scores, every PRS neighbour cost (evaluated lazily, exactly the positions
-// the reference visits) and the final prediction SSE.
-template <int BS>
-struct PaFast {
-    static constexpr int R = 4;
-    static constexpr int L = 2 * R + 1;          // lattice side
-    static constexpr int PR = BS + 2 * R;        // patch rows
-    static constexpr int PB = BS + 2 * R;        // patch bytes per row
-    static constexpr int PWW = PB / 4 + 1;       // words per row (+1: unaligned reads)
-    static constexpr int NW = BS / 4;            // words per block row
-    static constexpr int PATCH_WORDS = PR * PWW;
-    static constexpr int CUR_WORDS = BS * NW;
-    static constexpr int WORDS = 4 * PATCH_WORDS + CUR_WORDS + 4;  // patches, cur block, visited
-};
-
-// Loads patch row r of candidate centre (cx, cy) (pels) into smem words;
-// rows/columns outside the frame are edge-replicated (only inadmissible
-// positions ever read them).
-template <int BS>
-__device__ __forceinline__ void load_patch_row(const uint8_t* ref, int W, int H, int x0, int y0,
-                                               int cx, int cy, int r, uint32_t* dst) {
-    using F = PaFast<BS>;
-    const int y = clampi(y0 + cy - F::R + r, 0, H - 1);
-    const int xs = x0 + cx - F::R;
-    const uint8_t* row = ref + size_t(y) * W;
-    if (xs >= 0 && xs + F::PB <= W) {
-        const uintptr_t ad = reinterpret_cast<uintptr_t>(row + xs);
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(ad & ~uintptr_t(3));
-        const uint32_t sh = uint32_t(ad & 3) * 8;
-        uint32_t prev = __ldg(w);
-#pragma unroll
-        for (int i = 0; i < F::PB / 4; ++i) {
-            const uint32_t nxt = (i + 1 < F::PB / 4 || sh) ? __ldg(w + i + 1) : 0u;
-            dst[i] = __funnelshift_r(prev, nxt, sh);
-            prev = nxt;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < F::PB / 4; ++i) {
-            uint32_t v = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v |= uint32_t(row[clampi(xs + 4 * i + k, 0, W - 1)]) << (8 * k);
-            dst[i] = v;
-        }
-    }
-    dst[F::PB / 4] = 0u;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
-// SAD of block row r against the patch at lattice offset (i, j) in [0, 2R]^2.
-template <int BS>
-__device__ __forceinline__ uint32_t patch_row_sad(const uint32_t* pw, const uint32_t* cw, int i, int j,
-                                                  int r) {
-    using F = PaFast<BS>;
-    const uint32_t* row = pw + (j + r) * F::PWW + (i >> 2);
-    const uint32_t* c = cw + r * F::NW;
-    const uint32_t sh = uint32_t(i & 3) * 8;
-    uint32_t acc = 0, w0 = row[0];
-#pragma unroll
-    for (int k = 0; k < F::NW; ++k) {
-        const uint32_t w1 = row[k + 1];
-        acc = vad4(c[k], __funnelshift_r(w0, w1, sh), acc);
-        w0 = w1;
-    }
-    return acc;
-}
-
-// gather_candidates (estimators.cpp:238-255): lane i < 4 returns candidate i's
-// MV word (A, B, C, T), waiting for dependencies still in flight.
+// gather_candidates (estimators.cpp:238-255): lane i < 4 returns candidate
+// i's MV word (A, B, C, T), waiting for dependencies still in flight.
 __device__ __forceinline__ uint32_t fetch_candidate(const PaArgs& a, uint32_t g, int h, int v, int p,
                                                     int lane) {
     const Batch& b = a.b;
@@ -1106,7 +1132,7 @@ __device__ __forceinline__ uint32_t fetch_candidate(const PaArgs& a, uint32_t g,
         if (src) {
             mvw = ld_relaxed(src);
             while (mvw == kSentinel) {
-                __nanosleep(32);
+                __nanosleep(a.poll_ns);
                 mvw = ld_relaxed(src);
             }
         } else if (lane == 3 && a.prev0) {
@@ -1114,103 +1140,157 @@ __device__ __forceinline__ uint32_t fetch_candidate(const PaArgs& a, uint32_t g,
             mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
         }
     }
+    __syncwarp();
     return mvw;
 }
 
-// Integer-pel fast path for one block (warp-cooperative): brs_select +
-// prs_refine decisions identical to the reference; also returns the block's
-// prediction SSE.  The current block is already in smem (cw).
 template <int BS>
-__device__ PaResult pa_fast_block(const PaParams& P, const PaBlock& B, int lane, bool boundary,
-                                  int myvx, int myvy, uint32_t* ws, uint32_t& sse_out) {
-    // myvx/myvy: clipped (even) candidate (lane >> 3) of this lane, half-pel
-    using F = PaFast<BS>;
-    uint32_t* patch = ws;                        // [4][PR][PWW]
-    const uint32_t* cw = ws + 4 * F::PATCH_WORDS;  // [BS][NW]
-    uint32_t* vis = ws + 4 * F::PATCH_WORDS + F::CUR_WORDS;  // [3] lattice bitmap
-    // --- stage the four candidate patches -----------------------------------
+__device__ __forceinline__ void load_row(const uint8_t* p, uint32_t (&w)[BS / 4]) {
+    if (BS == 8) {
+        const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = c2.x;
+        w[1 % (BS / 4)] = c2.y;
+    } else {
+        const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(p));
+        w[0] = c4.x;
+        w[1 % (BS / 4)] = c4.y;
+        w[2 % (BS / 4)] = c4.z;
+        w[3 % (BS / 4)] = c4.w;
+    }
+}
+
+// Fast path for one block (warp).  mvw: lane i < 4 holds candidate i's raw MV
+// word.  Returns false (nothing computed) when a clipped candidate is
+// half-pel, i.e. the block needs the generic path.
+template <int BS>
+__device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bool boundary,
+                               uint32_t mvw, uint32_t* ws, PaResult& res, uint32_t& sse_out) {
+    using F = WPatch<BS>;
+    constexpr int NW = BS / 4;
+    constexpr int L = F::L;
+    const int W = P.W;
+    uint32_t* patch = ws;                 // [4][PR][PWW]
+    uint32_t* table = ws + 4 * F::WORDS;  // [81] lattice costs (x4; kInf = inadmissible)
+    // my candidate slot (lanes 8c..8c+7 serve candidate c) and its duplicate map
     const int c = lane >> 3, sub = lane & 7;
-    const int ccx = myvx >> 1, ccy = myvy >> 1;  // pels
-    for (int r = sub; r < F::PR; r += 8)
-        load_patch_row<BS>(B.ref, P.W, P.H, B.x0, B.y0, ccx, ccy, r,
-                           patch + c * F::PATCH_WORDS + r * F::PWW);
-    // shape scores (boundary blocks) read the alpha planes directly
+    const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
+    const int myx = clip_comp(mv_dx(mine), B.w.lo_x, B.w.hi_x);  // clip_to_window (:275-276)
+    const int myy = clip_comp(mv_dy(mine), B.w.lo_y, B.w.hi_y);
+    if (__any_sync(0xFFFFFFFFu, ((myx | myy) & 1) != 0)) return false;
+    int md = c;  // first candidate with the same clipped vector
+#pragma unroll
+    for (int j = 2; j >= 0; --j) {
+        const int jx = __shfl_sync(0xFFFFFFFFu, myx, 8 * j), jy = __shfl_sync(0xFFFFFFFFu, myy, 8 * j);
+        if (j < c && jx == myx && jy == myy) md = j;
+    }
+    // --- the single round of reference loads: distinct candidate patches -------
+    if (md == c)
+        for (int r = sub; r < F::PR; r += 8)
+            stage_patch_row<BS>(B.ref, W, P.H, B.x0, B.y0, myx >> 1, myy >> 1, r,
+                                patch + c * F::WORDS + r * F::PWW);
+    // current block: every lane holds all of it (broadcast loads)
+    uint32_t cb[BS][NW];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) load_row<BS>(B.cur + size_t(B.y0 + r) * W + B.x0, cb[r]);
+    // shape scores (boundary blocks): alpha rows of my candidate
     const bool shape = boundary && (c < 3 || P.bt_shape);
     uint32_t s = 0;
     if (shape)
         for (int r = sub; r < BS; r += 8)
-            s += row_shape(B.ca, B.ra, P.W, P.H, B.x0, B.y0 + r, BS, ccx, ccy) * (255u * 4u);
-    if (lane < 3) vis[lane] = 0u;
+            s += row_shape(B.ca, B.ra, W, P.H, B.x0, B.y0 + r, BS, myx >> 1, myy >> 1) * (255u * 4u);
     __syncwarp();
-    if (!shape)
-        for (int r = sub; r < BS; r += 8)
-            s += 4u * patch_row_sad<BS>(patch + c * F::PATCH_WORDS, cw, F::R, F::R, r);
+    // --- brs_select (estimators.cpp:257-301) ------------------------------------
+    if (!shape) {
+        const uint32_t* pc = patch + md * F::WORDS;
+#pragma unroll
+        for (int r = 0; r < BS; ++r) {
+            if ((r & 7) != sub) continue;
+            const uint32_t* row = pc + (F::R + r) * F::PWW + F::R / 4;  // byte R: word aligned
+            uint32_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) acc = vad4(cb[r][k], row[k], acc);
+            s += acc * 4u;
+        }
+    }
     s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
     s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
     s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
-    // brs_select: strict <, so A, B, C, T win ties in that order (estimators.cpp:295)
     uint32_t best = __shfl_sync(0xFFFFFFFFu, s, 0);
     int win = 0;
 #pragma unroll
     for (int i = 1; i < 4; ++i) {
         const uint32_t si = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
-        if (si < best) {
+        if (si < best) {  // strict <: A, B, C, T tie order (:295)
             best = si;
             win = i;
         }
     }
     const bool win_shape = boundary && (win < 3 || P.bt_shape);
-    const int wx = __shfl_sync(0xFFFFFFFFu, myvx, 8 * win), wy = __shfl_sync(0xFFFFFFFFu, myvy, 8 * win);
-    const uint32_t* pw = patch + win * F::PATCH_WORDS;
-    // --- prs_refine (estimators.cpp:311-382) ---------------------------------
-    int ci = F::R, cj = F::R;
-    uint32_t ccost = best;
-    if (win_shape) {  // the centre's texture cost was not computed by BRS
-        uint32_t t = 0;
-        for (int r = lane; r < BS; r += 32) t += patch_row_sad<BS>(pw, cw, ci, cj, r);
-        ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
-    }
-    if (lane == 0) {
-        const int bit = F::R * F::L + F::R;
-        vis[bit >> 5] |= 1u << (bit & 31);
+    const int wx = __shfl_sync(0xFFFFFFFFu, myx, 8 * win), wy = __shfl_sync(0xFFFFFFFFu, myy, 8 * win);
+    const int wp = __shfl_sync(0xFFFFFFFFu, md, 8 * win);
+    const uint32_t* pw = patch + wp * F::WORDS;  // the winner's patch
+    // --- all 81 lattice costs around the winner ---------------------------------
+    // lane = (column i, group of 3 rows j); each shifted patch row is read once
+    // and reused for every j it pairs with.
+    if (lane < 3 * L) {
+        const int i = lane % L, jg = lane / L, j0 = 3 * jg;
+        uint32_t acc[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int pr = 0; pr < BS + 2; ++pr) {  // patch rows j0 .. j0 + BS + 1
+            uint32_t w[NW];
+            patch_words<BS>(pw + (j0 + pr) * F::PWW, i, w);
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) {
+                const int r = pr - jj;  // block row paired with this patch row at j = j0 + jj
+                if (r >= 0 && r < BS) {
+#pragma unroll
+                    for (int k = 0; k < NW; ++k) acc[jj] = vad4(cb[r][k], w[k], acc[jj]);
+                }
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+            const int j = j0 + jj;
+            const int vx = wx + 2 * (i - F::R), vy = wy + 2 * (j - F::R);
+            const bool adm = vx >= B.w.lo_x && vx <= B.w.hi_x && vy >= B.w.lo_y && vy <= B.w.hi_y;
+            table[j * L + i] = adm ? acc[jj] * 4u : kInf;
+        }
     }
     __syncwarp();
+    // --- prs_refine (estimators.cpp:311-382) as lookups ------------------------
+    uint32_t ccost = win_shape ? table[F::R * L + F::R] : best;
+    // Unique-evaluation counting (:321-332): a neighbour of the current centre
+    // was evaluated before iff it is the start or lies in the 3x3 neighbourhood
+    // of an earlier centre (each iteration evaluates all admissible neighbours).
+    int pcx[4] = {99, 99, 99, 99}, pcy[4] = {99, 99, 99, 99};
+    int ci = 0, cj = 0;
     uint32_t dpd = 1, iters = 0;
-    const int k = lane >> 2, q = lane & 3;
-    const bool leader = q == 0;
+    const int k = lane & 7;
+    const int kx = c_off8[k][0], ky = c_off8[k][1];
     for (int it = 0; it < P.max_iter; ++it) {
         if (ccost == 0) break;  // already a global minimum (:341)
-        const int ni = ci + c_off8[k][0], nj = cj + c_off8[k][1];
-        const int vx = wx + 2 * (ni - F::R), vy = wy + 2 * (nj - F::R);
-        const bool adm = vx >= B.w.lo_x && vx <= B.w.hi_x && vy >= B.w.lo_y && vy <= B.w.hi_y;
-        uint32_t part = 0;
-        if (adm)
-            for (int r = q; r < BS; r += 4) part += patch_row_sad<BS>(pw, cw, ni, nj, r);
-        part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
-        part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
-        const uint32_t cost = 4u * part;
-        bool fresh = false;
-        if (adm && leader) {  // unique aggregate evaluations (:321-332)
-            const int bit = nj * F::L + ni;
-            const uint32_t m = 1u << (bit & 31);
-            fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
-        }
-        dpd += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
-        const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, (adm && leader) ? cost : kInf);
+        const int px = ci + kx, py = cj + ky;
+        const uint32_t cost = table[(py + F::R) * L + px + F::R];
+        const bool adm = lane < 8 && cost != kInf;
+        bool seen = px == 0 && py == 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) seen |= abs(px - pcx[j]) <= 1 && abs(py - pcy[j]) <= 1;
+        dpd += __popc(__ballot_sync(0xFFFFFFFFu, adm && !seen));
+        const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, adm ? cost : kInf);
         if (m >= ccost) break;  // centre kept (:376)
-        const uint32_t ties = __ballot_sync(0xFFFFFFFFu, adm && leader && cost == m);
+        const uint32_t ties = __ballot_sync(0xFFFFFFFFu, adm && cost == m);
         int w;
         if (__popc(ties) == 1) {
-            w = (__ffs(ties) - 1) >> 2;
+            w = __ffs(ties) - 1;
         } else {
             // stable descending sort by off . dir (:357-362): the first tied
-            // neighbour in sorted order has the largest key, lowest index on equal keys
+            // neighbour in sorted order = largest key, lowest index on equal keys
             double dir_x, dir_y;
-            prs_direction(P, B, lane, wx + 2 * (ci - F::R), wy + 2 * (cj - F::R), dir_x, dir_y);
+            prs_direction(P, B, lane, wx + 2 * ci, wy + 2 * cj, dir_x, dir_y);
             w = -1;
             double bestkey = 0.0;
             for (int o = 0; o < 8; ++o) {
-                if (!((ties >> (4 * o)) & 1u)) continue;
+                if (!((ties >> o) & 1u)) continue;
                 const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x),
                                              __dmul_rn(double(c_off8[o][1]), dir_y));
                 if (w < 0 || key > bestkey) {
@@ -1219,38 +1299,39 @@ __device__ PaResult pa_fast_block(const PaParams& P, const PaBlock& B, int lane,
                 }
             }
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j == it) {
+                pcx[j] = ci;
+                pcy[j] = cj;
+            }
         ci += c_off8[w][0];
         cj += c_off8[w][1];
         ccost = m;
         ++iters;
     }
-    // --- fused predict_frame + psnr SSE at the final vector ------------------
-    uint32_t sse = 0;
-    for (int r = lane; r < BS; r += 32) {
-        const uint32_t* row = pw + (cj + r) * F::PWW + (ci >> 2);
-        const uint32_t sh = uint32_t(ci & 3) * 8;
-        uint32_t w0 = row[0];
+    // --- fused predict_frame + psnr SSE at the final vector ---------------------
+    uint32_t se = 0;
 #pragma unroll
-        for (int kk = 0; kk < F::NW; ++kk) {
-            const uint32_t w1 = row[kk + 1];
-            sse = sq4(cw[r * F::NW + kk], __funnelshift_r(w0, w1, sh), sse);
-            w0 = w1;
-        }
+    for (int r = 0; r < BS; ++r) {
+        if (r != lane) continue;
+        uint32_t w[NW];
+        patch_words<BS>(pw + (F::R + cj + r) * F::PWW, F::R + ci, w);
+#pragma unroll
+        for (int kk = 0; kk < NW; ++kk) se = sq4(cb[r][kk], w[kk], se);
     }
-    sse_out = __reduce_add_sync(0xFFFFFFFFu, sse);
-    PaResult res;
-    res.dx = wx + 2 * (ci - F::R);
-    res.dy = wy + 2 * (cj - F::R);
+    sse_out = __reduce_add_sync(0xFFFFFFFFu, se);
+    res.dx = wx + 2 * ci;
+    res.dy = wy + 2 * cj;
     res.cost_q4 = ccost;
     res.dpd = dpd;
     res.iters = iters;
-    return res;
+    return true;
 }
 
 template <int BS>
-__global__ void __launch_bounds__(512, BS == 8 ? 2 : 1) pa_kernel(PaArgs a) {
+__global__ void __launch_bounds__(512, 1) pa_kernel(PaArgs a) {
     extern __shared__ uint32_t s_pa[];
-    using F = PaFast<BS>;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t* ws = s_pa + wid * a.warp_words;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
@@ -1258,10 +1339,14 @@ __global__ void __launch_bounds__(512, BS == 8 ? 2 : 1) pa_kernel(PaArgs a) {
     const Batch& b = a.b;
     const PaParams& P = a.P;
     const size_t plane = size_t(b.W) * b.H;
-    int item = blockIdx.x * (blockDim.x >> 5) + wid;
-    uint2 e = item < n ? a.list[item] : make_uint2(0u, 0u);
-    for (; item < n; item += nwarps) {
-        const uint2 e_next = item + nwarps < n ? a.list[item + nwarps] : make_uint2(0u, 0u);  // prefetch
+    // Static round-robin over the wavefront-sorted list: every dependency of
+    // entry e sits at a smaller index, each warp handles its entries in
+    // increasing order and the grid is sized so every warp is resident, so
+    // the smallest unfinished entry is always being worked on (no deadlock,
+    // no grid-wide barrier).
+    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+        const uint2 e = a.list[item];
+        if (e.x == kInvalidEntry) continue;
         int h, v, p, seq;
         bool boundary;
         const uint32_t g = decode_entry(b, e, h, v, p, seq, boundary);
@@ -1274,32 +1359,14 @@ __global__ void __launch_bounds__(512, BS == 8 ? 2 : 1) pa_kernel(PaArgs a) {
         B.x0 = h * BS;
         B.y0 = v * BS;
         B.w = hp_window(B.x0, B.y0, BS, P.W, P.H, P.S);
-        // round A: current block into smem + candidate MVs, concurrently
-        if (a.fast && lane < BS) {
-            uint32_t* dst = ws + 4 * F::PATCH_WORDS + lane * F::NW;
-            const uint8_t* src = B.cur + size_t(B.y0 + lane) * b.W + B.x0;
-            if (BS == 8) {
-                const uint2 w = __ldg(reinterpret_cast<const uint2*>(src));
-                dst[0] = w.x;
-                dst[1] = w.y;
-            } else {
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(src));
-                dst[0] = w.x;
-                dst[1] = w.y;
-                dst[2] = w.z;
-                dst[3] = w.w;
-            }
-        }
+        unsigned long long t0 = 0;
+        if (a.trace) t0 = gtimer();
         const uint32_t mvw = fetch_candidate(a, g, h, v, p, lane);
-        const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, lane >> 3);
-        const int myvx = clip_comp(mv_dx(mine), B.w.lo_x, B.w.hi_x);  // clip_to_window (:275-276)
-        const int myvy = clip_comp(mv_dy(mine), B.w.lo_y, B.w.hi_y);
-        const bool odd = __any_sync(0xFFFFFFFFu, ((myvx | myvy) & 1) != 0);
+        unsigned long long t1 = 0;
+        if (a.trace) t1 = gtimer();
         PaResult r;
-        uint32_t sse;
-        if (a.fast && !odd) {
-            r = pa_fast_block<BS>(P, B, lane, boundary, myvx, myvy, ws, sse);
-        } else {
+        uint32_t sse = 0;
+        if (!(a.fast && pa_patch_block<BS>(P, B, lane, boundary, mvw, ws, r, sse))) {
             int rdx[4], rdy[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -1315,9 +1382,16 @@ __global__ void __launch_bounds__(512, BS == 8 ? 2 : 1) pa_kernel(PaArgs a) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters, ty, true);
             if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, 4, r.dpd, ty);
+            if (a.trace) {
+                unsigned smid;
+                asm("mov.u32 %0, %%smid;" : "=r"(smid));
+                a.trace[4 * item + 0] = t0;
+                a.trace[4 * item + 1] = t1;
+                a.trace[4 * item + 2] = gtimer();
+                a.trace[4 * item + 3] = smid;
+            }
         }
         __syncwarp();
-        e = e_next;
     }
 }
 
@@ -1626,7 +1700,7 @@ Scratch carve(const Batch& b, int nbins, void* base) {
     s.types = p;
     p += align_up(nb);
     s.list = reinterpret_cast<uint2*>(p);
-    p += align_up(nb * 8);
+    p += align_up((nb + size_t(kTasksPerWarpMax) * nbins) * 8);
     s.hist = reinterpret_cast<int*>(p);
     p += align_up(size_t(nbins) * 4);
     s.offs = reinterpret_cast<int*>(p);
@@ -1639,17 +1713,31 @@ Scratch carve(const Batch& b, int nbins, void* base) {
 
 }  // namespace
 
-// Sequence stagger of the PA wavefront keys (key = t + skew * seq): spreads the
-// ramp-up/ramp-down of the per-sequence wavefronts so dependent blocks sit
-// further apart in the work list.
-int pa_skew(const Batch& b) { return b.steps() + (b.n_seq - 1) <= 8192 ? 1 : 0; }
+// Ordering of the PA work list: key = A * t + S * seq, t = h + 2v + p.  Any
+// A >= 1 keeps every dependency (key - A or key - 2A) strictly earlier; S > 0
+// staggers the sequences' wavefronts.  Overridable for experiments through
+// ME_PA_KEY_A / ME_PA_KEY_S.
+struct KeyParams {
+    int a, s;
+};
 
-int pa_bins(const Batch& b) { return b.steps() + pa_skew(b) * (b.n_seq - 1); }
+KeyParams pa_key(const Batch& b) {
+    KeyParams k{1, 1};
+    if (const char* e = getenv("ME_PA_KEY_A")) k.a = std::max(1, atoi(e));
+    if (const char* e = getenv("ME_PA_KEY_S")) k.s = std::max(0, atoi(e));
+    if (int64_t(k.a) * (b.steps() - 1) + int64_t(k.s) * (b.n_seq - 1) + 1 > 12288) k = KeyParams{1, 0};
+    return k;
+}
+
+int pa_bins(const Batch& b) {
+    const KeyParams k = pa_key(b);
+    return k.a * (b.steps() - 1) + k.s * (b.n_seq - 1) + 1;
+}
 
 size_t scratch_bytes(const Batch& b, int algo) {
     const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
     const size_t nb = size_t(b.nblocks());
-    return align_up(nb) + align_up(nb * 8) + align_up(size_t(nbins) * 4) +
+    return align_up(nb) + align_up((nb + size_t(kTasksPerWarpMax) * nbins) * 8) + align_up(size_t(nbins) * 4) +
            align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4) + 256;
 }
 
@@ -1676,7 +1764,11 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     ca.hist = s.hist;
     ca.nbins = nbins;
     ca.stats = stats;
-    ca.skew = pa_skew(b);
+    {
+        const KeyParams k = pa_key(b);
+        ca.key_a = k.a;
+        ca.key_s = k.s;
+    }
     const int64_t nb = b.nblocks();
     const size_t hist_smem = size_t(nbins) * 4;
     {
@@ -1687,7 +1779,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         if ((e = cudaGetLastError())) return e;
     }
     if (events) cudaEventRecord(events[1], st);
-    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, s.offs, s.cursor);
+    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, 1, s.offs, s.cursor, s.list);
     if ((e = cudaGetLastError())) return e;
     {
         const int threads = 256;
@@ -1732,9 +1824,18 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         pa_args.prev0 = prev0;
         pa_args.stats = stats;
         pa_args.fast = (pa_args.P.step == 2 && cfg.max_iterations <= 4) ? 1 : 0;
+        pa_args.poll_ns = getenv("ME_PA_POLL_NS") ? atoi(getenv("ME_PA_POLL_NS")) : 64;
+        pa_args.trace = nullptr;
+        const char* trace_path = getenv("ME_PA_TRACE");
+        int n_host = 0;
+        if (trace_path) {
+            cudaStreamSynchronize(st);
+            cudaMemcpy(&n_host, nlist, 4, cudaMemcpyDeviceToHost);
+            cudaMalloc(&pa_args.trace, size_t(n_host) * 32);
+            cudaMemset(pa_args.trace, 0, size_t(n_host) * 32);
+        }
         const int threads = 512;
-        const int fast_words = b.bs == 8 ? PaFast<8>::WORDS : PaFast<16>::WORDS;
-        pa_args.warp_words = std::max(fast_words, pa_args.P.bm_words);
+        pa_args.warp_words = std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
         const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
         auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
@@ -1743,6 +1844,19 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         // persistent: every warp must be co-resident (dependency spinning)
         kern<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(pa_args);
         if ((e = cudaGetLastError())) return e;
+        if (trace_path) {
+            std::vector<unsigned long long> h(size_t(n_host) * 4);
+            std::vector<uint2> lst(n_host);
+            cudaMemcpyAsync(h.data(), pa_args.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(lst.data(), s.list, lst.size() * 8, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            if (FILE* f = fopen(trace_path, "wb")) {
+                fwrite(h.data(), 8, h.size(), f);
+                fwrite(lst.data(), 8, lst.size(), f);
+                fclose(f);
+            }
+            cudaFree(pa_args.trace);
+        }
     } else {
         RingArgs ra;
         ra.b = b;
