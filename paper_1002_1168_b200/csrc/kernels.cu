@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "kernels.h"
@@ -374,7 +375,6 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
 // Each bin is padded to a multiple of `pad` entries (invalid markers), so a
 // warp that claims `pad` aligned entries never straddles two bins.
 constexpr uint32_t kInvalidEntry = 0xFFFFFFFFu;
-constexpr int kTasksPerWarpMax = 4;  // PA: 8-lane groups (BS 8) -> 4 blocks per warp
 
 __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
                             uint2* list) {
@@ -1045,39 +1045,28 @@ struct WPatch {
 };
 
 // Loads patch row r (0..PR-1) of the candidate at pel offset (cx, cy) into
-// dst.  Rows / columns outside the frame are edge-replicated (only
-// inadmissible positions ever read them).
+// dst.  Branch-free: the row index is clamped and every 4-byte word is loaded
+// only when it lies inside the frame row (W % 4 == 0, so words never straddle
+// rows); bytes outside the frame read as 0.  Only inadmissible positions —
+// never evaluated — touch those bytes.
 template <int BS>
 __device__ __forceinline__ void stage_patch_row(const uint8_t* ref, int W, int H, int x0, int y0,
                                                 int cx, int cy, int r, uint32_t* dst) {
     using F = WPatch<BS>;
     constexpr int PW = F::PB / 4;
     const int y = clampi(y0 + cy - F::R + r, 0, H - 1);
-    const int xs = x0 + cx - F::R;
+    const int xs = x0 + cx - F::R;                 // first byte (may be < 0 or run past W)
+    const int wa = xs & ~3;                        // floor to a word boundary (two's complement)
+    const uint32_t sh = uint32_t(xs - wa) * 8;
     const uint8_t* row = ref + size_t(y) * W;
-    uint32_t w[PW];
-    if (xs >= 0 && xs + F::PB <= W) {
-        const uintptr_t ad = reinterpret_cast<uintptr_t>(row + xs);
-        const uint32_t* aw = reinterpret_cast<const uint32_t*>(ad & ~uintptr_t(3));
-        const uint32_t sh = uint32_t(ad & 3) * 8;
-        uint32_t prev = __ldg(aw);
+    uint32_t w[PW + 1];
 #pragma unroll
-        for (int i = 0; i < PW; ++i) {
-            const uint32_t nxt = (i + 1 < PW || sh) ? __ldg(aw + i + 1) : 0u;
-            w[i] = __funnelshift_r(prev, nxt, sh);
-            prev = nxt;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < PW; ++i) {
-            uint32_t v = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v |= uint32_t(row[clampi(xs + 4 * i + k, 0, W - 1)]) << (8 * k);
-            w[i] = v;
-        }
+    for (int i = 0; i <= PW; ++i) {
+        const int c = wa + 4 * i;
+        w[i] = (c >= 0 && c + 4 <= W) ? __ldg(reinterpret_cast<const uint32_t*>(row + c)) : 0u;
     }
 #pragma unroll
-    for (int i = 0; i < PW; ++i) dst[i] = w[i];
+    for (int i = 0; i < PW; ++i) dst[i] = __funnelshift_r(w[i], w[i + 1], sh);
     dst[PW] = 0u;
 }
 
@@ -1142,6 +1131,12 @@ __device__ __forceinline__ uint32_t fetch_candidate(const PaArgs& a, uint32_t g,
     }
     __syncwarp();
     return mvw;
+}
+
+template <int NW>
+__device__ __forceinline__ void ld8u_or16(const uint8_t* p, uint32_t (&w)[NW]) {
+    if (NW == 2) ld8u(p, w[0], w[1 % NW]);
+    else ld16u(p, w);
 }
 
 template <int BS>
@@ -1722,7 +1717,7 @@ struct KeyParams {
 };
 
 KeyParams pa_key(const Batch& b) {
-    KeyParams k{1, 1};
+    KeyParams k{2, 1};
     if (const char* e = getenv("ME_PA_KEY_A")) k.a = std::max(1, atoi(e));
     if (const char* e = getenv("ME_PA_KEY_S")) k.s = std::max(0, atoi(e));
     if (int64_t(k.a) * (b.steps() - 1) + int64_t(k.s) * (b.n_seq - 1) + 1 > 12288) k = KeyParams{1, 0};
