@@ -1695,7 +1695,7 @@ Scratch carve(const Batch& b, int nbins, void* base) {
     s.types = p;
     p += align_up(nb);
     s.list = reinterpret_cast<uint2*>(p);
-    p += align_up((nb + size_t(kTasksPerWarpMax) * nbins) * 8);
+    p += align_up((nb + size_t(nbins)) * 8);
     s.hist = reinterpret_cast<int*>(p);
     p += align_up(size_t(nbins) * 4);
     s.offs = reinterpret_cast<int*>(p);
@@ -1732,7 +1732,7 @@ int pa_bins(const Batch& b) {
 size_t scratch_bytes(const Batch& b, int algo) {
     const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
     const size_t nb = size_t(b.nblocks());
-    return align_up(nb) + align_up((nb + size_t(kTasksPerWarpMax) * nbins) * 8) + align_up(size_t(nbins) * 4) +
+    return align_up(nb) + align_up((nb + size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
            align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4) + 256;
 }
 
