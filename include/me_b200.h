@@ -193,6 +193,12 @@ me_status me_b200_prs_refine(me_ctx* ctx, int width, int height, const uint8_t* 
                              int step, int32_t out_mv[2], int64_t* out_dpd_steps,
                              uint32_t* descent_log_q4, int* log_len);
 
+/* prs_update (estimators.hpp:144-145, estimators.cpp:303-309): the per-pixel
+ * update d_i - eps * dpd * (u_x, u_y) in pels (out[0] = x, out[1] = y). */
+me_status me_b200_prs_update(me_ctx* ctx, int width, int height, const uint8_t* cur,
+                             const uint8_t* ref, int x, int y, const int32_t d[2], double epsilon,
+                             double theta, double out[2]);
+
 /* sad_texture (metrics.hpp:57, metrics.cpp:43-63), 4 x SAD, any vector
  * (edge-replicated reads, half-pel bilinear). */
 me_status me_b200_sad_texture(me_ctx* ctx, int width, int height, const uint8_t* cur,

@@ -42,6 +42,7 @@ from .api import (  # noqa: F401
     gather_candidates,
     predict_frame,
     prs_refine,
+    prs_update,
     psnr,
     psnr_from_sse,
     residual,

@@ -136,6 +136,7 @@ SIGNATURES = {
     "me_b200_block_search": (I, [P, I, I, I, P, P, I, I, I, I, I32P, I64P, U32P]),
     "me_b200_brs_select": (I, [P, I, I, P, P, P, P, I, I, I, I, I32P, I, I, I32P, U8P, U32P]),
     "me_b200_prs_refine": (I, [P, I, I, P, P, I, I, I, I32P, I, C.c_double, C.c_double, I, I, I32P, I64P, U32P, C.POINTER(I)]),
+    "me_b200_prs_update": (I, [P, I, I, P, P, I, I, I32P, C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "me_b200_sad_texture": (I, [P, I, I, P, P, I, I, I, I, I, U32P]),
     "me_b200_sad_shape": (I, [P, I, I, P, P, I, I, I, I, I, I64P]),
     "me_b200_classify_blocks": (I, [P, I, I, P, I, P]),

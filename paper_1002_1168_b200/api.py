@@ -424,6 +424,15 @@ def brs_select(cur, ref, cur_alpha, ref_alpha, rect: BlockRect, btype: BlockType
     return int(mv[0]), int(mv[1])
 
 
+def prs_update(cur, ref, x: int, y: int, d_i: MV, cfg: PrsConfig):
+    """estimators.cpp:303-309 (one pixel, on the GPU); returns (x, y) in pels."""
+    c, r = _plane(cur, "cur"), _plane(ref, "ref")
+    d = (C.c_int32 * 2)(int(d_i[0]), int(d_i[1]))
+    out = (C.c_double * 2)()
+    check(lib().me_b200_prs_update(ctx(), c.shape[1], c.shape[0], _ptr(c), _ptr(r), int(x), int(y), d, float(cfg.epsilon), float(cfg.theta), out))
+    return out[0], out[1]
+
+
 def prs_refine(cur, ref, rect: BlockRect, d0: MV, scfg: SearchConfig, cfg: PrsConfig, stats: SearchStats, descent_log: Optional[list] = None) -> MV:
     """estimators.cpp:311-382."""
     scfg.validate()

@@ -460,6 +460,24 @@ me_status me_b200_prs_refine(me_ctx* ctx, int W, int H, const uint8_t* cur, cons
     return ok();
 }
 
+me_status me_b200_prs_update(me_ctx* ctx, int W, int H, const uint8_t* cur, const uint8_t* ref, int x,
+                             int y, const int32_t d[2], double epsilon, double theta, double out[2]) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!cur || !ref || !d || !out) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    if (W <= 0 || H <= 0 || x < 0 || y < 0 || x >= W || y >= H)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "pixel outside the frame");
+    const uint8_t* host[2] = {cur, ref};
+    const uint8_t* dev[2];
+    if ((s = stage_planes(ctx, size_t(W) * H, host, dev, 2))) return s;
+    ME_CUDA(ctx->aux.reserve(256));
+    double* o = static_cast<double*>(ctx->aux.p);
+    ME_CUDA(mek::prs_update_single(dev[0], dev[1], W, H, x, y, d[0], d[1], epsilon, theta, o, ctx->stream));
+    ME_CUDA(cudaMemcpyAsync(out, o, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    s = sync(ctx);
+    return s ? s : ok();
+}
+
 me_status me_b200_sad_texture(me_ctx* ctx, int W, int H, const uint8_t* cur, const uint8_t* ref,
                               int x0, int y0, int size, int dx, int dy, uint32_t* out_sad_q4) {
     me_status s = check_ctx(ctx);

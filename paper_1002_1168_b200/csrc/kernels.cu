@@ -1601,6 +1601,20 @@ __global__ void prs_single_kernel(PaParams P, PaBlock B, int d0x, int d0y, int64
     }
 }
 
+// prs_update (estimators.cpp:303-309) at one pixel, round-to-nearest intrinsics.
+__global__ void prs_update_kernel(const uint8_t* cur, const uint8_t* ref, int W, int H, int x, int y,
+                                  int dx, int dy, double eps, double theta, double* out) {
+    const int i4 = interp4(ref, W, H, 2 * x - dx, 2 * y - dy);
+    const double e = __dsub_rn(double(cur[size_t(y) * W + x]), double(i4) * 0.25);
+    const double gx = (double(pxc(cur, W, H, x + 1, y)) - double(pxc(cur, W, H, x - 1, y))) / 2.0;
+    const double gy = (double(pxc(cur, W, H, x, y + 1)) - double(pxc(cur, W, H, x, y - 1))) / 2.0;
+    const double ux = fabs(gx) < theta ? 0.0 : __ddiv_rn(1.0, gx);
+    const double uy = fabs(gy) < theta ? 0.0 : __ddiv_rn(1.0, gy);
+    const double ee = __dmul_rn(eps, e);
+    out[0] = __dsub_rn(0.5 * dx, __dmul_rn(ee, ux));
+    out[1] = __dsub_rn(0.5 * dy, __dmul_rn(ee, uy));
+}
+
 __global__ void sad_texture_single_kernel(const uint8_t* cur, const uint8_t* ref, int W, int H,
                                           int x0, int y0, int bs, int dx2, int dy2, int64_t* out) {
     const int lane = threadIdx.x & 31;
@@ -1969,6 +1983,12 @@ cudaError_t prs_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int
     cudaError_t e = cudaFuncSetAttribute(prs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e) return e;
     prs_single_kernel<<<1, 32, smem, st>>>(P, B, d0x, d0y, out);
+    return cudaGetLastError();
+}
+
+cudaError_t prs_update_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x, int y,
+                              int dx, int dy, double eps, double theta, double* out, cudaStream_t st) {
+    prs_update_kernel<<<1, 1, 0, st>>>(cur, ref, W, H, x, y, dx, dy, eps, theta, out);
     return cudaGetLastError();
 }
 

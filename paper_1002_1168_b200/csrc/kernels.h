@@ -44,6 +44,8 @@ cudaError_t brs_single(const uint8_t* cur, const uint8_t* ref, const uint8_t* ca
 cudaError_t prs_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
                        int size, int d0x, int d0y, int range, double eps, double theta,
                        int max_iter, int step, int64_t* out, cudaStream_t st);
+cudaError_t prs_update_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x, int y,
+                              int dx, int dy, double eps, double theta, double* out, cudaStream_t st);
 cudaError_t sad_texture_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
                                int size, int dx, int dy, int64_t* out, cudaStream_t st);
 cudaError_t sad_shape_single(const uint8_t* ca, const uint8_t* ra, int W, int H, int x0, int y0,
