@@ -75,10 +75,10 @@ class Oracle:
             raise FileNotFoundError(path)
         self.L = C.CDLL(path)
         self.p = "orc_" if kind == "port" else "ref_"
-        self.L[self.p + "last_error"].restype = C.c_char_p
+        getattr(self.L, self.p + "last_error").restype = C.c_char_p
 
     def _f(self, name):
-        return self.L[self.p + name]
+        return getattr(self.L, self.p + name)
 
     def _chk(self, rc):
         if rc != ME_OK:

@@ -113,7 +113,7 @@ __device__ __forceinline__ uint32_t row_sad4(const uint8_t* cur, const uint8_t* 
                                              int x0, int y, int bs, int dx2, int dy2) {
     if (((dx2 | dy2) & 1) == 0) {
         const int sx = x0 + (dx2 >> 1), sy = y + (dy2 >> 1);
-        if (sx >= 0 && sx + bs <= W && sy >= 0 && sy < H && ((x0 | W) & 3) == 0) {
+        if ((bs == 8 || bs == 16) && sx >= 0 && sx + bs <= W && sy >= 0 && sy < H && ((x0 | W) & 3) == 0) {
             const uint8_t* c = cur + size_t(y) * W + x0;
             const uint8_t* r = ref + size_t(sy) * W + sx;
             uint32_t acc = 0;
@@ -145,7 +145,7 @@ __device__ __forceinline__ uint32_t row_sad4(const uint8_t* cur, const uint8_t* 
 __device__ __forceinline__ uint32_t row_shape(const uint8_t* ca, const uint8_t* ra, int W, int H,
                                               int x0, int y, int bs, int fx, int fy) {
     const int sx = x0 + fx, sy = y + fy;
-    if (sx >= 0 && sx + bs <= W && sy >= 0 && sy < H && ((x0 | W) & 3) == 0) {
+    if ((bs == 8 || bs == 16) && sx >= 0 && sx + bs <= W && sy >= 0 && sy < H && ((x0 | W) & 3) == 0) {
         const uint8_t* c = ca + size_t(y) * W + x0;
         const uint8_t* r = ra + size_t(sy) * W + sx;
         uint32_t bits = 0;
