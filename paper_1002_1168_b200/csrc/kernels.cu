@@ -309,43 +309,91 @@ __device__ __forceinline__ uint32_t block_sse0(const uint8_t* cur, const uint8_t
     return s;
 }
 
+// One thread classifies a 16-pixel-wide column strip of one block row (two
+// 8x8 blocks or one 16x16 block): every alpha, cur and ref row of the strip is
+// fetched with 16-byte loads in a single round (the luma is loaded
+// speculatively — it is only needed for transparent blocks' zero-vector SSE,
+// and is the compulsory read of those frames anyway).
+template <int BS>
 __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
     extern __shared__ int s_hist[];
+    constexpr int NB = 16 / BS;  // blocks per strip
     const Batch& b = a.b;
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
-    const int64_t n = b.nblocks();
+    const int strips = b.cols / NB;  // strips per block row
+    const int64_t n = int64_t(b.n_seq) * b.pairs * b.rows * strips;
     const size_t plane = size_t(b.W) * b.H;
     const int lane = threadIdx.x & 31;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     // uniform trip count so whole warps reach the warp-level reductions
-    for (int64_t g0 = int64_t(blockIdx.x) * blockDim.x; g0 < n; g0 += stride) {
-        const int64_t g = g0 + threadIdx.x;
+    for (int64_t s0 = int64_t(blockIdx.x) * blockDim.x; s0 < n; s0 += stride) {
+        const int64_t si = s0 + threadIdx.x;
         uint32_t sse = 0, n_t = 0;
         int64_t gp = -1;
-        if (g < n) {
-            const int h = int(g % b.cols);
-            int64_t t = g / b.cols;
+        if (si < n) {
+            const int hs = int(si % strips);
+            int64_t t = si / strips;
             const int v = int(t % b.rows);
             gp = t / b.rows;  // seq * pairs + p
             const int p = int(gp % b.pairs);
             const int seq = int(gp / b.pairs);
             const size_t fcur = size_t(seq) * b.F + p + b.d, fref = size_t(seq) * b.F + p;
-            const uint8_t* a_cur = b.alpha ? b.alpha + fcur * plane : nullptr;
-            const int ty = classify_one(a_cur, b.W, h * b.bs, v * b.bs, b.bs);
-            a.types[g] = uint8_t(ty);
-            uint4 r;
-            r.x = ty == ME_TRANSPARENT ? 0u : kSentinel;
-            r.y = 0u;
-            r.z = 0u;
-            r.w = uint32_t(ty) << 8;
-            *reinterpret_cast<uint4*>(a.recs + g) = r;
-            if (ty != ME_TRANSPARENT) {
-                atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
-            } else if (a.stats) {
-                sse = block_sse0(b.luma + fcur * plane, b.luma + fref * plane, b.W, h * b.bs,
-                                 v * b.bs, b.bs);
-                n_t = 1;
+            const size_t off = size_t(v * BS) * b.W + size_t(hs) * 16;
+            const uint8_t* ac = b.alpha ? b.alpha + fcur * plane + off : nullptr;
+            const uint8_t* cc = b.luma + fcur * plane + off;
+            const uint8_t* rc = b.luma + fref * plane + off;
+            uint4 al[BS], cu[BS], re[BS];
+#pragma unroll
+            for (int y = 0; y < BS; ++y) {
+                al[y] = ac ? __ldg(reinterpret_cast<const uint4*>(ac + size_t(y) * b.W)) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                if (a.stats) {
+                    cu[y] = __ldg(reinterpret_cast<const uint4*>(cc + size_t(y) * b.W));
+                    re[y] = __ldg(reinterpret_cast<const uint4*>(rc + size_t(y) * b.W));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                // classify_block (frame.cpp:81-104): any sample set / all set
+                uint32_t any = 0, nz = 1, s = 0;
+#pragma unroll
+                for (int y = 0; y < BS; ++y) {
+                    const uint32_t w0 = NB == 2 ? (k ? al[y].z : al[y].x) : al[y].x;
+                    const uint32_t w1 = NB == 2 ? (k ? al[y].w : al[y].y) : al[y].y;
+                    any |= w0 | w1;
+                    nz &= (__vcmpeq4(w0, 0u) | __vcmpeq4(w1, 0u)) == 0u;
+                    if (NB == 1) {
+                        any |= al[y].z | al[y].w;
+                        nz &= (__vcmpeq4(al[y].z, 0u) | __vcmpeq4(al[y].w, 0u)) == 0u;
+                    }
+                    if (a.stats) {
+                        if (NB == 2) {
+                            s = sq4(k ? cu[y].z : cu[y].x, k ? re[y].z : re[y].x, s);
+                            s = sq4(k ? cu[y].w : cu[y].y, k ? re[y].w : re[y].y, s);
+                        } else {
+                            s = sq4(cu[y].x, re[y].x, s);
+                            s = sq4(cu[y].y, re[y].y, s);
+                            s = sq4(cu[y].z, re[y].z, s);
+                            s = sq4(cu[y].w, re[y].w, s);
+                        }
+                    }
+                }
+                const int ty = !any ? ME_TRANSPARENT : (nz ? ME_OPAQUE : ME_BOUNDARY);
+                const int h = hs * NB + k;
+                const int64_t g = (gp * b.rows + v) * b.cols + h;
+                a.types[g] = uint8_t(ty);
+                uint4 r;
+                r.x = ty == ME_TRANSPARENT ? 0u : kSentinel;
+                r.y = 0u;
+                r.z = 0u;
+                r.w = uint32_t(ty) << 8;
+                *reinterpret_cast<uint4*>(a.recs + g) = r;
+                if (ty != ME_TRANSPARENT) {
+                    atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
+                } else {
+                    sse += s;
+                    n_t += 1;
+                }
             }
         }
         if (a.stats) {
@@ -362,7 +410,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             } else if (n_t) {
                 unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp);
                 if (sse) atomicAdd(st + 5, static_cast<unsigned long long>(sse));
-                atomicAdd(st + 4, 1ull);
+                atomicAdd(st + 4, static_cast<unsigned long long>(n_t));
             }
         }
     }
@@ -985,7 +1033,7 @@ __device__ __forceinline__ int clip_comp(int v, int lo, int hi) { return v < lo 
 
 // brs_select (estimators.cpp:257-301) then prs_refine.  cand[] holds the four
 // raw candidates A, B, C, T (every lane).  Returns also the BRS winner slot.
-__device__ PaResult pa_block(const PaParams& P, const PaBlock& B, int lane, bool boundary,
+__device__ __noinline__ PaResult pa_block(const PaParams& P, const PaBlock& B, int lane, bool boundary,
                              const int cdx[4], const int cdy[4], uint32_t* bitmap,
                              uint32_t* brs_scores = nullptr, int* brs_kinds = nullptr) {
     const int k = lane >> 3;
@@ -1039,9 +1087,14 @@ struct WPatch {
     static constexpr int NP = L * L;        // 81 lattice positions
     static constexpr int PR = BS + 2 * R;   // patch rows
     static constexpr int PB = BS + 2 * R;   // patch bytes per row
-    static constexpr int PWW = PB / 4 + 1;  // words per row (+1 pad for unaligned reads)
+    // A patch row is staged as CH raw 16-byte aligned chunks (two lanes per row
+    // share one L1 wavefront); the candidate's byte offset into the first
+    // chunk is applied when reading.  The row stride is padded so the 8
+    // (or 16) block rows a warp reads at once fall in distinct banks.
+    static constexpr int CH = (PB + 15) / 16 + 1;
+    static constexpr int PWW = BS == 8 ? 12 : 20;
     static constexpr int WORDS = PR * PWW;
-    static constexpr int WARP_WORDS = 4 * WORDS + NP + 3;
+    static constexpr int WARP_WORDS = 4 * WORDS + 4;  // patches + visited bitmap
 };
 
 // Loads patch row r (0..PR-1) of the candidate at pel offset (cx, cy) into
@@ -1165,7 +1218,7 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
     constexpr int L = F::L;
     const int W = P.W;
     uint32_t* patch = ws;                 // [4][PR][PWW]
-    uint32_t* table = ws + 4 * F::WORDS;  // [81] lattice costs (x4; kInf = inadmissible)
+    uint32_t* table = ws + 4 * F::WORDS;  // [3] visited bitmap
     // my candidate slot (lanes 8c..8c+7 serve candidate c) and its duplicate map
     const int c = lane >> 3, sub = lane & 7;
     const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
@@ -1179,10 +1232,30 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
         if (j < c && jx == myx && jy == myy) md = j;
     }
     // --- the single round of reference loads: distinct candidate patches -------
-    if (md == c)
-        for (int r = sub; r < F::PR; r += 8)
-            stage_patch_row<BS>(B.ref, W, P.H, B.x0, B.y0, myx >> 1, myy >> 1, r,
-                                patch + c * F::WORDS + r * F::PWW);
+    // 16-byte aligned chunks, consecutive lanes on the same row (one L1
+    // wavefront per row); chunks outside the frame row read as zero (only
+    // inadmissible positions touch them), rows are clamped.
+    int po = 0;  // byte offset of my candidate's patch start in its first chunk
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
+        const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
+        const int cdup = __shfl_sync(0xFFFFFFFFu, md, 8 * cc);
+        const int xs = B.x0 + ccx - F::R;
+        const int a0 = xs & ~15;
+        if (c == cc) po = xs - a0;
+        if (cdup != cc) continue;  // warp-uniform
+        for (int idx = lane; idx < F::PR * F::CH; idx += 32) {
+            const int r = idx / F::CH, ch = idx - r * F::CH;
+            const int y = clampi(B.y0 + ccy - F::R + r, 0, P.H - 1);
+            const int cs = a0 + 16 * ch;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (cs >= 0 && cs + 16 <= W) v = __ldg(reinterpret_cast<const uint4*>(B.ref + size_t(y) * W + cs));
+            *reinterpret_cast<uint4*>(patch + cc * F::WORDS + r * F::PWW + 4 * ch) = v;
+        }
+    }
+    // the patch my candidate's BRS score reads (duplicates share one)
+    const int mpo = __shfl_sync(0xFFFFFFFFu, po, 8 * md);
     // current block: every lane holds all of it (broadcast loads)
     uint32_t cb[BS][NW];
 #pragma unroll
@@ -1200,10 +1273,11 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
 #pragma unroll
         for (int r = 0; r < BS; ++r) {
             if ((r & 7) != sub) continue;
-            const uint32_t* row = pc + (F::R + r) * F::PWW + F::R / 4;  // byte R: word aligned
+            uint32_t w[NW];
+            patch_words<BS>(pc + (F::R + r) * F::PWW, F::R + mpo, w);
             uint32_t acc = 0;
 #pragma unroll
-            for (int k = 0; k < NW; ++k) acc = vad4(cb[r][k], row[k], acc);
+            for (int k = 0; k < NW; ++k) acc = vad4(cb[r][k], w[k], acc);
             s += acc * 4u;
         }
     }
@@ -1223,60 +1297,63 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
     const bool win_shape = boundary && (win < 3 || P.bt_shape);
     const int wx = __shfl_sync(0xFFFFFFFFu, myx, 8 * win), wy = __shfl_sync(0xFFFFFFFFu, myy, 8 * win);
     const int wp = __shfl_sync(0xFFFFFFFFu, md, 8 * win);
+    const int wo = __shfl_sync(0xFFFFFFFFu, mpo, 8 * win);  // its byte offset
     const uint32_t* pw = patch + wp * F::WORDS;  // the winner's patch
-    // --- all 81 lattice costs around the winner ---------------------------------
-    // lane = (column i, group of 3 rows j); each shifted patch row is read once
-    // and reused for every j it pairs with.
-    if (lane < 3 * L) {
-        const int i = lane % L, jg = lane / L, j0 = 3 * jg;
-        uint32_t acc[3] = {0u, 0u, 0u};
-#pragma unroll
-        for (int pr = 0; pr < BS + 2; ++pr) {  // patch rows j0 .. j0 + BS + 1
-            uint32_t w[NW];
-            patch_words<BS>(pw + (j0 + pr) * F::PWW, i, w);
-#pragma unroll
-            for (int jj = 0; jj < 3; ++jj) {
-                const int r = pr - jj;  // block row paired with this patch row at j = j0 + jj
-                if (r >= 0 && r < BS) {
-#pragma unroll
-                    for (int k = 0; k < NW; ++k) acc[jj] = vad4(cb[r][k], w[k], acc[jj]);
-                }
-            }
-        }
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) {
-            const int j = j0 + jj;
-            const int vx = wx + 2 * (i - F::R), vy = wy + 2 * (j - F::R);
-            const bool adm = vx >= B.w.lo_x && vx <= B.w.hi_x && vy >= B.w.lo_y && vy <= B.w.hi_y;
-            table[j * L + i] = adm ? acc[jj] * 4u : kInf;
-        }
-    }
+    // --- prs_refine (estimators.cpp:311-382), lazily from the staged patch ----
+    // Each iteration scores the centre's 8 neighbours: lanes 4k..4k+3 own
+    // neighbour k, BS/4 block rows each; all reads hit shared memory.
+    uint32_t* vis = table;  // [3] visited lattice bits (9 x 9 around the start)
+    if (lane < 3) vis[lane] = lane == 1 ? (1u << (F::R * L + F::R - 32)) : 0u;
     __syncwarp();
-    // --- prs_refine (estimators.cpp:311-382) as lookups ------------------------
-    uint32_t ccost = win_shape ? table[F::R * L + F::R] : best;
-    // Unique-evaluation counting (:321-332): a neighbour of the current centre
-    // was evaluated before iff it is the start or lies in the 3x3 neighbourhood
-    // of an earlier centre (each iteration evaluates all admissible neighbours).
-    int pcx[4] = {99, 99, 99, 99}, pcy[4] = {99, 99, 99, 99};
-    int ci = 0, cj = 0;
+    uint32_t ccost = best;
+    if (win_shape) {  // the centre's texture cost was not computed by BRS
+        uint32_t t = 0;
+#pragma unroll
+        for (int r = 0; r < BS; ++r)
+            if ((r & 7) == sub) {
+                uint32_t w[NW];
+                patch_words<BS>(pw + (F::R + r) * F::PWW, F::R + wo, w);
+#pragma unroll
+                for (int kk = 0; kk < NW; ++kk) t = vad4(cb[r][kk], w[kk], t);
+            }
+        t = (c == 0) ? t : 0u;
+        ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
+    }
+    int ci = 0, cj = 0;  // centre, pels relative to the BRS winner
     uint32_t dpd = 1, iters = 0;
-    const int k = lane & 7;
+    const int k = lane >> 2, q = lane & 3;
     const int kx = c_off8[k][0], ky = c_off8[k][1];
     for (int it = 0; it < P.max_iter; ++it) {
         if (ccost == 0) break;  // already a global minimum (:341)
         const int px = ci + kx, py = cj + ky;
-        const uint32_t cost = table[(py + F::R) * L + px + F::R];
-        const bool adm = lane < 8 && cost != kInf;
-        bool seen = px == 0 && py == 0;
+        const bool adm = wx + 2 * px >= B.w.lo_x && wx + 2 * px <= B.w.hi_x &&
+                         wy + 2 * py >= B.w.lo_y && wy + 2 * py <= B.w.hi_y;
+        uint32_t part = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) seen |= abs(px - pcx[j]) <= 1 && abs(py - pcy[j]) <= 1;
-        dpd += __popc(__ballot_sync(0xFFFFFFFFu, adm && !seen));
-        const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, adm ? cost : kInf);
+        for (int r = 0; r < BS; ++r)
+            if ((r & 3) == q) {
+                uint32_t w[NW];
+                patch_words<BS>(pw + (F::R + py + r) * F::PWW, F::R + px + wo, w);
+#pragma unroll
+                for (int kk = 0; kk < NW; ++kk) part = vad4(cb[r][kk], w[kk], part);
+            }
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
+        const uint32_t cost = 4u * part;
+        const bool lead = adm && q == 0;
+        bool fresh = false;
+        if (lead) {  // unique aggregate evaluations (:321-332)
+            const int bit = (F::R + py) * L + F::R + px;
+            const uint32_t m = 1u << (bit & 31);
+            fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
+        }
+        dpd += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
+        const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, lead ? cost : kInf);
         if (m >= ccost) break;  // centre kept (:376)
-        const uint32_t ties = __ballot_sync(0xFFFFFFFFu, adm && cost == m);
+        const uint32_t ties = __ballot_sync(0xFFFFFFFFu, lead && cost == m);
         int w;
         if (__popc(ties) == 1) {
-            w = __ffs(ties) - 1;
+            w = (__ffs(ties) - 1) >> 2;
         } else {
             // stable descending sort by off . dir (:357-362): the first tied
             // neighbour in sorted order = largest key, lowest index on equal keys
@@ -1285,7 +1362,7 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
             w = -1;
             double bestkey = 0.0;
             for (int o = 0; o < 8; ++o) {
-                if (!((ties >> o) & 1u)) continue;
+                if (!((ties >> (4 * o)) & 1u)) continue;
                 const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x),
                                              __dmul_rn(double(c_off8[o][1]), dir_y));
                 if (w < 0 || key > bestkey) {
@@ -1294,12 +1371,6 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
                 }
             }
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j == it) {
-                pcx[j] = ci;
-                pcy[j] = cj;
-            }
         ci += c_off8[w][0];
         cj += c_off8[w][1];
         ccost = m;
@@ -1311,7 +1382,7 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
     for (int r = 0; r < BS; ++r) {
         if (r != lane) continue;
         uint32_t w[NW];
-        patch_words<BS>(pw + (F::R + cj + r) * F::PWW, F::R + ci, w);
+        patch_words<BS>(pw + (F::R + cj + r) * F::PWW, F::R + ci + wo, w);
 #pragma unroll
         for (int kk = 0; kk < NW; ++kk) se = sq4(cb[r][kk], w[kk], se);
     }
@@ -1325,7 +1396,7 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
 }
 
 template <int BS>
-__global__ void __launch_bounds__(512, 1) pa_kernel(PaArgs a) {
+__global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
     extern __shared__ uint32_t s_pa[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t* ws = s_pa + wid * a.warp_words;
@@ -1782,9 +1853,14 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     const size_t hist_smem = size_t(nbins) * 4;
     {
         const int threads = 256;
-        int grid = int(std::min<int64_t>((nb + threads - 1) / threads, int64_t(num_sms) * 8));
+        // a 16-pixel strip per thread: two 8x8 blocks or one 16x16 block (W % 16 == 0)
+        const int64_t strips = nb / (16 / b.bs);
+        int grid = int(std::min<int64_t>((strips + threads - 1) / threads, int64_t(num_sms) * 8));
         if (grid < 1) grid = 1;
-        classify_kernel<<<grid, threads, hist_smem, st>>>(ca);
+        if (b.bs == 8)
+            classify_kernel<8><<<grid, threads, hist_smem, st>>>(ca);
+        else
+            classify_kernel<16><<<grid, threads, hist_smem, st>>>(ca);
         if ((e = cudaGetLastError())) return e;
     }
     if (events) cudaEventRecord(events[1], st);
@@ -1843,7 +1919,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             cudaMalloc(&pa_args.trace, size_t(n_host) * 32);
             cudaMemset(pa_args.trace, 0, size_t(n_host) * 32);
         }
-        const int threads = 512;
+        const int threads = 256;
         pa_args.warp_words = std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
         const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
         auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
