@@ -81,6 +81,21 @@ me_status upload(me_ctx* ctx, DevBuf& buf, size_t off, const void* host, size_t 
 
 size_t pad16(size_t n) { return (n + 15) & ~size_t(15); }
 
+constexpr int kPipelineChunks = 8;
+
+// Lazily creates the copy / d2h streams and the chunk events of the
+// host-pointer pipeline.
+me_status ensure_pipeline(me_ctx* ctx) {
+    if (ctx->copy_stream) return ME_OK;
+    ME_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    ME_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < kPipelineChunks; ++k) {
+        ME_CUDA(cudaEventCreateWithFlags(&ctx->ev_in[k], cudaEventDisableTiming));
+        ME_CUDA(cudaEventCreateWithFlags(&ctx->ev_out[k], cudaEventDisableTiming));
+    }
+    return ME_OK;
+}
+
 me_status sync(me_ctx* ctx) {
     ME_CUDA(cudaStreamSynchronize(ctx->stream));
     ME_CUDA(cudaGetLastError());
@@ -153,6 +168,14 @@ void me_b200_ctx_destroy(me_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamSynchronize(c->d2h_stream);
+        for (auto& e : c->ev_in) cudaEventDestroy(e);
+        for (auto& e : c->ev_out) cudaEventDestroy(e);
+        cudaStreamDestroy(c->copy_stream);
+        cudaStreamDestroy(c->d2h_stream);
+    }
     for (DevBuf* b : {&c->types, &c->worklist, &c->counters, &c->tasks, &c->in_luma, &c->in_alpha,
                       &c->out_recs, &c->out_stats, &c->out_pred, &c->aux})
         b->release();
@@ -258,33 +281,54 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
     if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
     const size_t plane = size_t(W) * H;
-    const size_t in_bytes = plane * n_frames * n_seq;
+    const size_t seq_bytes = plane * n_frames;
     const int pairs = n_frames - cfg->ref_distance;
-    const size_t nrec = size_t(n_seq) * pairs * (W / cfg->block_size) * (H / cfg->block_size);
-    ME_CUDA(ctx->in_luma.reserve(in_bytes + 256));
-    if (alpha) ME_CUDA(ctx->in_alpha.reserve(in_bytes + 256));
-    ME_CUDA(ctx->out_recs.reserve(nrec * sizeof(me_block_rec)));
+    const size_t seq_recs = size_t(pairs) * (W / cfg->block_size) * (H / cfg->block_size);
+    ME_CUDA(ctx->in_luma.reserve(seq_bytes * n_seq + 256));
+    if (alpha) ME_CUDA(ctx->in_alpha.reserve(seq_bytes * n_seq + 256));
+    ME_CUDA(ctx->out_recs.reserve(seq_recs * n_seq * sizeof(me_block_rec)));
     ME_CUDA(ctx->out_stats.reserve(size_t(n_seq) * pairs * sizeof(me_pair_stats)));
     if (pred) ME_CUDA(ctx->out_pred.reserve(plane * pairs * n_seq));
-    ME_CUDA(cudaMemcpyAsync(ctx->in_luma.p, luma, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    if (alpha)
-        ME_CUDA(cudaMemcpyAsync(ctx->in_alpha.p, alpha, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    const mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H,
-                                    static_cast<const uint8_t*>(ctx->in_luma.p),
-                                    alpha ? static_cast<const uint8_t*>(ctx->in_alpha.p) : nullptr);
-    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
-    ME_CUDA(mek::run_batch(b, *cfg, nullptr, static_cast<me_block_rec*>(ctx->out_recs.p),
-                           static_cast<me_pair_stats*>(ctx->out_stats.p),
-                           pred ? static_cast<uint8_t*>(ctx->out_pred.p) : nullptr, ctx->tasks.p,
-                           ctx->tasks.cap, ctx->num_sms, ctx->stream, ctx->events()));
-    ctx->ev_valid = ctx->profiling;
-    ME_CUDA(cudaMemcpyAsync(recs, ctx->out_recs.p, nrec * sizeof(me_block_rec),
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    ME_CUDA(cudaMemcpyAsync(stats, ctx->out_stats.p, size_t(n_seq) * pairs * sizeof(me_pair_stats),
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    if (pred)
-        ME_CUDA(cudaMemcpyAsync(pred, ctx->out_pred.p, plane * pairs * n_seq, cudaMemcpyDeviceToHost,
-                                ctx->stream));
+    if ((s = ensure_pipeline(ctx))) return s;
+    // Chunked pipeline: the sequences are independent, so chunk k's H2D (copy
+    // stream) overlaps chunk k-1's estimation (compute stream) and chunk
+    // k-2's D2H (d2h stream).  PCIe is the bound of this path.
+    const int nchunks = std::min(n_seq, kPipelineChunks);
+    uint8_t* dl = static_cast<uint8_t*>(ctx->in_luma.p);
+    uint8_t* da = static_cast<uint8_t*>(ctx->in_alpha.p);
+    me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
+    me_pair_stats* ds = static_cast<me_pair_stats*>(ctx->out_stats.p);
+    uint8_t* dp = static_cast<uint8_t*>(ctx->out_pred.p);
+    for (int k = 0; k < nchunks; ++k) {
+        const int s0 = int(int64_t(n_seq) * k / nchunks), s1 = int(int64_t(n_seq) * (k + 1) / nchunks);
+        const size_t o = seq_bytes * s0, n = seq_bytes * (s1 - s0);
+        ME_CUDA(cudaMemcpyAsync(dl + o, luma + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
+        if (alpha) ME_CUDA(cudaMemcpyAsync(da + o, alpha + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
+        ME_CUDA(cudaEventRecord(ctx->ev_in[k], ctx->copy_stream));
+    }
+    for (int k = 0; k < nchunks; ++k) {
+        const int s0 = int(int64_t(n_seq) * k / nchunks), s1 = int(int64_t(n_seq) * (k + 1) / nchunks);
+        const int ns = s1 - s0;
+        ME_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[k], 0));
+        const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, dl + seq_bytes * s0,
+                                        alpha ? da + seq_bytes * s0 : nullptr);
+        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+        ME_CUDA(mek::run_batch(b, *cfg, nullptr, dr + seq_recs * s0, ds + size_t(pairs) * s0,
+                               pred ? dp + plane * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
+                               ctx->num_sms, ctx->stream, nullptr));
+        ME_CUDA(cudaEventRecord(ctx->ev_out[k], ctx->stream));
+        ME_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_out[k], 0));
+        ME_CUDA(cudaMemcpyAsync(recs + seq_recs * s0, dr + seq_recs * s0, seq_recs * ns * sizeof(me_block_rec),
+                                cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        ME_CUDA(cudaMemcpyAsync(stats + size_t(pairs) * s0, ds + size_t(pairs) * s0,
+                                size_t(pairs) * ns * sizeof(me_pair_stats), cudaMemcpyDeviceToHost,
+                                ctx->d2h_stream));
+        if (pred)
+            ME_CUDA(cudaMemcpyAsync(pred + plane * pairs * s0, dp + plane * pairs * s0, plane * pairs * ns,
+                                    cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    }
+    ctx->ev_valid = false;
+    ME_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
     s = sync(ctx);
     return s ? s : ok();
 }

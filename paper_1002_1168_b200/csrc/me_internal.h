@@ -74,6 +74,9 @@ struct me_ctx {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     bool ev_valid = false;
     cudaEvent_t* events() { return profiling ? ev : nullptr; }
+    // host-pointer pipeline: H2D / D2H streams and per-chunk events
+    cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
 };
 
 #endif
