@@ -1802,7 +1802,7 @@ struct KeyParams {
 };
 
 KeyParams pa_key(const Batch& b) {
-    KeyParams k{2, 1};
+    KeyParams k{1, 0};
     if (const char* e = getenv("ME_PA_KEY_A")) k.a = std::max(1, atoi(e));
     if (const char* e = getenv("ME_PA_KEY_S")) k.s = std::max(0, atoi(e));
     if (int64_t(k.a) * (b.steps() - 1) + int64_t(k.s) * (b.n_seq - 1) + 1 > 12288) k = KeyParams{1, 0};
