@@ -1462,6 +1462,270 @@ __global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// pa_fast_kernel: the 8x8, integer-pel PA path of the benchmark (config 4),
+// written for a short instruction stream per block: kernel arguments by
+// value, no address-taken structs, decoded work-list entries, the current
+// block staged once in shared memory, 16-byte-chunk patch staging (two lanes
+// per patch row), lazy PRS on the staged patch.  Same algorithm and
+// dependency protocol as pa_kernel; blocks with a half-pel candidate fall
+// back to the generic path.
+// ---------------------------------------------------------------------------
+
+constexpr int kFastPR = 16;        // patch rows (8 + 2R)
+constexpr int kFastPWW = 12;       // patch row stride in words (8 used: two 16-byte chunks)
+constexpr int kFastPatch = kFastPR * kFastPWW;
+constexpr int kFastWarpWords = 4 * kFastPatch + 16 + 4;  // patches, current block, visited
+
+__device__ __noinline__ void pa_generic_task(const PaArgs& a, uint2 e, uint32_t mvw, uint32_t* bm,
+                                             int lane) {
+    const Batch& b = a.b;
+    int h, v, p, seq;
+    bool boundary;
+    const uint32_t g = decode_entry(b, e, h, v, p, seq, boundary);
+    const size_t plane = size_t(b.W) * b.H;
+    PaBlock B;
+    const size_t fc = size_t(seq) * b.F + p + b.d, fr = size_t(seq) * b.F + p;
+    B.cur = b.luma + fc * plane;
+    B.ref = b.luma + fr * plane;
+    B.ca = b.alpha ? b.alpha + fc * plane : nullptr;
+    B.ra = b.alpha ? b.alpha + fr * plane : nullptr;
+    B.x0 = h * 8;
+    B.y0 = v * 8;
+    B.w = hp_window(B.x0, B.y0, 8, a.P.W, a.P.H, a.P.S);
+    int rdx[4], rdy[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t w = __shfl_sync(0xFFFFFFFFu, mvw, i);
+        rdx[i] = mv_dx(w);
+        rdy[i] = mv_dy(w);
+    }
+    const PaResult r = pa_block(a.P, B, lane, boundary, rdx, rdy, bm);
+    uint32_t s = lane < 8 ? row_sse(B.cur, B.ref, a.P.W, a.P.H, B.x0, B.y0 + lane, 8, r.dx, r.dy) : 0u;
+    s = __reduce_add_sync(0xFFFFFFFFu, s);
+    if (lane == 0) {
+        const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+        write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters, ty, true);
+        if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), s, 4, r.dpd, ty);
+    }
+}
+
+// 2 words of a staged patch row: bytes [t, t + 8) of the row's 32 raw bytes.
+__device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, uint32_t& r1) {
+    const int q = t >> 2;
+    const uint32_t sh = uint32_t(t & 3) * 8;
+    const uint32_t w0 = row[q], w1 = row[q + 1], w2 = row[q + 2];
+    r0 = __funnelshift_r(w0, w1, sh);
+    r1 = __funnelshift_r(w1, w2, sh);
+}
+
+__global__ void __launch_bounds__(256, 3) pa_fast_kernel(const PaArgs a) {
+    extern __shared__ uint32_t s_pa[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* ws = s_pa + wid * kFastWarpWords;
+    uint32_t* patch = ws;                    // [4][16][12]
+    uint32_t* cw = ws + 4 * kFastPatch;      // [8][2] current block
+    uint32_t* vis = cw + 16;                 // [3] visited lattice bits
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int n = *a.nlist;
+    const int W = a.b.W, H = a.b.H, S = a.P.S;
+    const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
+    const size_t plane = size_t(W) * H;
+    const int c = lane >> 3, sub = lane & 7;
+    const int k = lane >> 2, q = lane & 3;   // PRS: neighbour k, rows q and q + 4
+    const int kx = c_off8[k][0], ky = c_off8[k][1];
+    // static round-robin over the wavefront-sorted list (see pa_kernel)
+    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+        const uint2 e = __ldg(a.list + item);
+        if (e.x == kInvalidEntry) continue;
+        const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
+        const uint32_t seq = e.y >> 16;
+        const bool boundary = (e.x & kBoundaryBit) != 0;
+        const uint32_t pair = seq * pairs + uint32_t(p);
+        const uint32_t g = (pair * rows + uint32_t(v)) * cols + uint32_t(h);
+        const uint32_t fref = seq * uint32_t(a.b.F) + uint32_t(p);
+        const uint8_t* cur = a.b.luma + size_t(fref + a.b.d) * plane;
+        const uint8_t* ref = a.b.luma + size_t(fref) * plane;
+        const int x0 = h * 8, y0 = v * 8;
+        const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
+        const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
+        // --- round A: current block -> smem, candidate MV words (lanes 0..3)
+        if (lane < 8) {
+            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cur + size_t(y0 + lane) * W + x0));
+            cw[2 * lane] = c2.x;
+            cw[2 * lane + 1] = c2.y;
+        }
+        uint32_t mvw = 0;
+        if (lane < 4) {
+            const uint32_t* src = nullptr;
+            if (lane == 0 && h > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - 1);
+            if (lane == 1 && v > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - cols);
+            if (lane == 2 && v > 0 && uint32_t(h) + 1 < cols) src = reinterpret_cast<const uint32_t*>(a.recs + g - cols + 1);
+            if (lane == 3 && p > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - rows * cols);
+            if (src) {
+                mvw = ld_relaxed(src);
+                while (mvw == kSentinel) {
+                    __nanosleep(a.poll_ns);
+                    mvw = ld_relaxed(src);
+                }
+            } else if (lane == 3 && a.prev0) {
+                const int i = v * int(cols) + h;
+                mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+            }
+        }
+        __syncwarp();
+        // my candidate (lanes 8c..8c+7 serve candidate c), clip_to_window (:275-276)
+        const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
+        const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
+        if (__any_sync(0xFFFFFFFFu, ((myx | myy) & 1) != 0)) {
+            pa_generic_task(a, e, mvw, ws, lane);
+            __syncwarp();
+            continue;
+        }
+        // duplicate candidates share a patch
+        int md = c;
+#pragma unroll
+        for (int j = 2; j >= 0; --j) {
+            const int jx = __shfl_sync(0xFFFFFFFFu, myx, 8 * j), jy = __shfl_sync(0xFFFFFFFFu, myy, 8 * j);
+            if (j < c && jx == myx && jy == myy) md = j;
+        }
+        // --- round B: patches of the distinct candidates, 16-byte chunks -------
+        {
+            const int r = lane >> 1, ch = lane & 1;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
+                const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
+                const int cdup = __shfl_sync(0xFFFFFFFFu, md, 8 * cc);
+                if (cdup != cc) continue;  // warp-uniform
+                const int cs = ((x0 + ccx - 4) & ~15) + 16 * ch;
+                const int y = clampi(y0 + ccy - 4 + r, 0, H - 1);
+                uint4 val = make_uint4(0u, 0u, 0u, 0u);
+                if (cs >= 0 && cs + 16 <= W) val = __ldg(reinterpret_cast<const uint4*>(ref + size_t(y) * W + cs));
+                *reinterpret_cast<uint4*>(patch + cc * kFastPatch + r * kFastPWW + 4 * ch) = val;
+            }
+        }
+        // shape scores (boundary blocks): my candidate, my row
+        const bool shape = boundary && (c < 3 || a.P.bt_shape);
+        uint32_t s = 0;
+        if (shape) {
+            const size_t ao = size_t(y0 + sub) * W + x0;
+            const uint8_t* ca = a.b.alpha + size_t(fref + a.b.d) * plane;
+            const uint8_t* ra = a.b.alpha + size_t(fref) * plane;
+            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(ca + ao));
+            uint32_t r0, r1;
+            ld8u(ra + ao + (myy >> 1) * W + (myx >> 1), r0, r1);
+            s = ((__popc(__vcmpne4(c2.x, r0)) + __popc(__vcmpne4(c2.y, r1))) >> 3) * (255u * 4u);
+        }
+        if (lane < 3) vis[lane] = lane == 1 ? (1u << (4 * 9 + 4 - 32)) : 0u;  // start = bit 40
+        __syncwarp();
+        // --- brs_select (estimators.cpp:257-301) --------------------------------
+        const uint32_t c0 = cw[2 * sub], c1 = cw[2 * sub + 1];  // my BRS row of the block
+        if (!shape) {
+            const int po = (x0 + (myx >> 1) - 4) & 15;
+            uint32_t w0, w1;
+            prow8(patch + md * kFastPatch + (4 + sub) * kFastPWW, 4 + po, w0, w1);
+            s = vad4(c1, w1, vad4(c0, w0, 0u)) * 4u;
+        }
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
+        uint32_t best = __shfl_sync(0xFFFFFFFFu, s, 0);
+        int win = 0;
+#pragma unroll
+        for (int i = 1; i < 4; ++i) {
+            const uint32_t si = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
+            if (si < best) {  // strict <: A, B, C, T tie order (:295)
+                best = si;
+                win = i;
+            }
+        }
+        const bool win_shape = boundary && (win < 3 || a.P.bt_shape);
+        const int wx = __shfl_sync(0xFFFFFFFFu, myx, 8 * win), wy = __shfl_sync(0xFFFFFFFFu, myy, 8 * win);
+        const int wp = __shfl_sync(0xFFFFFFFFu, md, 8 * win);
+        const uint32_t* pw = patch + wp * kFastPatch;
+        const int wo = (x0 + (wx >> 1) - 4) & 15;  // the winner patch's byte offset
+        // my two PRS rows of the block
+        const uint32_t ra0 = cw[2 * q], ra1 = cw[2 * q + 1], rb0 = cw[2 * q + 8], rb1 = cw[2 * q + 9];
+        uint32_t ccost = best;
+        if (win_shape) {  // the centre's texture cost was not computed by BRS
+            uint32_t w0, w1;
+            prow8(pw + (4 + sub) * kFastPWW, 4 + wo, w0, w1);
+            uint32_t t = c == 0 ? vad4(c1, w1, vad4(c0, w0, 0u)) : 0u;
+            ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
+        }
+        // --- prs_refine (estimators.cpp:311-382), lazily from the patch ---------
+        int ci = 0, cj = 0;
+        uint32_t dpd = 1, iters = 0;
+        for (int it = 0; it < a.P.max_iter; ++it) {
+            if (ccost == 0) break;  // already a global minimum (:341)
+            const int px = ci + kx, py = cj + ky;
+            const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
+            uint32_t w0, w1, w2, w3;
+            prow8(pw + (4 + py + q) * kFastPWW, 4 + px + wo, w0, w1);
+            prow8(pw + (8 + py + q) * kFastPWW, 4 + px + wo, w2, w3);
+            uint32_t part = vad4(rb1, w3, vad4(rb0, w2, vad4(ra1, w1, vad4(ra0, w0, 0u))));
+            part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
+            part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
+            const uint32_t cost = 4u * part;
+            const bool lead = adm && q == 0;
+            bool fresh = false;
+            if (lead) {  // unique aggregate evaluations (:321-332)
+                const int bit = (4 + py) * 9 + 4 + px;
+                const uint32_t m = 1u << (bit & 31);
+                fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
+            }
+            dpd += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
+            const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, lead ? cost : kInf);
+            if (m >= ccost) break;  // centre kept (:376)
+            const uint32_t ties = __ballot_sync(0xFFFFFFFFu, lead && cost == m);
+            int w;
+            if (__popc(ties) == 1) {
+                w = (__ffs(ties) - 1) >> 2;
+            } else {
+                // stable descending sort by off . dir (:357-362): the first tied
+                // neighbour in sorted order = largest key, lowest index on equal keys
+                PaBlock B;
+                B.cur = cur;
+                B.ref = ref;
+                B.ca = B.ra = nullptr;
+                B.x0 = x0;
+                B.y0 = y0;
+                double dir_x, dir_y;
+                prs_direction(a.P, B, lane, wx + 2 * ci, wy + 2 * cj, dir_x, dir_y);
+                w = -1;
+                double bestkey = 0.0;
+                for (int o = 0; o < 8; ++o) {
+                    if (!((ties >> (4 * o)) & 1u)) continue;
+                    const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x), __dmul_rn(double(c_off8[o][1]), dir_y));
+                    if (w < 0 || key > bestkey) {
+                        w = o;
+                        bestkey = key;
+                    }
+                }
+            }
+            ci += c_off8[w][0];
+            cj += c_off8[w][1];
+            ccost = m;
+            ++iters;
+        }
+        // --- fused predict_frame + psnr SSE at the final vector -----------------
+        uint32_t se = 0;
+        if (lane < 8) {
+            uint32_t w0, w1;
+            prow8(pw + (4 + cj + lane) * kFastPWW, 4 + ci + wo, w0, w1);
+            se = sq4(cw[2 * lane + 1], w1, sq4(cw[2 * lane], w0, 0u));
+        }
+        se = __reduce_add_sync(0xFFFFFFFFu, se);
+        if (lane == 0) {
+            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+            write_rec(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty, true);
+            if (a.stats) add_stats(a.stats + pair, se, 4, dpd, ty);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // mc_kernel: predict_frame (compensation.cpp:30-71) fused with the psnr SSE
 // (metrics.cpp:108-124) and the per-pair SearchStats reduction.  One thread
 // per 8-pixel row segment; the prediction is only stored when requested.
@@ -1920,9 +2184,13 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             cudaMemset(pa_args.trace, 0, size_t(n_host) * 32);
         }
         const int threads = 256;
-        pa_args.warp_words = std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
+        // 8x8 integer-pel blocks: the lean fast kernel (ME_PA_MODE=warp forces pa_kernel)
+        const char* mode = getenv("ME_PA_MODE");
+        const bool fast8 = b.bs == 8 && pa_args.fast && !(mode && std::string(mode) == "warp");
+        pa_args.warp_words = fast8 ? std::max(pa_args.P.bm_words, kFastWarpWords)
+                                   : std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
         const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
-        auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
+        auto kern = fast8 ? pa_fast_kernel : (b.bs == 8 ? pa_kernel<8> : pa_kernel<16>);
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
