@@ -1148,6 +1148,7 @@ struct PaArgs {
     int fast;              // patch fast path allowed (step 2, max_iter <= 4)
     int warp_words;        // shared words per warp
     int poll_ns;           // dependency poll interval
+    int* counter;          // dynamic item counter (zeroed) or null: static round robin
     unsigned long long* trace;  // debug: per entry {claimed, deps ready, done, smid} (ns)
 };
 
@@ -1518,7 +1519,8 @@ __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, 
     r1 = __funnelshift_r(w1, w2, sh);
 }
 
-__global__ void __launch_bounds__(256, 3) pa_fast_kernel(const PaArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     extern __shared__ uint32_t s_pa[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t* ws = s_pa + wid * kFastWarpWords;
@@ -1529,39 +1531,60 @@ __global__ void __launch_bounds__(256, 3) pa_fast_kernel(const PaArgs a) {
     const int n = *a.nlist;
     const int W = a.b.W, H = a.b.H, S = a.P.S;
     const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
-    const size_t plane = size_t(W) * H;
     const int c = lane >> 3, sub = lane & 7;
     const int k = lane >> 2, q = lane & 3;   // PRS: neighbour k, rows q and q + 4
     const int kx = c_off8[k][0], ky = c_off8[k][1];
     // static round-robin over the wavefront-sorted list (see pa_kernel)
-    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+    // Items are taken in list (wavefront) order, statically round robin or
+    // dynamically from a counter; either way the least unfinished item's
+    // dependencies are finished, so the wait below always makes progress.
+    // The next item is claimed one item ahead to hide the claim latency.
+    int* const ctr = a.counter;
+    int item = blockIdx.x * (blockDim.x >> 5) + wid, nxt = item + nwarps;
+    if (ctr) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(ctr, 2);
+        t = __shfl_sync(0xFFFFFFFFu, t, 0);
+        item = t;
+        nxt = t + 1;
+    }
+    for (; item < n;) {
         const uint2 e = __ldg(a.list + item);
+        item = nxt;
+        if (ctr) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(ctr, 1);
+            nxt = __shfl_sync(0xFFFFFFFFu, t, 0);
+        } else {
+            nxt += nwarps;
+        }
         if (e.x == kInvalidEntry) continue;
         const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
         const uint32_t seq = e.y >> 16;
         const bool boundary = (e.x & kBoundaryBit) != 0;
         const uint32_t pair = seq * pairs + uint32_t(p);
         const uint32_t g = (pair * rows + uint32_t(v)) * cols + uint32_t(h);
+        // plane offsets in 32 bits: the launcher routes batches of >= 4 GiB elsewhere
+        const uint32_t plane = uint32_t(W) * uint32_t(H);
         const uint32_t fref = seq * uint32_t(a.b.F) + uint32_t(p);
-        const uint8_t* cur = a.b.luma + size_t(fref + a.b.d) * plane;
-        const uint8_t* ref = a.b.luma + size_t(fref) * plane;
+        const uint32_t oref = fref * plane, ocur = oref + uint32_t(a.b.d) * plane;
         const int x0 = h * 8, y0 = v * 8;
         const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
         const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
-        // --- round A: current block -> smem, candidate MV words (lanes 0..3)
-        if (lane < 8) {
-            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(cur + size_t(y0 + lane) * W + x0));
-            cw[2 * lane] = c2.x;
-            cw[2 * lane + 1] = c2.y;
-        }
+        // --- round A: current block rows (lanes 0..7) and the candidates' MV
+        // words (lanes 0..3) in flight together
+        uint2 crow = make_uint2(0u, 0u);
+        if (lane < 8)
+            crow = __ldg(reinterpret_cast<const uint2*>(a.b.luma + (ocur + uint32_t(y0 + lane) * W + uint32_t(x0))));
         uint32_t mvw = 0;
-        if (lane < 4) {
-            const uint32_t* src = nullptr;
-            if (lane == 0 && h > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - 1);
-            if (lane == 1 && v > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - cols);
-            if (lane == 2 && v > 0 && uint32_t(h) + 1 < cols) src = reinterpret_cast<const uint32_t*>(a.recs + g - cols + 1);
-            if (lane == 3 && p > 0) src = reinterpret_cast<const uint32_t*>(a.recs + g - rows * cols);
-            if (src) {
+        {
+            int back = -1;  // records back from g: A 1, B cols, C cols - 1, T rows * cols
+            if (lane == 0 && h > 0) back = 1;
+            if (lane == 1 && v > 0) back = int(cols);
+            if (lane == 2 && v > 0 && uint32_t(h) + 1 < cols) back = int(cols) - 1;
+            if (lane == 3 && p > 0) back = int(rows * cols);
+            if (back >= 0) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
                 mvw = ld_relaxed(src);
                 while (mvw == kSentinel) {
                     __nanosleep(a.poll_ns);
@@ -1572,7 +1595,10 @@ __global__ void __launch_bounds__(256, 3) pa_fast_kernel(const PaArgs a) {
                 mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
             }
         }
-        __syncwarp();
+        if (lane < 8) {
+            cw[2 * lane] = crow.x;
+            cw[2 * lane + 1] = crow.y;
+        }
         // my candidate (lanes 8c..8c+7 serve candidate c), clip_to_window (:275-276)
         const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
         const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
@@ -1588,34 +1614,39 @@ __global__ void __launch_bounds__(256, 3) pa_fast_kernel(const PaArgs a) {
             const int jx = __shfl_sync(0xFFFFFFFFu, myx, 8 * j), jy = __shfl_sync(0xFFFFFFFFu, myy, 8 * j);
             if (j < c && jx == myx && jy == myy) md = j;
         }
-        // --- round B: patches of the distinct candidates, 16-byte chunks -------
+        // --- round B: all loads of the distinct candidates' patches (16-byte
+        // chunks, two lanes per patch row) and of the shape rows in flight
+        // together, then the shared-memory stores
+        const bool shape = boundary && (c < 3 || a.P.bt_shape);
+        uint2 cal = make_uint2(0u, 0u);
+        uint32_t ral0 = 0, ral1 = 0;
+        if (shape) {
+            const uint32_t ao = uint32_t(y0 + sub) * W + uint32_t(x0);
+            cal = __ldg(reinterpret_cast<const uint2*>(a.b.alpha + (ocur + ao)));
+            ld8u(a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1))), ral0, ral1);
+        }
         {
             const int r = lane >> 1, ch = lane & 1;
+            uint4 pv[4];
+            bool pd[4];
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
                 const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
-                const int cdup = __shfl_sync(0xFFFFFFFFu, md, 8 * cc);
-                if (cdup != cc) continue;  // warp-uniform
+                pd[cc] = __shfl_sync(0xFFFFFFFFu, md, 8 * cc) == cc;  // warp-uniform
                 const int cs = ((x0 + ccx - 4) & ~15) + 16 * ch;
                 const int y = clampi(y0 + ccy - 4 + r, 0, H - 1);
-                uint4 val = make_uint4(0u, 0u, 0u, 0u);
-                if (cs >= 0 && cs + 16 <= W) val = __ldg(reinterpret_cast<const uint4*>(ref + size_t(y) * W + cs));
-                *reinterpret_cast<uint4*>(patch + cc * kFastPatch + r * kFastPWW + 4 * ch) = val;
+                pv[cc] = make_uint4(0u, 0u, 0u, 0u);
+                if (pd[cc] && cs >= 0 && cs + 16 <= W)
+                    pv[cc] = __ldg(reinterpret_cast<const uint4*>(a.b.luma + (oref + uint32_t(y) * W + uint32_t(cs))));
             }
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+                if (pd[cc]) *reinterpret_cast<uint4*>(patch + cc * kFastPatch + r * kFastPWW + 4 * ch) = pv[cc];
         }
         // shape scores (boundary blocks): my candidate, my row
-        const bool shape = boundary && (c < 3 || a.P.bt_shape);
         uint32_t s = 0;
-        if (shape) {
-            const size_t ao = size_t(y0 + sub) * W + x0;
-            const uint8_t* ca = a.b.alpha + size_t(fref + a.b.d) * plane;
-            const uint8_t* ra = a.b.alpha + size_t(fref) * plane;
-            const uint2 c2 = __ldg(reinterpret_cast<const uint2*>(ca + ao));
-            uint32_t r0, r1;
-            ld8u(ra + ao + (myy >> 1) * W + (myx >> 1), r0, r1);
-            s = ((__popc(__vcmpne4(c2.x, r0)) + __popc(__vcmpne4(c2.y, r1))) >> 3) * (255u * 4u);
-        }
+        if (shape) s = ((__popc(__vcmpne4(cal.x, ral0)) + __popc(__vcmpne4(cal.y, ral1))) >> 3) * (255u * 4u);
         if (lane < 3) vis[lane] = lane == 1 ? (1u << (4 * 9 + 4 - 32)) : 0u;  // start = bit 40
         __syncwarp();
         // --- brs_select (estimators.cpp:257-301) --------------------------------
@@ -1685,8 +1716,8 @@ __global__ void __launch_bounds__(256, 3) pa_fast_kernel(const PaArgs a) {
                 // stable descending sort by off . dir (:357-362): the first tied
                 // neighbour in sorted order = largest key, lowest index on equal keys
                 PaBlock B;
-                B.cur = cur;
-                B.ref = ref;
+                B.cur = a.b.luma + ocur;
+                B.ref = a.b.luma + oref;
                 B.ca = B.ra = nullptr;
                 B.x0 = x0;
                 B.y0 = y0;
@@ -2169,6 +2200,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         pa_args.P = make_pa_params(b, cfg);
         pa_args.list = s.list;
         pa_args.nlist = nlist;
+        const char* sched = getenv("ME_PA_SCHED");
+        pa_args.counter = (sched && std::string(sched) == "dyn") ? s.counter : nullptr;
         pa_args.recs = recs;
         pa_args.prev0 = prev0;
         pa_args.stats = stats;
@@ -2186,11 +2219,15 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         const int threads = 256;
         // 8x8 integer-pel blocks: the lean fast kernel (ME_PA_MODE=warp forces pa_kernel)
         const char* mode = getenv("ME_PA_MODE");
-        const bool fast8 = b.bs == 8 && pa_args.fast && !(mode && std::string(mode) == "warp");
+        const bool fast8 = b.bs == 8 && pa_args.fast && !(mode && std::string(mode) == "warp") &&
+                           size_t(b.n_seq) * b.F * b.W * b.H < (size_t(1) << 32);
         pa_args.warp_words = fast8 ? std::max(pa_args.P.bm_words, kFastWarpWords)
                                    : std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
         const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
-        auto kern = fast8 ? pa_fast_kernel : (b.bs == 8 ? pa_kernel<8> : pa_kernel<16>);
+        const char* minb = getenv("ME_PA_MINB");
+        const int mb = minb ? atoi(minb) : 5;
+        auto fk = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
+        auto kern = fast8 ? fk : (b.bs == 8 ? pa_kernel<8> : pa_kernel<16>);
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);

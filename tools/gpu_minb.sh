@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+timeout 180 python -m pytest tests/test_gpu_parity.py tests/test_golden.py -m gpu -q --timeout 100 -x 2>&1 | tail -2
+for mb in 3 4 5 6; do
+  ME_PA_MINB=$mb timeout 120 python bench.py --workload cfg4-pa --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/k.json 2>gpurun_out/k.log
+  python -c "import json;d=json.load(open('gpurun_out/k.json'));print('minb $mb', 'ms/step %.3f'%d['ms_per_step'], {k:round(v,3) for k,v in d['stages_ms'].items()})" || tail -3 gpurun_out/k.log
+done

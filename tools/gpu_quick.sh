@@ -4,5 +4,5 @@ for wl in cfg4-pa cfg2-pa; do
   timeout 120 python bench.py --workload $wl --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/k.json 2>gpurun_out/k.log
   python -c "import json;d=json.load(open('gpurun_out/k.json'));print('$wl', 'ms/step %.3f'%d['ms_per_step'], {k:round(v,3) for k,v in d['stages_ms'].items()})" || tail -3 gpurun_out/k.log
 done
-ME_PA_MODE=warp timeout 120 python bench.py --workload cfg4-pa --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/k.json 2>gpurun_out/k.log
-python -c "import json;d=json.load(open('gpurun_out/k.json'));print('cfg4 warp-mode', 'ms/step %.3f'%d['ms_per_step'], {k:round(v,3) for k,v in d['stages_ms'].items()})" || tail -3 gpurun_out/k.log
+ME_PA_MINB=4 timeout 120 python bench.py --workload cfg4-pa --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/k.json 2>gpurun_out/k.log
+python -c "import json;d=json.load(open('gpurun_out/k.json'));print('cfg4 minb4', 'ms/step %.3f'%d['ms_per_step'], {k:round(v,3) for k,v in d['stages_ms'].items()})" || tail -3 gpurun_out/k.log
