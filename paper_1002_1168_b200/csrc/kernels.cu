@@ -228,6 +228,18 @@ __device__ __forceinline__ void add_stats(me_pair_stats* st, uint32_t sse, uint3
     atomicAdd(s + (type == ME_OPAQUE ? 2 : (type == ME_BOUNDARY ? 3 : 4)), 1ull);
 }
 
+// PA blocks: the type counts and the 4 comparisons per block are added by
+// classify_kernel; the search adds only the SSE and the dpd count, as
+// fire-and-forget reductions.
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void add_stats_pa(me_pair_stats* st, uint32_t sse, uint32_t dpd) {
+    unsigned long long* s = reinterpret_cast<unsigned long long*>(st);
+    if (sse) red_add_u64(s + 5, sse);
+    red_add_u64(s + 1, dpd);
+}
+
 // The MV word is the whole payload a dependent block needs, and it is a single
 // 32-bit word: relaxed gpu-scope accesses suffice (no acquire fence, which
 // would invalidate the SM's L1 on every poll).
@@ -257,6 +269,15 @@ __device__ __forceinline__ void write_rec(me_block_rec* r, int dx, int dy, uint3
         st_relaxed(w, pack_mv(dx, dy));
     else
         w[0] = pack_mv(dx, dy);
+}
+
+// The whole record in one 16-byte store; its 32-bit MV word (element 0) is
+// single-copy atomic, which is all a dependent block reads.
+__device__ __forceinline__ void write_rec_v4(me_block_rec* r, int dx, int dy, uint32_t cost_q4,
+                                             uint32_t cmp, uint32_t dpd, uint32_t iters, uint32_t type) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(r), "r"(pack_mv(dx, dy)),
+                 "r"(cost_q4), "r"((cmp & 0xFFFF) | (dpd << 16)), "r"((iters & 0xFF) | ((type & 0xFF) << 8))
+                 : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -329,7 +350,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
     // uniform trip count so whole warps reach the warp-level reductions
     for (int64_t s0 = int64_t(blockIdx.x) * blockDim.x; s0 < n; s0 += stride) {
         const int64_t si = s0 + threadIdx.x;
-        uint32_t sse = 0, n_t = 0;
+        uint32_t sse = 0, n_t = 0, n_o = 0, n_b = 0;
         int64_t gp = -1;
         if (si < n) {
             const int hs = int(si % strips);
@@ -390,6 +411,8 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
                 *reinterpret_cast<uint4*>(a.recs + g) = r;
                 if (ty != ME_TRANSPARENT) {
                     atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
+                    n_o += ty == ME_OPAQUE;
+                    n_b += ty == ME_BOUNDARY;
                 } else {
                     sse += s;
                     n_t += 1;
@@ -399,18 +422,27 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
         if (a.stats) {
             const int64_t gp0 = __shfl_sync(0xFFFFFFFFu, gp, 0);
             const bool uniform = __all_sync(0xFFFFFFFFu, gp == gp0 || gp < 0);
+            if (!a.pa) n_o = n_b = 0;  // the other searches count their own blocks
             if (uniform) {
                 const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, sse);
                 const uint32_t wn = __reduce_add_sync(0xFFFFFFFFu, n_t);
-                if (lane == 0 && wn) {
+                const uint32_t wo = __reduce_add_sync(0xFFFFFFFFu, n_o);
+                const uint32_t wb = __reduce_add_sync(0xFFFFFFFFu, n_b);
+                if (lane == 0) {
                     unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp0);
-                    if (ws) atomicAdd(st + 5, static_cast<unsigned long long>(ws));
-                    atomicAdd(st + 4, static_cast<unsigned long long>(wn));
+                    if (ws) red_add_u64(st + 5, ws);
+                    if (wn) red_add_u64(st + 4, wn);
+                    if (wo) red_add_u64(st + 2, wo);
+                    if (wb) red_add_u64(st + 3, wb);
+                    if (wo + wb) red_add_u64(st + 0, 4ull * (wo + wb));  // brs_select: 4 per block (:290)
                 }
-            } else if (n_t) {
+            } else if (gp >= 0) {
                 unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp);
-                if (sse) atomicAdd(st + 5, static_cast<unsigned long long>(sse));
-                atomicAdd(st + 4, static_cast<unsigned long long>(n_t));
+                if (sse) red_add_u64(st + 5, sse);
+                if (n_t) red_add_u64(st + 4, n_t);
+                if (n_o) red_add_u64(st + 2, n_o);
+                if (n_b) red_add_u64(st + 3, n_b);
+                if (n_o + n_b) red_add_u64(st + 0, 4ull * (n_o + n_b));
             }
         }
     }
@@ -1448,7 +1480,7 @@ __global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
         if (lane == 0) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters, ty, true);
-            if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, 4, r.dpd, ty);
+            if (a.stats) add_stats_pa(a.stats + (size_t(seq) * b.pairs + p), sse, r.dpd);
             if (a.trace) {
                 unsigned smid;
                 asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1506,7 +1538,7 @@ __device__ __noinline__ void pa_generic_task(const PaArgs& a, uint2 e, uint32_t 
     if (lane == 0) {
         const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
         write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters, ty, true);
-        if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), s, 4, r.dpd, ty);
+        if (a.stats) add_stats_pa(a.stats + (size_t(seq) * b.pairs + p), s, r.dpd);
     }
 }
 
@@ -1749,8 +1781,8 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         se = __reduce_add_sync(0xFFFFFFFFu, se);
         if (lane == 0) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
-            write_rec(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty, true);
-            if (a.stats) add_stats(a.stats + pair, se, 4, dpd, ty);
+            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
+            if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
         }
         __syncwarp();
     }
