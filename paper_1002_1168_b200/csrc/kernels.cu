@@ -1631,6 +1631,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             cw[2 * lane] = crow.x;
             cw[2 * lane + 1] = crow.y;
         }
+        __syncwarp();  // reconverge after the polls (else the shuffles below take the divergent path)
         // my candidate (lanes 8c..8c+7 serve candidate c), clip_to_window (:275-276)
         const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
         const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
