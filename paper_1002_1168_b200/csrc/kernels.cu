@@ -1500,47 +1500,15 @@ __global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
 // value, no address-taken structs, decoded work-list entries, the current
 // block staged once in shared memory, 16-byte-chunk patch staging (two lanes
 // per patch row), lazy PRS on the staged patch.  Same algorithm and
-// dependency protocol as pa_kernel; blocks with a half-pel candidate fall
-// back to the generic path.
+// dependency protocol as pa_kernel.  All candidates are integer-pel: A, B, C
+// and T come from this integer-pel search (no external prev field, which may
+// be half-pel and is routed to pa_kernel).
 // ---------------------------------------------------------------------------
 
 constexpr int kFastPR = 16;        // patch rows (8 + 2R)
 constexpr int kFastPWW = 12;       // patch row stride in words (8 used: two 16-byte chunks)
 constexpr int kFastPatch = kFastPR * kFastPWW;
 constexpr int kFastWarpWords = 4 * kFastPatch + 16 + 4;  // patches, current block, visited
-
-__device__ __noinline__ void pa_generic_task(const PaArgs& a, uint2 e, uint32_t mvw, uint32_t* bm,
-                                             int lane) {
-    const Batch& b = a.b;
-    int h, v, p, seq;
-    bool boundary;
-    const uint32_t g = decode_entry(b, e, h, v, p, seq, boundary);
-    const size_t plane = size_t(b.W) * b.H;
-    PaBlock B;
-    const size_t fc = size_t(seq) * b.F + p + b.d, fr = size_t(seq) * b.F + p;
-    B.cur = b.luma + fc * plane;
-    B.ref = b.luma + fr * plane;
-    B.ca = b.alpha ? b.alpha + fc * plane : nullptr;
-    B.ra = b.alpha ? b.alpha + fr * plane : nullptr;
-    B.x0 = h * 8;
-    B.y0 = v * 8;
-    B.w = hp_window(B.x0, B.y0, 8, a.P.W, a.P.H, a.P.S);
-    int rdx[4], rdy[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t w = __shfl_sync(0xFFFFFFFFu, mvw, i);
-        rdx[i] = mv_dx(w);
-        rdy[i] = mv_dy(w);
-    }
-    const PaResult r = pa_block(a.P, B, lane, boundary, rdx, rdy, bm);
-    uint32_t s = lane < 8 ? row_sse(B.cur, B.ref, a.P.W, a.P.H, B.x0, B.y0 + lane, 8, r.dx, r.dy) : 0u;
-    s = __reduce_add_sync(0xFFFFFFFFu, s);
-    if (lane == 0) {
-        const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
-        write_rec(a.recs + g, r.dx, r.dy, r.cost_q4, 4, r.dpd, r.iters, ty, true);
-        if (a.stats) add_stats_pa(a.stats + (size_t(seq) * b.pairs + p), s, r.dpd);
-    }
-}
 
 // 2 words of a staged patch row: bytes [t, t + 8) of the row's 32 raw bytes.
 __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, uint32_t& r1) {
@@ -1615,16 +1583,12 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             if (lane == 1 && v > 0) back = int(cols);
             if (lane == 2 && v > 0 && uint32_t(h) + 1 < cols) back = int(cols) - 1;
             if (lane == 3 && p > 0) back = int(rows * cols);
-            if (back >= 0) {
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
-                mvw = ld_relaxed(src);
-                while (mvw == kSentinel) {
-                    __nanosleep(a.poll_ns);
-                    mvw = ld_relaxed(src);
-                }
-            } else if (lane == 3 && a.prev0) {
-                const int i = v * int(cols) + h;
-                mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
+            if (back >= 0) mvw = ld_relaxed(src);
+            // warp-uniform wait (a vote per poll keeps the warp converged)
+            while (__any_sync(0xFFFFFFFFu, back >= 0 && mvw == kSentinel)) {
+                __nanosleep(a.poll_ns);
+                if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
             }
         }
         if (lane < 8) {
@@ -1635,11 +1599,6 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         // my candidate (lanes 8c..8c+7 serve candidate c), clip_to_window (:275-276)
         const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
         const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
-        if (__any_sync(0xFFFFFFFFu, ((myx | myy) & 1) != 0)) {
-            pa_generic_task(a, e, mvw, ws, lane);
-            __syncwarp();
-            continue;
-        }
         // duplicate candidates share a patch
         int md = c;
 #pragma unroll
@@ -1781,6 +1740,257 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         }
         se = __reduce_add_sync(0xFFFFFFFFu, se);
         if (lane == 0) {
+            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
+            if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pa_duo_kernel: pa_fast_kernel's algorithm with TWO blocks per warp, one per
+// half-warp, so the per-block scalar work (decode, window, candidate
+// bookkeeping, reductions, loop control) is issued once for two blocks.  The
+// two blocks are consecutive list entries of the same wavefront step (the
+// sort pads every step to an even count), hence independent.  Patches are
+// staged with cp.async (no register staging).  Lanes of a half: BRS =
+// candidate x rows {q, q+4}; PRS = neighbour x rows {q, q+2, q+4, q+6}.
+// ---------------------------------------------------------------------------
+
+constexpr int kDuoTaskWords = 4 * kFastPatch + 16 + 4;  // patches, current block, visited
+constexpr int kDuoWarpWords = 2 * kDuoTaskWords;
+
+__device__ __forceinline__ void cp_async16(uint32_t* smem, const void* gmem, bool fill) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int n = fill ? 16 : 0;  // n = 0: zero-fill (patch columns outside the frame)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
+    extern __shared__ uint32_t s_pa[];
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int hf = lane >> 4, hl = lane & 15, hb = hf << 4;
+    const uint32_t hmask = hf ? 0xFFFF0000u : 0x0000FFFFu;
+    uint32_t* ws = s_pa + wid * kDuoWarpWords;
+    uint32_t* patch = ws + hf * kDuoTaskWords;  // [4][16][12]
+    uint32_t* cw = patch + 4 * kFastPatch;      // [8][2] current block
+    uint32_t* vis = cw + 16;                    // [3] visited lattice bits
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int n = *a.nlist;
+    const int W = a.b.W, H = a.b.H, S = a.P.S;
+    const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
+    const uint32_t plane = uint32_t(W) * uint32_t(H);
+    const int c = hl >> 2, q4 = hl & 3;  // BRS: candidate c, block rows q4 and q4 + 4
+    const int k = hl >> 1, q2 = hl & 1;  // PRS: neighbour k, block rows q2 + {0, 2, 4, 6}
+    const int kx = c_off8[k][0], ky = c_off8[k][1];
+    for (int item = 2 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 2 * nwarps) {
+        const uint2 e = __ldg(a.list + item + hf);
+        const bool act = e.x != kInvalidEntry;  // uniform per half
+        if (!__any_sync(FULL, act)) continue;
+        const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
+        const uint32_t seq = e.y >> 16;
+        const bool boundary = (e.x & kBoundaryBit) != 0;
+        const uint32_t pair = seq * pairs + uint32_t(p);
+        const uint32_t g = (pair * rows + uint32_t(v)) * cols + uint32_t(h);
+        const uint32_t fref = seq * uint32_t(a.b.F) + uint32_t(p);
+        const uint32_t oref = fref * plane, ocur = oref + uint32_t(a.b.d) * plane;
+        const int x0 = h * 8, y0 = v * 8;
+        const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
+        const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
+        // --- round A: current rows (lanes 0..7 of a half) + MV words (0..3) ----
+        uint2 crow = make_uint2(0u, 0u);
+        if (act && hl < 8)
+            crow = __ldg(reinterpret_cast<const uint2*>(a.b.luma + (ocur + uint32_t(y0 + hl) * W + uint32_t(x0))));
+        uint32_t mvw = 0;
+        {
+            int back = -1;  // records back from g: A 1, B cols, C cols - 1, T rows * cols
+            if (act && hl == 0 && h > 0) back = 1;
+            if (act && hl == 1 && v > 0) back = int(cols);
+            if (act && hl == 2 && v > 0 && uint32_t(h) + 1 < cols) back = int(cols) - 1;
+            if (act && hl == 3 && p > 0) back = int(rows * cols);
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
+            if (back >= 0) mvw = ld_relaxed(src);
+            // warp-uniform wait (a vote per poll keeps the warp converged)
+            while (__any_sync(FULL, back >= 0 && mvw == kSentinel)) {
+                __nanosleep(a.poll_ns);
+                if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
+            }
+        }
+        if (hl < 8) {
+            cw[2 * hl] = crow.x;
+            cw[2 * hl + 1] = crow.y;
+        }
+        if (hl < 3) vis[hl] = hl == 1 ? (1u << (4 * 9 + 4 - 32)) : 0u;  // start = bit 40
+        __syncwarp();
+        // my candidate, clip_to_window (:275-276)
+        const uint32_t mine = __shfl_sync(FULL, mvw, hb + c);
+        const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
+        // duplicate candidates share a patch
+        int md = c;
+#pragma unroll
+        for (int j = 2; j >= 0; --j) {
+            const int jx = __shfl_sync(FULL, myx, hb + 4 * j), jy = __shfl_sync(FULL, myy, hb + 4 * j);
+            if (j < c && jx == myx && jy == myy) md = j;
+        }
+        // --- round B: patches of the distinct candidates (cp.async, lane = patch
+        // row, two 16-byte chunks) and the shape rows, all in flight together ----
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const int ccx = __shfl_sync(FULL, myx, hb + 4 * cc) >> 1;
+            const int ccy = __shfl_sync(FULL, myy, hb + 4 * cc) >> 1;
+            const bool own = __shfl_sync(FULL, md, hb + 4 * cc) == cc;  // uniform per half
+            if (act && own) {
+                const int cs = (x0 + ccx - 4) & ~15;
+                const int y = clampi(y0 + ccy - 4 + hl, 0, H - 1);
+                const uint8_t* src = a.b.luma + (oref + uint32_t(y) * W);
+                uint32_t* dst = patch + cc * kFastPatch + hl * kFastPWW;
+                const bool in0 = cs >= 0 && cs + 16 <= W, in1 = cs + 16 >= 0 && cs + 32 <= W;
+                cp_async16(dst, in0 ? src + cs : src, in0);
+                cp_async16(dst + 4, in1 ? src + cs + 16 : src, in1);
+            }
+        }
+        const bool shape = act && boundary && (c < 3 || a.P.bt_shape);
+        uint2 ca0 = make_uint2(0u, 0u), ca1 = ca0;
+        uint32_t r00 = 0, r01 = 0, r10 = 0, r11 = 0;
+        if (shape) {
+            const uint32_t ao = uint32_t(y0 + q4) * W + uint32_t(x0);
+            const uint8_t* cap = a.b.alpha + (ocur + ao);
+            const uint8_t* rap = a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1)));
+            ca0 = __ldg(reinterpret_cast<const uint2*>(cap));
+            ca1 = __ldg(reinterpret_cast<const uint2*>(cap + 4 * W));
+            ld8u(rap, r00, r01);
+            ld8u(rap + 4 * W, r10, r11);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        // --- brs_select (estimators.cpp:257-301) ------------------------------
+        uint32_t s;
+        if (shape) {
+            s = ((__popc(__vcmpne4(ca0.x, r00)) + __popc(__vcmpne4(ca0.y, r01)) + __popc(__vcmpne4(ca1.x, r10)) +
+                  __popc(__vcmpne4(ca1.y, r11))) >> 3) * (255u * 4u);
+        } else {
+            const int po = (x0 + (myx >> 1) - 4) & 15;
+            const uint32_t* pr = patch + md * kFastPatch + (4 + q4) * kFastPWW;
+            uint32_t w0, w1, w2, w3;
+            prow8(pr, 4 + po, w0, w1);
+            prow8(pr + 4 * kFastPWW, 4 + po, w2, w3);
+            s = vad4(cw[2 * q4 + 9], w3, vad4(cw[2 * q4 + 8], w2, vad4(cw[2 * q4 + 1], w1, vad4(cw[2 * q4], w0, 0u)))) * 4u;
+        }
+        s += __shfl_xor_sync(FULL, s, 1);
+        s += __shfl_xor_sync(FULL, s, 2);
+        uint32_t best = __shfl_sync(FULL, s, hb);
+        int win = 0;
+#pragma unroll
+        for (int i = 1; i < 4; ++i) {
+            const uint32_t si = __shfl_sync(FULL, s, hb + 4 * i);
+            if (si < best) {  // strict <: A, B, C, T tie order (:295)
+                best = si;
+                win = i;
+            }
+        }
+        const bool win_shape = boundary && (win < 3 || a.P.bt_shape);
+        const int wx = __shfl_sync(FULL, myx, hb + 4 * win), wy = __shfl_sync(FULL, myy, hb + 4 * win);
+        const int wp = __shfl_sync(FULL, md, hb + 4 * win);
+        const uint32_t* pw = patch + wp * kFastPatch;
+        const int wo = (x0 + (wx >> 1) - 4) & 15;  // the winner patch's byte offset
+        uint32_t ccost = best;
+        if (__any_sync(FULL, act && win_shape)) {  // the centre's texture cost was not computed by BRS
+            uint32_t w0, w1, w2, w3;
+            prow8(pw + (4 + q4) * kFastPWW, 4 + wo, w0, w1);
+            prow8(pw + (8 + q4) * kFastPWW, 4 + wo, w2, w3);
+            uint32_t t = c == 0 ? vad4(cw[2 * q4 + 9], w3, vad4(cw[2 * q4 + 8], w2, vad4(cw[2 * q4 + 1], w1, vad4(cw[2 * q4], w0, 0u)))) : 0u;
+            t += __shfl_xor_sync(FULL, t, 1);
+            t += __shfl_xor_sync(FULL, t, 2);
+            t = __shfl_sync(FULL, t, hb);
+            if (win_shape) ccost = 4u * t;
+        }
+        // --- prs_refine (estimators.cpp:311-382), lazily from the patch -------
+        int ci = 0, cj = 0;
+        uint32_t dpd = 1, iters = 0;
+        bool alive = act;
+        for (int it = 0; it < a.P.max_iter; ++it) {
+            alive = alive && ccost != 0;  // already a global minimum (:341)
+            if (!__any_sync(FULL, alive)) break;
+            const int px = ci + kx, py = cj + ky;
+            const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
+            const uint32_t* pr = pw + (4 + py + q2) * kFastPWW;
+            const int tt = 4 + px + wo;
+            uint32_t w0, w1, part = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {  // block rows q2 + 2i (current rows re-read from smem: registers)
+                const uint2 cr = *reinterpret_cast<const uint2*>(cw + 2 * q2 + 4 * i);
+                prow8(pr + 2 * i * kFastPWW, tt, w0, w1);
+                part = vad4(cr.y, w1, vad4(cr.x, w0, part));
+            }
+            part += __shfl_xor_sync(FULL, part, 1);
+            const uint32_t cost = 4u * part;
+            const bool lead = alive && adm && q2 == 0;
+            bool fresh = false;
+            if (lead) {  // unique aggregate evaluations (:321-332)
+                const int bit = (4 + py) * 9 + 4 + px;
+                const uint32_t m = 1u << (bit & 31);
+                fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
+            }
+            dpd += __popc(__ballot_sync(FULL, fresh) & hmask);
+            uint32_t m = lead ? cost : kInf;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+            const bool move = alive && m < ccost;  // else the centre is kept (:376)
+            const uint32_t ties = (__ballot_sync(FULL, lead && cost == m) & hmask) >> hb;
+            int w = (__ffs(ties) - 1) >> 1;
+            const bool tie = move && __popc(ties) > 1;
+            if (__any_sync(FULL, tie)) {
+                // stable descending sort by off . dir (:357-362), computed with the
+                // full warp for each half that needs it
+#pragma unroll 1
+                for (int t = 0; t < 2; ++t) {
+                    if (!__shfl_sync(FULL, tie, 16 * t)) continue;  // warp-uniform
+                    PaBlock B;
+                    B.cur = a.b.luma + __shfl_sync(FULL, ocur, 16 * t);
+                    B.ref = a.b.luma + __shfl_sync(FULL, oref, 16 * t);
+                    B.ca = B.ra = nullptr;
+                    B.x0 = __shfl_sync(FULL, x0, 16 * t);
+                    B.y0 = __shfl_sync(FULL, y0, 16 * t);
+                    const int cx = __shfl_sync(FULL, wx + 2 * ci, 16 * t), cy = __shfl_sync(FULL, wy + 2 * cj, 16 * t);
+                    double dir_x, dir_y;
+                    prs_direction(a.P, B, lane, cx, cy, dir_x, dir_y);
+                    if (hf == t) {
+                        int wb = -1;
+                        double bestkey = 0.0;
+                        for (int o = 0; o < 8; ++o) {
+                            if (!((ties >> (2 * o)) & 1u)) continue;
+                            const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x), __dmul_rn(double(c_off8[o][1]), dir_y));
+                            if (wb < 0 || key > bestkey) {
+                                wb = o;
+                                bestkey = key;
+                            }
+                        }
+                        w = wb;
+                    }
+                }
+            }
+            if (move) {
+                ci += c_off8[w][0];
+                cj += c_off8[w][1];
+                ccost = m;
+                ++iters;
+            }
+            alive = move;
+        }
+        // --- fused predict_frame + psnr SSE at the final vector ---------------
+        uint32_t se = 0;
+        if (hl < 8) {
+            uint32_t w0, w1;
+            prow8(pw + (4 + cj + hl) * kFastPWW, 4 + ci + wo, w0, w1);
+            se = sq4(cw[2 * hl + 1], w1, sq4(cw[2 * hl], w0, 0u));
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) se += __shfl_xor_sync(FULL, se, o);
+        if (act && hl == 0) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
@@ -2149,6 +2359,17 @@ size_t scratch_bytes(const Batch& b, int algo) {
            align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4) + 256;
 }
 
+// 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel
+int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0) {
+    const int step = cfg.halfpel ? 1 : cfg.step;
+    const bool fast = b.bs == 8 && step == 2 && cfg.max_iterations <= 4 && !prev0 &&
+                      size_t(b.n_seq) * b.F * b.W * b.H < (size_t(1) << 32);
+    const char* mode = getenv("ME_PA_MODE");
+    const std::string m = mode ? mode : "duo";
+    if (!fast || m == "warp") return 0;
+    return m == "fast" ? 1 : 2;
+}
+
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
                       size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events) {
@@ -2192,7 +2413,12 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         if ((e = cudaGetLastError())) return e;
     }
     if (events) cudaEventRecord(events[1], st);
-    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, 1, s.offs, s.cursor, s.list);
+    // PA on 8x8 integer-pel blocks: pa_duo_kernel (default) or pa_fast_kernel
+    // (ME_PA_MODE=fast); ME_PA_MODE=warp forces the generic pa_kernel.  The duo
+    // kernel takes list entries in pairs: every wavefront step is padded to an
+    // even count.
+    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0) : 0;
+    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, pa_mode == 2 ? 2 : 1, s.offs, s.cursor, s.list);
     if ((e = cudaGetLastError())) return e;
     {
         const int threads = 256;
@@ -2251,16 +2477,19 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         }
         const int threads = 256;
         // 8x8 integer-pel blocks: the lean fast kernel (ME_PA_MODE=warp forces pa_kernel)
-        const char* mode = getenv("ME_PA_MODE");
-        const bool fast8 = b.bs == 8 && pa_args.fast && !(mode && std::string(mode) == "warp") &&
-                           size_t(b.n_seq) * b.F * b.W * b.H < (size_t(1) << 32);
-        pa_args.warp_words = fast8 ? std::max(pa_args.P.bm_words, kFastWarpWords)
-                                   : std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
+        pa_args.warp_words = pa_mode == 2   ? std::max(pa_args.P.bm_words, kDuoWarpWords)
+                             : pa_mode == 1 ? std::max(pa_args.P.bm_words, kFastWarpWords)
+                                            : std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
         const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
         const char* minb = getenv("ME_PA_MINB");
-        const int mb = minb ? atoi(minb) : 5;
-        auto fk = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
-        auto kern = fast8 ? fk : (b.bs == 8 ? pa_kernel<8> : pa_kernel<16>);
+        auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
+        if (pa_mode == 1) {
+            const int mb = minb ? atoi(minb) : 5;
+            kern = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
+        } else if (pa_mode == 2) {
+            const int mb = minb ? atoi(minb) : 3;
+            kern = mb == 4 ? pa_duo_kernel<4> : pa_duo_kernel<3>;
+        }
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
