@@ -1758,7 +1758,12 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
 // candidate x rows {q, q+4}; PRS = neighbour x rows {q, q+2, q+4, q+6}.
 // ---------------------------------------------------------------------------
 
-constexpr int kDuoTaskWords = 4 * kFastPatch + 16 + 4;  // patches, current block, visited
+#ifndef ME_DUO_PWW
+#define ME_DUO_PWW 8
+#endif
+constexpr int kDuoPWW = ME_DUO_PWW;            // patch row stride in words (8 used)
+constexpr int kDuoPatch = kFastPR * kDuoPWW;
+constexpr int kDuoTaskWords = 4 * kDuoPatch + 16 + 4;  // patches, current block, visited
 constexpr int kDuoWarpWords = 2 * kDuoTaskWords;
 
 __device__ __forceinline__ void cp_async16(uint32_t* smem, const void* gmem, bool fill) {
@@ -1768,8 +1773,8 @@ __device__ __forceinline__ void cp_async16(uint32_t* smem, const void* gmem, boo
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     extern __shared__ uint32_t s_pa[];
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1777,7 +1782,7 @@ __global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
     const uint32_t hmask = hf ? 0xFFFF0000u : 0x0000FFFFu;
     uint32_t* ws = s_pa + wid * kDuoWarpWords;
     uint32_t* patch = ws + hf * kDuoTaskWords;  // [4][16][12]
-    uint32_t* cw = patch + 4 * kFastPatch;      // [8][2] current block
+    uint32_t* cw = patch + 4 * kDuoPatch;      // [8][2] current block
     uint32_t* vis = cw + 16;                    // [3] visited lattice bits
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     const int n = *a.nlist;
@@ -1847,7 +1852,7 @@ __global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
                 const int cs = (x0 + ccx - 4) & ~15;
                 const int y = clampi(y0 + ccy - 4 + hl, 0, H - 1);
                 const uint8_t* src = a.b.luma + (oref + uint32_t(y) * W);
-                uint32_t* dst = patch + cc * kFastPatch + hl * kFastPWW;
+                uint32_t* dst = patch + cc * kDuoPatch + hl * kDuoPWW;
                 const bool in0 = cs >= 0 && cs + 16 <= W, in1 = cs + 16 >= 0 && cs + 32 <= W;
                 cp_async16(dst, in0 ? src + cs : src, in0);
                 cp_async16(dst + 4, in1 ? src + cs + 16 : src, in1);
@@ -1874,10 +1879,10 @@ __global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
                   __popc(__vcmpne4(ca1.y, r11))) >> 3) * (255u * 4u);
         } else {
             const int po = (x0 + (myx >> 1) - 4) & 15;
-            const uint32_t* pr = patch + md * kFastPatch + (4 + q4) * kFastPWW;
+            const uint32_t* pr = patch + md * kDuoPatch + (4 + q4) * kDuoPWW;
             uint32_t w0, w1, w2, w3;
             prow8(pr, 4 + po, w0, w1);
-            prow8(pr + 4 * kFastPWW, 4 + po, w2, w3);
+            prow8(pr + 4 * kDuoPWW, 4 + po, w2, w3);
             s = vad4(cw[2 * q4 + 9], w3, vad4(cw[2 * q4 + 8], w2, vad4(cw[2 * q4 + 1], w1, vad4(cw[2 * q4], w0, 0u)))) * 4u;
         }
         s += __shfl_xor_sync(FULL, s, 1);
@@ -1895,13 +1900,13 @@ __global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
         const bool win_shape = boundary && (win < 3 || a.P.bt_shape);
         const int wx = __shfl_sync(FULL, myx, hb + 4 * win), wy = __shfl_sync(FULL, myy, hb + 4 * win);
         const int wp = __shfl_sync(FULL, md, hb + 4 * win);
-        const uint32_t* pw = patch + wp * kFastPatch;
+        const uint32_t* pw = patch + wp * kDuoPatch;
         const int wo = (x0 + (wx >> 1) - 4) & 15;  // the winner patch's byte offset
         uint32_t ccost = best;
         if (__any_sync(FULL, act && win_shape)) {  // the centre's texture cost was not computed by BRS
             uint32_t w0, w1, w2, w3;
-            prow8(pw + (4 + q4) * kFastPWW, 4 + wo, w0, w1);
-            prow8(pw + (8 + q4) * kFastPWW, 4 + wo, w2, w3);
+            prow8(pw + (4 + q4) * kDuoPWW, 4 + wo, w0, w1);
+            prow8(pw + (8 + q4) * kDuoPWW, 4 + wo, w2, w3);
             uint32_t t = c == 0 ? vad4(cw[2 * q4 + 9], w3, vad4(cw[2 * q4 + 8], w2, vad4(cw[2 * q4 + 1], w1, vad4(cw[2 * q4], w0, 0u)))) : 0u;
             t += __shfl_xor_sync(FULL, t, 1);
             t += __shfl_xor_sync(FULL, t, 2);
@@ -1917,13 +1922,13 @@ __global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
             if (!__any_sync(FULL, alive)) break;
             const int px = ci + kx, py = cj + ky;
             const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
-            const uint32_t* pr = pw + (4 + py + q2) * kFastPWW;
+            const uint32_t* pr = pw + (4 + py + q2) * kDuoPWW;
             const int tt = 4 + px + wo;
             uint32_t w0, w1, part = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {  // block rows q2 + 2i (current rows re-read from smem: registers)
                 const uint2 cr = *reinterpret_cast<const uint2*>(cw + 2 * q2 + 4 * i);
-                prow8(pr + 2 * i * kFastPWW, tt, w0, w1);
+                prow8(pr + 2 * i * kDuoPWW, tt, w0, w1);
                 part = vad4(cr.y, w1, vad4(cr.x, w0, part));
             }
             part += __shfl_xor_sync(FULL, part, 1);
@@ -1985,7 +1990,7 @@ __global__ void __launch_bounds__(256, MINB) pa_duo_kernel(const PaArgs a) {
         uint32_t se = 0;
         if (hl < 8) {
             uint32_t w0, w1;
-            prow8(pw + (4 + cj + hl) * kFastPWW, 4 + ci + wo, w0, w1);
+            prow8(pw + (4 + cj + hl) * kDuoPWW, 4 + ci + wo, w0, w1);
             se = sq4(cw[2 * hl + 1], w1, sq4(cw[2 * hl], w0, 0u));
         }
 #pragma unroll
@@ -2475,8 +2480,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             cudaMalloc(&pa_args.trace, size_t(n_host) * 32);
             cudaMemset(pa_args.trace, 0, size_t(n_host) * 32);
         }
-        const int threads = 256;
-        // 8x8 integer-pel blocks: the lean fast kernel (ME_PA_MODE=warp forces pa_kernel)
+        const char* cta = getenv("ME_PA_CTA");
+        const int threads = pa_mode == 2 && cta ? atoi(cta) : 256;
         pa_args.warp_words = pa_mode == 2   ? std::max(pa_args.P.bm_words, kDuoWarpWords)
                              : pa_mode == 1 ? std::max(pa_args.P.bm_words, kFastWarpWords)
                                             : std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
@@ -2487,8 +2492,11 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             const int mb = minb ? atoi(minb) : 5;
             kern = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         } else if (pa_mode == 2) {
-            const int mb = minb ? atoi(minb) : 3;
-            kern = mb == 4 ? pa_duo_kernel<4> : pa_duo_kernel<3>;
+            const int mb = minb ? atoi(minb) : 4;
+            if (threads == 128)
+                kern = mb == 8 ? pa_duo_kernel<128, 8> : mb == 6 ? pa_duo_kernel<128, 6> : pa_duo_kernel<128, 7>;
+            else
+                kern = mb == 4 ? pa_duo_kernel<256, 4> : pa_duo_kernel<256, 3>;
         }
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
         int occ = 0;
