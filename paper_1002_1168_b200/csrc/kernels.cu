@@ -1773,7 +1773,7 @@ __device__ __forceinline__ void cp_async16(uint32_t* smem, const void* gmem, boo
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int THREADS, int MINB>
+template <int THREADS, int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     extern __shared__ uint32_t s_pa[];
     constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -1783,7 +1783,6 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     uint32_t* ws = s_pa + wid * kDuoWarpWords;
     uint32_t* patch = ws + hf * kDuoTaskWords;  // [4][16][12]
     uint32_t* cw = patch + 4 * kDuoPatch;      // [8][2] current block
-    uint32_t* vis = cw + 16;                    // [3] visited lattice bits
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     const int n = *a.nlist;
     const int W = a.b.W, H = a.b.H, S = a.P.S;
@@ -1795,6 +1794,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     for (int item = 2 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 2 * nwarps) {
         const uint2 e = __ldg(a.list + item + hf);
         const bool act = e.x != kInvalidEntry;  // uniform per half
+        unsigned long long t_claim = 0, t_ready = 0;
+        if (TRACE) t_claim = gtimer();
         if (!__any_sync(FULL, act)) continue;
         const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
         const uint32_t seq = e.y >> 16;
@@ -1810,7 +1811,19 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
         uint2 crow = make_uint2(0u, 0u);
         if (act && hl < 8)
             crow = __ldg(reinterpret_cast<const uint2*>(a.b.luma + (ocur + uint32_t(y0 + hl) * W + uint32_t(x0))));
+        // a candidate's 16 x 32-byte reference patch into slot `slot` (cp.async,
+        // lane = patch row, two 16-byte chunks; zero-fill outside the frame)
+        auto stage = [&](int slot, int cpx, int cpy) {
+            const int cs = (x0 + cpx - 4) & ~15;
+            const int y = clampi(y0 + cpy - 4 + hl, 0, H - 1);
+            const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
+            uint32_t* dst = patch + slot * kDuoPatch + hl * kDuoPWW;
+            const bool in0 = cs >= 0 && cs + 16 <= W, in1 = cs + 16 >= 0 && cs + 32 <= W;
+            cp_async16(dst, in0 ? rowp + cs : rowp, in0);
+            cp_async16(dst + 4, in1 ? rowp + cs + 16 : rowp, in1);
+        };
         uint32_t mvw = 0;
+        bool b_early;
         {
             int back = -1;  // records back from g: A 1, B cols, C cols - 1, T rows * cols
             if (act && hl == 0 && h > 0) back = 1;
@@ -1819,44 +1832,47 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             if (act && hl == 3 && p > 0) back = int(rows * cols);
             const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
             if (back >= 0) mvw = ld_relaxed(src);
+            // B lies two wavefront steps back and is usually final already: its
+            // patch (slot 1) goes out before the wait for A, C and T
+            const uint32_t mb = __shfl_sync(FULL, mvw, hb + 1);
+            b_early = act && mb != kSentinel;  // uniform per half
+            if (b_early)
+                stage(1, clip_comp(mv_dx(mb), lo_x, hi_x) >> 1, clip_comp(mv_dy(mb), lo_y, hi_y) >> 1);
             // warp-uniform wait (a vote per poll keeps the warp converged)
             while (__any_sync(FULL, back >= 0 && mvw == kSentinel)) {
                 __nanosleep(a.poll_ns);
                 if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
             }
         }
+        if (TRACE) t_ready = gtimer();
         if (hl < 8) {
             cw[2 * hl] = crow.x;
             cw[2 * hl + 1] = crow.y;
         }
-        if (hl < 3) vis[hl] = hl == 1 ? (1u << (4 * 9 + 4 - 32)) : 0u;  // start = bit 40
         __syncwarp();
         // my candidate, clip_to_window (:275-276)
         const uint32_t mine = __shfl_sync(FULL, mvw, hb + c);
         const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
-        // duplicate candidates share a patch
+        // duplicate candidates share a patch: B's slot first (it may be staged
+        // already), else the first equal candidate's
         int md = c;
+        {
+            const int bx = __shfl_sync(FULL, myx, hb + 4), by = __shfl_sync(FULL, myy, hb + 4);
 #pragma unroll
-        for (int j = 2; j >= 0; --j) {
-            const int jx = __shfl_sync(FULL, myx, hb + 4 * j), jy = __shfl_sync(FULL, myy, hb + 4 * j);
-            if (j < c && jx == myx && jy == myy) md = j;
+            for (int j = 2; j >= 0; --j) {
+                const int jx = __shfl_sync(FULL, myx, hb + 4 * j), jy = __shfl_sync(FULL, myy, hb + 4 * j);
+                if (j < c && jx == myx && jy == myy) md = j;
+            }
+            if (bx == myx && by == myy) md = 1;
         }
-        // --- round B: patches of the distinct candidates (cp.async, lane = patch
-        // row, two 16-byte chunks) and the shape rows, all in flight together ----
+        // --- round B: patches of the remaining distinct candidates and the
+        // shape rows, all in flight together ----------------------------------
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
             const int ccx = __shfl_sync(FULL, myx, hb + 4 * cc) >> 1;
             const int ccy = __shfl_sync(FULL, myy, hb + 4 * cc) >> 1;
             const bool own = __shfl_sync(FULL, md, hb + 4 * cc) == cc;  // uniform per half
-            if (act && own) {
-                const int cs = (x0 + ccx - 4) & ~15;
-                const int y = clampi(y0 + ccy - 4 + hl, 0, H - 1);
-                const uint8_t* src = a.b.luma + (oref + uint32_t(y) * W);
-                uint32_t* dst = patch + cc * kDuoPatch + hl * kDuoPWW;
-                const bool in0 = cs >= 0 && cs + 16 <= W, in1 = cs + 16 >= 0 && cs + 32 <= W;
-                cp_async16(dst, in0 ? src + cs : src, in0);
-                cp_async16(dst + 4, in1 ? src + cs + 16 : src, in1);
-            }
+            if (act && own && !(cc == 1 && b_early)) stage(cc, ccx, ccy);
         }
         const bool shape = act && boundary && (c < 3 || a.P.bt_shape);
         uint2 ca0 = make_uint2(0u, 0u), ca1 = ca0;
@@ -1872,6 +1888,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
         }
         cp_async_wait_all();
         __syncwarp();
+        unsigned long long t_patch = 0;
+        if (TRACE) t_patch = gtimer();
         // --- brs_select (estimators.cpp:257-301) ------------------------------
         uint32_t s;
         if (shape) {
@@ -1885,7 +1903,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             prow8(pr + 4 * kDuoPWW, 4 + po, w2, w3);
             s = vad4(cw[2 * q4 + 9], w3, vad4(cw[2 * q4 + 8], w2, vad4(cw[2 * q4 + 1], w1, vad4(cw[2 * q4], w0, 0u)))) * 4u;
         }
-        s += __shfl_xor_sync(FULL, s, 1);
+        s += __shfl_xor_sync(FULL, s, 1);  // the candidate's 4 lanes
         s += __shfl_xor_sync(FULL, s, 2);
         uint32_t best = __shfl_sync(FULL, s, hb);
         int win = 0;
@@ -1917,6 +1935,11 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
         int ci = 0, cj = 0;
         uint32_t dpd = 1, iters = 0;
         bool alive = act;
+        // earlier centres (relative to the start; at most 3 before the 4th
+        // iteration): a neighbour q is a fresh evaluation (:321-332) iff it is
+        // at Chebyshev distance >= 2 from every earlier centre (every position
+        // within distance 1 of one was evaluated then, the start included)
+        int pc0 = 0, pc1 = 0, pc2 = 0;  // packed (x + 8) | (y + 8) << 4
         for (int it = 0; it < a.P.max_iter; ++it) {
             alive = alive && ccost != 0;  // already a global minimum (:341)
             if (!__any_sync(FULL, alive)) break;
@@ -1934,15 +1957,14 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             part += __shfl_xor_sync(FULL, part, 1);
             const uint32_t cost = 4u * part;
             const bool lead = alive && adm && q2 == 0;
-            bool fresh = false;
-            if (lead) {  // unique aggregate evaluations (:321-332)
-                const int bit = (4 + py) * 9 + 4 + px;
-                const uint32_t m = 1u << (bit & 31);
-                fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
-            }
+            bool fresh = lead;
+            auto far = [&](int pc) { return max(abs(px + 8 - (pc & 15)), abs(py + 8 - (pc >> 4))) >= 2; };
+            if (it >= 1) fresh = fresh && far(pc0);
+            if (it >= 2) fresh = fresh && far(pc1);
+            if (it >= 3) fresh = fresh && far(pc2);
             dpd += __popc(__ballot_sync(FULL, fresh) & hmask);
-            uint32_t m = lead ? cost : kInf;
-#pragma unroll
+            uint32_t m = lead ? cost : kInf;  // min over the half (full-mask shuffles:
+#pragma unroll                                // half-mask reductions serialise the halves)
             for (int o = 1; o < 16; o <<= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
             const bool move = alive && m < ccost;  // else the centre is kept (:376)
             const uint32_t ties = (__ballot_sync(FULL, lead && cost == m) & hmask) >> hb;
@@ -1978,6 +2000,10 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
                     }
                 }
             }
+            const int pc = (ci + 8) | ((cj + 8) << 4);
+            if (it == 0) pc0 = pc;
+            if (it == 1) pc1 = pc;
+            if (it == 2) pc2 = pc;
             if (move) {
                 ci += c_off8[w][0];
                 cj += c_off8[w][1];
@@ -1999,6 +2025,13 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
+            if (TRACE) {  // {claimed, dependencies ready, patches staged, record published}
+                unsigned long long* tr = a.trace + size_t(item + hf) * 4;
+                tr[0] = t_claim;
+                tr[1] = t_ready;
+                tr[2] = gtimer();
+                tr[3] = t_patch;
+            }
         }
         __syncwarp();
     }
@@ -2493,7 +2526,9 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             kern = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         } else if (pa_mode == 2) {
             const int mb = minb ? atoi(minb) : 4;
-            if (threads == 128)
+            if (trace_path)
+                kern = pa_duo_kernel<256, 4, true>;
+            else if (threads == 128)
                 kern = mb == 8 ? pa_duo_kernel<128, 8> : mb == 6 ? pa_duo_kernel<128, 6> : pa_duo_kernel<128, 7>;
             else
                 kern = mb == 4 ? pa_duo_kernel<256, 4> : pa_duo_kernel<256, 3>;

@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-export ME_PA_KEY_A=1 ME_PA_KEY_S=0
-ME_PA_TRACE=gpurun_out/trace_cfg2.bin timeout 120 python bench.py --workload cfg2-pa --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>gpurun_out/t.log; echo rc=$?
+ME_PA_TRACE=gpurun_out/trace_cfg4.bin timeout 120 python bench.py --workload cfg4-pa --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>gpurun_out/t.log; echo rc=$?

@@ -1,19 +1,53 @@
-import numpy as np, sys
-for name in ("cfg2", "cfg4"):
-    try: raw = open(f"gpurun_out/trace_{name}.bin","rb").read()
-    except OSError: continue
-    n = len(raw) // 40
-    tr = np.frombuffer(raw[:n*32], np.uint64).reshape(n, 4).astype(np.int64)
-    lst = np.frombuffer(raw[n*32:], np.uint32).reshape(n, 2)
-    valid = tr[:,0] > 0
-    tr = tr[valid]; lst = lst[valid]
-    t0 = tr[:,0].min()
-    claim = (tr[:,0]-t0)/1e3; deps=(tr[:,1]-t0)/1e3; done=(tr[:,2]-t0)/1e3
-    h = lst[:,0] & 0xFFFF; v = (lst[:,0]>>16)&0x7FFF; p = lst[:,1]&0xFFFF
-    step = h + 2*v + p
-    print(name, "tasks", len(tr), "span us %.1f" % done.max())
-    print("  wait us: mean %.2f p50 %.2f p90 %.2f" % ((deps-claim).mean(), np.median(deps-claim), np.percentile(deps-claim,90)))
-    print("  work us: mean %.2f p50 %.2f p90 %.2f max %.2f" % ((done-deps).mean(), np.median(done-deps), np.percentile(done-deps,90), (done-deps).max()))
-    st = np.unique(step)
-    md = np.array([done[step==s].max() for s in st])
-    print("  per-step increments mean %.2f" % np.diff(md).mean())
+"""Analyse a PA wavefront trace (ME_PA_TRACE=file): per list entry
+{claim, deps ready, done, smid} (globaltimer ns) followed by the list.
+usage: trace_report.py TRACE.bin COLS ROWS PAIRS"""
+import sys
+
+import numpy as np
+
+raw = open(sys.argv[1], "rb").read()
+cols, rows, pairs = (int(x) for x in sys.argv[2:5])
+n = len(raw) // 40
+tr = np.frombuffer(raw[: n * 32], np.uint64).reshape(n, 4).astype(np.int64)
+lst = np.frombuffer(raw[n * 32:], np.uint32).reshape(n, 2)
+valid = tr[:, 0] > 0
+tr, lst = tr[valid], lst[valid]
+t0 = tr[:, 0].min()
+claim, ready, done = ((tr[:, i] - t0) / 1e3 for i in range(3))
+h = (lst[:, 0] & 0xFFFF).astype(np.int64)
+v = ((lst[:, 0] >> 16) & 0x7FFF).astype(np.int64)
+p = (lst[:, 1] & 0xFFFF).astype(np.int64)
+seq = (lst[:, 1] >> 16).astype(np.int64)
+nseq = seq.max() + 1
+step = h + 2 * v + p
+grid = np.full((nseq, pairs, rows, cols), -1e9)
+grid[seq, p, v, h] = done
+def dep(s, pp, vv, hh, ok):
+    out = np.full(len(s), -1e9)
+    out[ok] = grid[s[ok], pp[ok], vv[ok], hh[ok]]
+    return out
+dA = dep(seq, p, v, h - 1, h > 0)
+dB = dep(seq, p, v - 1, h, v > 0)
+dC = dep(seq, p, v - 1, h + 1, (v > 0) & (h + 1 < cols))
+dT = dep(seq, p - 1, v, h, p > 0)
+dmax = np.maximum.reduce([dA, dB, dC, dT])
+has = dmax > -1e8
+print("tasks", len(tr), "span us %.1f" % done.max(), "steps", step.max() + 1)
+patch = (tr[:, 3] - t0) / 1e3
+print("ready->patches staged us: mean %.2f p50 %.2f p90 %.2f" % ((patch - ready).mean(), *np.percentile(patch - ready, [50, 90])))
+print("patches->done us:         mean %.2f p50 %.2f p90 %.2f" % ((done - patch).mean(), *np.percentile(done - patch, [50, 90])))
+print("work (ready->done) us: mean %.2f p50 %.2f p90 %.2f p99 %.2f" % ((done - ready).mean(), *np.percentile(done - ready, [50, 90, 99])))
+print("claim->ready us:       mean %.2f p50 %.2f p90 %.2f" % ((ready - claim).mean(), *np.percentile(ready - claim, [50, 90])))
+late = ready[has] - dmax[has]
+print("detect (ready - last dep done) us: mean %.2f p50 %.2f p90 %.2f" % (late.mean(), *np.percentile(late, [50, 90])))
+slack = claim[has] - dmax[has]
+print("claim - last dep done us: mean %.2f p50 %.2f (negative = claimed before its deps finished: %.0f%%)" % (slack.mean(), np.median(slack), 100 * (slack < 0).mean()))
+st = np.unique(step)
+md = np.array([done[step == s].max() for s in st])
+mc = np.array([claim[step == s].min() for s in st])
+print("per-step: last-done increments mean %.2f us; first-claim increments mean %.2f us" % (np.diff(md).mean(), np.diff(mc).mean()))
+cnt = np.array([(step == s).sum() for s in st])
+print("items per step: min %d mean %.0f max %d" % (cnt.min(), cnt.mean(), cnt.max()))
+for q in (10, 50, 90):
+    i = int(len(st) * q / 100)
+    print("  step %d: items %d, claim %.1f..%.1f us, done max %.1f us" % (st[i], cnt[i], claim[step == st[i]].min(), claim[step == st[i]].max(), md[i]))
