@@ -2309,12 +2309,21 @@ __global__ void sse_kernel(const uint8_t* x, const uint8_t* y, int n, unsigned l
 
 namespace {
 
-constexpr int kEsBandRows = 64;  // dy rows of candidates staged per band (multiple of K=8)
+// dy rows of candidates staged per band (a multiple of K = 8): the whole
+// window when its 4 shifted copies fit in ~110 KB (one staging pass and one
+// flat task list per block, no partial band), else bands of 64 rows
+int es_band_rows(int bs, int S, int W, int H) {
+    const int WX = min(2 * S + 1, W - bs + 1), WY = min(2 * S + 1, H - bs + 1);
+    const int PW = ((WX - 1) >> 2) + (bs >> 2) + 1;
+    int rows = (WY + 7) / 8 * 8;
+    while (rows > 64 && size_t(4) * (size_t(rows + bs - 1) * PW + 32) * 4 > 110 * 1024) rows -= 8;
+    return rows;
+}
 
-size_t es_smem_bytes(int bs, int S, int W) {
+size_t es_smem_bytes(int bs, int S, int W, int H) {
     const int WX = min(2 * S + 1, W - bs + 1);
     const int PW = ((WX - 1) >> 2) + (bs >> 2) + 1;
-    const int srows = kEsBandRows + bs - 1;
+    const int srows = es_band_rows(bs, S, W, H) + bs - 1;
     return size_t(4) * (size_t(srows) * PW + 32) * 4;
 }
 
@@ -2476,9 +2485,9 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         ea.nlist = nlist;
         ea.counter = s.counter;
         ea.recs = recs;
-        ea.band_rows_max = kEsBandRows;
+        ea.band_rows_max = es_band_rows(b.bs, cfg.search_range, b.W, b.H);
         ea.stats = stats;
-        const size_t smem = es_smem_bytes(b.bs, cfg.search_range, b.W);
+        const size_t smem = es_smem_bytes(b.bs, cfg.search_range, b.W, b.H);
         if (b.bs == 16) {
             if ((e = cudaFuncSetAttribute(es_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
             int occ = 0;
@@ -2598,14 +2607,14 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
 cudaError_t block_search(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H, int x0,
                          int y0, int size, int range, int64_t* out, cudaStream_t st) {
     if (algo == ME_ALGO_ES) {
-        const size_t smem = es_smem_bytes(size, range, W);
+        const size_t smem = es_smem_bytes(size, range, W, H);
         cudaError_t e;
         if (size == 16) {
             if ((e = cudaFuncSetAttribute(es_single_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
-            es_single_kernel<16><<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, kEsBandRows, out);
+            es_single_kernel<16><<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, es_band_rows(size, range, W, H), out);
         } else {
             if ((e = cudaFuncSetAttribute(es_single_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
-            es_single_kernel<8><<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, kEsBandRows, out);
+            es_single_kernel<8><<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, es_band_rows(size, range, W, H), out);
         }
         return cudaGetLastError();
     }
