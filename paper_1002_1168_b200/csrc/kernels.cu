@@ -610,23 +610,39 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         const int rows_valid = min(srows, WY + BS - 1 - run0 * K);
         const uint8_t* rb = ref + size_t(row_g0) * W + (x0 + lo_x);
         __syncthreads();  // previous band / block done with smem
-        for (int idx = tid; idx < srows * PW; idx += blockDim.x) {
-            const int row = idx / PW, q = idx - row * PW;
-            uint32_t bytes[7];
+        // staging from aligned words: copy s, word q = bytes [4q + s, 4q + s + 4)
+        // of the row segment = a funnel shift of two aligned words.  Bytes past
+        // the segment are never paired with the current block (only rows and
+        // columns of admissible positions are summed), so the loads clamp to
+        // the segment's last aligned word and rows past the window are skipped.
+        for (int row = tid / PW, q = tid - (tid / PW) * PW; row < srows;) {
+            if (row < rows_valid) {
+                const uint8_t* seg = rb + size_t(row) * W;
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(seg) & ~uintptr_t(3);
+                const uint32_t off = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3);
+                const uintptr_t last = (reinterpret_cast<uintptr_t>(seg) + rowbytes - 1) & ~uintptr_t(3);
+                uint32_t g[3];
 #pragma unroll
-            for (int k = 0; k < 7; ++k) {
-                const int col = 4 * q + k;
-                bytes[k] = (row < rows_valid && col < rowbytes) ? rb[size_t(row) * W + col] : 0u;
+                for (int m = 0; m < 3; ++m) {
+                    const uintptr_t ad = min(a0 + 4 * uintptr_t(q + m), last);
+                    g[m] = __ldg(reinterpret_cast<const uint32_t*>(ad));
+                }
+#pragma unroll
+                for (int sft = 0; sft < 4; ++sft) {
+                    const uint32_t t = off + sft;  // 0..6
+                    const uint32_t lo = t < 4 ? g[0] : g[1], hi = t < 4 ? g[1] : g[2];
+                    sm[sft * CW + row * PW + q] = __funnelshift_r(lo, hi, (t & 3) * 8);
+                }
             }
-#pragma unroll
-            for (int s = 0; s < 4; ++s)
-                sm[s * CW + idx] = bytes[s] | (bytes[s + 1] << 8) | (bytes[s + 2] << 16) |
-                                   (bytes[s + 3] << 24);
+            q += blockDim.x;
+            while (q >= PW) {
+                q -= PW;
+                ++row;
+            }
         }
         __syncthreads();
-        const int ntask = WX * bruns;
-        for (int task = tid; task < ntask; task += blockDim.x) {
-            const int run = task / WX, col = task - run * WX;
+        // tasks (run, col) in raster order, walked incrementally (no division)
+        for (int run = tid / WX, col = tid - (tid / WX) * WX; run < bruns;) {
             const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
             uint32_t acc[K];
 #pragma unroll
@@ -645,19 +661,30 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
                     }
                 }
             }
+            // min over the run's K positions of (SAD, |dx|+|dy|, k) in 32 bits
+            // (SAD < 2^16, |dx|+|dy| <= 128, k < 8), then one 64-bit key
             const int dx = lo_x + col;
             const int ady = (run0 + run) * K;
+            const int adx = abs(dx);
+            uint32_t m32 = ~0u;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const int wy = ady + k;  // window row index
-                if (wy < WY) {
-                    const int dy = lo_y + wy;
-                    const unsigned long long key =
-                        (static_cast<unsigned long long>(acc[k]) << 40) |
-                        (static_cast<unsigned long long>(abs(dx) + abs(dy)) << 24) |
-                        static_cast<unsigned long long>(wy * WX + col);
-                    best = key < best ? key : best;
-                }
+                const uint32_t man = uint32_t(adx + abs(lo_y + wy));
+                const uint32_t kk = (acc[k] << 11) | (man << 3) | uint32_t(k);
+                m32 = wy < WY ? min(m32, kk) : m32;
+            }
+            if (m32 != ~0u) {
+                const uint32_t wy = uint32_t(ady) + (m32 & 7u);
+                const unsigned long long key = (static_cast<unsigned long long>(m32 >> 11) << 40) |
+                                               (static_cast<unsigned long long>((m32 >> 3) & 0xFFu) << 24) |
+                                               static_cast<unsigned long long>(wy * uint32_t(WX) + uint32_t(col));
+                best = key < best ? key : best;
+            }
+            col += blockDim.x;
+            while (col >= WX) {
+                col -= WX;
+                ++run;
             }
         }
     }
