@@ -415,7 +415,9 @@ def main():
             e2e_s = float(tt.item())
         if not np.array_equal(hrecs.numpy()[0].view(_lib.rec_dtype()).reshape(pairs, rows, cols), hrec):
             raise SystemExit("e2e records differ from the device-resident run")
-        e2e = {"value": total_units / e2e_s, "unit": "MB/s", "h2d_bytes_per_step": int(2 * n_seq * F * W * H), "d2h_bytes_per_step": int(n_seq * pairs * (rows * cols * 16 + 48)), "steps": n_e2e, "s_per_step": e2e_s}
+        h2d, d2h = B.last_transfer_bytes(local)  # counted by the library: alpha masks cross bit-packed
+        e2e = {"value": total_units / e2e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e, "s_per_step": e2e_s,
+               "input_bytes_per_step": int(2 * n_seq * F * W * H), "note": "pinned host buffers; luma as bytes, binary alpha bit-packed on the host cores and expanded on the GPU"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -120,6 +120,10 @@ enum { ME_STAGE_CLASSIFY = 0, ME_STAGE_SORT = 1, ME_STAGE_SEARCH = 2, ME_STAGE_M
 me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable);
 me_status me_b200_ctx_stage_ms(me_ctx* ctx, float* out, int n);
 
+/* Bytes the last me_b200_run_sequences call moved host->device and
+ * device->host (binary alpha masks cross PCIe bit-packed: W*H/8 per frame). */
+me_status me_b200_ctx_transfer_bytes(me_ctx* ctx, int64_t* h2d, int64_t* d2h);
+
 /* SearchConfig::validate + PrsConfig::validate (estimators.cpp:139-150). */
 me_status me_b200_validate_config(const me_config* cfg);
 

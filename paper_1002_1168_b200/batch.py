@@ -101,3 +101,11 @@ def run_sequences_ptr(cfg: BatchConfig, n_seq: int, F: int, W: int, H: int, luma
     """Raw host-pointer form (e.g. pinned torch tensors) for end-to-end timing."""
     c = cfg.c()
     check(lib().me_b200_run_sequences(ctx(device), C.byref(c), n_seq, F, W, H, C.c_void_p(luma_ptr), C.c_void_p(alpha_ptr) if alpha_ptr else None, C.c_void_p(recs_ptr), C.c_void_p(stats_ptr), None))
+
+
+def last_transfer_bytes(device: int = 0):
+    """(host->device, device->host) bytes of the last run_sequences call on this
+    thread's context; binary alpha masks cross PCIe bit-packed."""
+    h, d = C.c_int64(), C.c_int64()
+    check(lib().me_b200_ctx_transfer_bytes(ctx(device), C.byref(h), C.byref(d)))
+    return h.value, d.value

@@ -81,7 +81,7 @@ me_status upload(me_ctx* ctx, DevBuf& buf, size_t off, const void* host, size_t 
 
 size_t pad16(size_t n) { return (n + 15) & ~size_t(15); }
 
-constexpr int kPipelineChunks = 8;
+constexpr int kPipelineChunks = 32;  // upper bound (events); default chunk count below
 
 // Lazily creates the copy / d2h streams and the chunk events of the
 // host-pointer pipeline.
@@ -93,7 +93,26 @@ me_status ensure_pipeline(me_ctx* ctx) {
         ME_CUDA(cudaEventCreateWithFlags(&ctx->ev_in[k], cudaEventDisableTiming));
         ME_CUDA(cudaEventCreateWithFlags(&ctx->ev_out[k], cudaEventDisableTiming));
     }
+    for (int k = 0; k < 2; ++k) ME_CUDA(cudaEventCreateWithFlags(&ctx->ev_pack[k], cudaEventDisableTiming));
     return ME_OK;
+}
+
+// Packs a binary mask to 1 bit per pixel (bit i of byte j = pixel 8j + i) on
+// all host cores.  Returns false when some byte is neither 0 nor 255: such a
+// mask is not binary and is shipped as bytes (the shape SAD compares byte
+// values, so packing would not be exact).
+bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst) {
+    const int64_t nw = int64_t(n / 8);
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t i = 0; i < nw; ++i) {
+        uint64_t x;
+        std::memcpy(&x, src + 8 * i, 8);
+        const uint64_t hi = (x >> 7) & 0x0101010101010101ull;  // bit 0 of each byte = its bit 7
+        bad |= int(x != hi * 0xFFu);
+        dst[i] = uint8_t((hi * 0x0102040810204080ull) >> 56);
+    }
+    return !bad;
 }
 
 me_status sync(me_ctx* ctx) {
@@ -173,6 +192,7 @@ void me_b200_ctx_destroy(me_ctx* c) {
         cudaStreamSynchronize(c->d2h_stream);
         for (auto& e : c->ev_in) cudaEventDestroy(e);
         for (auto& e : c->ev_out) cudaEventDestroy(e);
+        for (auto& e : c->ev_pack) cudaEventDestroy(e);
         cudaStreamDestroy(c->copy_stream);
         cudaStreamDestroy(c->d2h_stream);
     }
@@ -181,6 +201,10 @@ void me_b200_ctx_destroy(me_ctx* c) {
         b->release();
     c->pin_a.release();
     c->pin_b.release();
+    for (int i = 0; i < 2; ++i) {
+        c->pack_host[i].release();
+        c->pack_dev[i].release();
+    }
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -194,6 +218,14 @@ me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable) {
         for (auto& e : ctx->ev) ME_CUDA(cudaEventCreate(&e));
     ctx->profiling = enable != 0;
     ctx->ev_valid = false;
+    return ok();
+}
+
+me_status me_b200_ctx_transfer_bytes(me_ctx* ctx, int64_t* h2d, int64_t* d2h) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (h2d) *h2d = ctx->h2d_bytes;
+    if (d2h) *d2h = ctx->d2h_bytes;
     return ok();
 }
 
@@ -293,22 +325,52 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     // Chunked pipeline: the sequences are independent, so chunk k's H2D (copy
     // stream) overlaps chunk k-1's estimation (compute stream) and chunk
     // k-2's D2H (d2h stream).  PCIe is the bound of this path.
-    const int nchunks = std::min(n_seq, kPipelineChunks);
+    const char* nc = getenv("ME_B200_CHUNKS");
+    const int nchunks = std::min(n_seq, std::max(1, std::min(kPipelineChunks, nc ? atoi(nc) : 16)));
     uint8_t* dl = static_cast<uint8_t*>(ctx->in_luma.p);
     uint8_t* da = static_cast<uint8_t*>(ctx->in_alpha.p);
     me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
     me_pair_stats* ds = static_cast<me_pair_stats*>(ctx->out_stats.p);
     uint8_t* dp = static_cast<uint8_t*>(ctx->out_pred.p);
-    for (int k = 0; k < nchunks; ++k) {
-        const int s0 = int(int64_t(n_seq) * k / nchunks), s1 = int(int64_t(n_seq) * (k + 1) / nchunks);
-        const size_t o = seq_bytes * s0, n = seq_bytes * (s1 - s0);
-        ME_CUDA(cudaMemcpyAsync(dl + o, luma + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
-        if (alpha) ME_CUDA(cudaMemcpyAsync(da + o, alpha + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
-        ME_CUDA(cudaEventRecord(ctx->ev_in[k], ctx->copy_stream));
-    }
+    // Binary alpha masks cross PCIe bit-packed (packed on the host cores while
+    // the previous chunk's copies are in flight, expanded on the device).
+    const bool pack = alpha && !getenv("ME_B200_NO_MASK_PACK");
+    const size_t max_chunk = seq_bytes * size_t((n_seq + nchunks - 1) / nchunks);
+    if (pack)
+        for (int i = 0; i < 2; ++i) {
+            ME_CUDA(ctx->pack_host[i].reserve(max_chunk / 8 + 64));
+            ME_CUDA(ctx->pack_dev[i].reserve(max_chunk / 8 + 64));
+        }
+    ctx->h2d_bytes = ctx->d2h_bytes = 0;
     for (int k = 0; k < nchunks; ++k) {
         const int s0 = int(int64_t(n_seq) * k / nchunks), s1 = int(int64_t(n_seq) * (k + 1) / nchunks);
         const int ns = s1 - s0;
+        const size_t o = seq_bytes * s0, n = seq_bytes * ns;
+        ME_CUDA(cudaMemcpyAsync(dl + o, luma + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
+        ctx->h2d_bytes += int64_t(n);
+        if (alpha) {
+            const int slot = k & 1;
+            bool packed = false;
+            if (pack) {
+                // the copy out of this staging slot (chunk k - 2) must be done
+                if (k >= 2) ME_CUDA(cudaEventSynchronize(ctx->ev_pack[slot]));
+                uint8_t* hb = static_cast<uint8_t*>(ctx->pack_host[slot].p);
+                packed = pack_binary_mask(alpha + o, n, hb);
+                if (packed) {
+                    uint8_t* db = static_cast<uint8_t*>(ctx->pack_dev[slot].p);
+                    ME_CUDA(cudaMemcpyAsync(db, hb, n / 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+                    ctx->h2d_bytes += int64_t(n / 8);
+                    ME_CUDA(cudaEventRecord(ctx->ev_pack[slot], ctx->copy_stream));
+                    ME_CUDA(mek::unpack_mask(db, da + o, n, ctx->copy_stream));
+                }
+            }
+            if (!packed) {
+                ME_CUDA(cudaMemcpyAsync(da + o, alpha + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
+                ctx->h2d_bytes += int64_t(n);
+            }
+        }
+        ME_CUDA(cudaEventRecord(ctx->ev_in[k], ctx->copy_stream));
+        // estimation of chunk k (compute stream) and its D2H (d2h stream)
         ME_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[k], 0));
         const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, dl + seq_bytes * s0,
                                         alpha ? da + seq_bytes * s0 : nullptr);
@@ -326,6 +388,8 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
         if (pred)
             ME_CUDA(cudaMemcpyAsync(pred + plane * pairs * s0, dp + plane * pairs * s0, plane * pairs * ns,
                                     cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        ctx->d2h_bytes += int64_t(seq_recs * ns * sizeof(me_block_rec) + size_t(pairs) * ns * sizeof(me_pair_stats) +
+                                  (pred ? plane * pairs * ns : 0));
     }
     ctx->ev_valid = false;
     ME_CUDA(cudaStreamSynchronize(ctx->d2h_stream));

@@ -2065,6 +2065,26 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// unpack_kernel: the host path ships binary alpha masks bit-packed (1/8 of the
+// PCIe bytes) and expands them here: one thread per 4 packed bytes -> 32 pixels.
+// ---------------------------------------------------------------------------
+__global__ void unpack_kernel(const uint32_t* __restrict__ bits, uint4* __restrict__ out, size_t nwords) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = __ldg(bits + i);
+        uint4 v[2];
+        uint32_t* o = reinterpret_cast<uint32_t*>(v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // 4 pixels per output word: bits 4q .. 4q+3
+            const uint32_t nib = (w >> (4 * q)) & 0xFu;
+            o[q] = ((nib & 1u) ? 0xFFu : 0u) | ((nib & 2u) ? 0xFF00u : 0u) | ((nib & 4u) ? 0xFF0000u : 0u) |
+                   ((nib & 8u) ? 0xFF000000u : 0u);
+        }
+        out[2 * i] = v[0];
+        out[2 * i + 1] = v[1];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // mc_kernel: predict_frame (compensation.cpp:30-71) fused with the psnr SSE
 // (metrics.cpp:108-124) and the per-pair SearchStats reduction.  One thread
 // per 8-pixel row segment; the prediction is only stored when requested.
@@ -2730,6 +2750,17 @@ cudaError_t classify_frame(const uint8_t* alpha, int W, int H, int bs, uint8_t* 
                            cudaStream_t st) {
     const int n = (W / bs) * (H / bs);
     classify_frame_kernel<<<(n + 255) / 256, 256, 0, st>>>(alpha, W, H, bs, types);
+    return cudaGetLastError();
+}
+
+cudaError_t unpack_mask(const uint8_t* bits, uint8_t* out, size_t n, cudaStream_t st) {
+    // n / 32 full words; a tail of 8..24 pixels is expanded from a padded word
+    const size_t nw = n / 32;
+    if (nw) {
+        const int grid = int(std::min<size_t>((nw + 255) / 256, 148 * 16));
+        unpack_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(bits), reinterpret_cast<uint4*>(out), nw);
+    }
+    if (n % 32) return cudaErrorInvalidValue;  // callers pass whole 32-pixel groups
     return cudaGetLastError();
 }
 

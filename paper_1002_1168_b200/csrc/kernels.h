@@ -53,6 +53,9 @@ cudaError_t sad_shape_single(const uint8_t* ca, const uint8_t* ra, int W, int H,
 cudaError_t classify_frame(const uint8_t* alpha, int W, int H, int bs, uint8_t* types,
                            cudaStream_t st);
 cudaError_t binarize(const uint8_t* gray, int n, int threshold, uint8_t* out, cudaStream_t st);
+// Expands a bit-packed binary mask (bit i of byte j = pixel 8j + i) to bytes
+// 0 / 255; n (pixels) is a multiple of 8.
+cudaError_t unpack_mask(const uint8_t* bits, uint8_t* out, size_t n, cudaStream_t st);
 cudaError_t predict(const uint8_t* ref, const uint8_t* cur, const int32_t* mv, const uint8_t* types,
                     int W, int H, int bs, uint8_t* pred, me_pair_stats* stats,
                     cudaStream_t st);

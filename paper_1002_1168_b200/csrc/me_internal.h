@@ -76,7 +76,12 @@ struct me_ctx {
     cudaEvent_t* events() { return profiling ? ev : nullptr; }
     // host-pointer pipeline: H2D / D2H streams and per-chunk events
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
-    cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
+    cudaEvent_t ev_in[32] = {}, ev_out[32] = {};
+    // bit-packed alpha staging (binary masks cross PCIe at 1 bit per pixel)
+    HostBuf pack_host[2];
+    DevBuf pack_dev[2];
+    cudaEvent_t ev_pack[2] = {};
+    int64_t h2d_bytes = 0, d2h_bytes = 0;  // of the last host-pointer batch
 };
 
 #endif

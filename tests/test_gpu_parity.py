@@ -209,3 +209,21 @@ def test_estimate_field_prev(me_gpu, port):
     flat = np.full((64, 64), 99, np.uint8)
     f2, _ = me_gpu.estimate_field(me_gpu.Algo.PA, flat, flat, None, None, pf, me_gpu.SearchConfig(block_size=8), me_gpu.PrsConfig())
     assert f2.at(0, 0) == (0, 0)
+
+
+@pytest.mark.parametrize("levels", [(0, 255), (0, 100, 255)])
+def test_host_path_mask_packing(me_gpu, port, levels):
+    """The host-pointer path ships binary masks bit-packed (expanded on the
+    device); a mask with other values must go as bytes — both bit-exact."""
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config4_batch(9, 900, frames=5)
+    if len(levels) == 3:  # make some object pixels a different nonzero value
+        alpha = alpha.copy()
+        alpha[:, :, ::3, ::5] = np.where(alpha[:, :, ::3, ::5] > 0, 100, 0)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in (0, 4, 8):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"seq {i}")
+        assert np.array_equal(stats[i], want_s)
