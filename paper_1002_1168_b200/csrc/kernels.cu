@@ -1871,7 +1871,11 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
                 if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
             }
         }
-        if (TRACE) t_ready = gtimer();
+        long long c_ready = 0;
+        if (TRACE) {
+            t_ready = gtimer();
+            c_ready = clock64();
+        }
         if (hl < 8) {
             cw[2 * hl] = crow.x;
             cw[2 * hl + 1] = crow.y;
@@ -1915,8 +1919,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
         }
         cp_async_wait_all();
         __syncwarp();
-        unsigned long long t_patch = 0;
-        if (TRACE) t_patch = gtimer();
+        long long c_patch = 0;
+        if (TRACE) c_patch = clock64();
         // --- brs_select (estimators.cpp:257-301) ------------------------------
         uint32_t s;
         if (shape) {
@@ -1958,6 +1962,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             t = __shfl_sync(FULL, t, hb);
             if (win_shape) ccost = 4u * t;
         }
+        long long c_brs = 0;
+        if (TRACE) c_brs = clock64();
         // --- prs_refine (estimators.cpp:311-382), lazily from the patch -------
         int ci = 0, cj = 0;
         uint32_t dpd = 1, iters = 0;
@@ -1990,9 +1996,12 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             if (it >= 2) fresh = fresh && far(pc1);
             if (it >= 3) fresh = fresh && far(pc2);
             dpd += __popc(__ballot_sync(FULL, fresh) & hmask);
-            uint32_t m = lead ? cost : kInf;  // min over the half (full-mask shuffles:
-#pragma unroll                                // half-mask reductions serialise the halves)
-            for (int o = 1; o < 16; o <<= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+            // per-half minimum: two independent full-warp reductions (a
+            // half-mask reduction would serialise the halves)
+            const uint32_t mine_c = lead ? cost : kInf;
+            const uint32_t m0 = __reduce_min_sync(FULL, hf ? kInf : mine_c);
+            const uint32_t m1 = __reduce_min_sync(FULL, hf ? mine_c : kInf);
+            const uint32_t m = hf ? m1 : m0;
             const bool move = alive && m < ccost;  // else the centre is kept (:376)
             const uint32_t ties = (__ballot_sync(FULL, lead && cost == m) & hmask) >> hb;
             int w = (__ffs(ties) - 1) >> 1;
@@ -2039,6 +2048,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             }
             alive = move;
         }
+        long long c_walk = 0;
+        if (TRACE) c_walk = clock64();
         // --- fused predict_frame + psnr SSE at the final vector ---------------
         uint32_t se = 0;
         if (hl < 8) {
@@ -2046,18 +2057,23 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             prow8(pw + (4 + cj + hl) * kDuoPWW, 4 + ci + wo, w0, w1);
             se = sq4(cw[2 * hl + 1], w1, sq4(cw[2 * hl], w0, 0u));
         }
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) se += __shfl_xor_sync(FULL, se, o);
+        {
+            const uint32_t s0 = __reduce_add_sync(FULL, hf ? 0u : se), s1 = __reduce_add_sync(FULL, hf ? se : 0u);
+            se = hf ? s1 : s0;
+        }
         if (act && hl == 0) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
-            if (TRACE) {  // {claimed, dependencies ready, patches staged, record published}
+            if (TRACE) {  // {claimed, dependencies ready, published (globaltimer ns), phase cycles}
                 unsigned long long* tr = a.trace + size_t(item + hf) * 4;
                 tr[0] = t_claim;
                 tr[1] = t_ready;
+                const long long c_end = clock64();
+                tr[1] = (unsigned long long)(c_patch - c_ready) | ((unsigned long long)(c_brs - c_patch) << 32);
                 tr[2] = gtimer();
-                tr[3] = t_patch;
+                // SM cycles: patches staged -> BRS done (tr[1] high), -> walk done, -> published
+                tr[3] = (unsigned long long)(c_walk - c_brs) | ((unsigned long long)(c_end - c_walk) << 32);
             }
         }
         __syncwarp();
