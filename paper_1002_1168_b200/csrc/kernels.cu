@@ -456,6 +456,10 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
 // warp that claims `pad` aligned entries never straddles two bins.
 constexpr uint32_t kInvalidEntry = 0xFFFFFFFFu;
 
+// one 128-byte line per bin cursor: the fill's per-(CTA, bin) atomics would
+// otherwise queue on a handful of L2 lines
+constexpr int kCursorStride = 32;
+
 __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
                             uint2* list) {
     __shared__ int s_part[1024];
@@ -480,7 +484,7 @@ __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int*
     int acc = s_part[threadIdx.x];
     for (int i = lo; i < hi; ++i) {
         offs[i] = acc;
-        cursor[i] = acc;
+        cursor[i * kCursorStride] = acc;
         for (int k = hist[i]; k < padded(hist[i]); ++k) list[acc + k] = make_uint2(kInvalidEntry, kInvalidEntry);
         acc += padded(hist[i]);
     }
@@ -488,49 +492,49 @@ __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int*
 
 // Scatter estimated block ids into key order (per-CTA ranges per bin keep the
 // global atomics to one per (CTA, bin)).
-__device__ __forceinline__ void split_block(const Batch& b, int64_t g, int& h, int& v, int& p,
-                                            int& seq) {
-    h = int(g % b.cols);
-    int64_t t = g / b.cols;
-    v = int(t % b.rows);
-    t /= b.rows;
-    p = int(t % b.pairs);
-    seq = int(t / b.pairs);
-}
 
 // Scatter estimated blocks into key order as decoded list entries
 // {h | v << 16 | boundary << 31, p | seq << 16} (per-CTA ranges per bin keep
 // the global atomics to one per (CTA, bin)).
-__global__ void fill_kernel(ClassArgs a, int* cursor, uint2* list) {
+// One CTA per rows_per_cta block rows (32-bit index math): count into a shared
+// histogram, reserve each bin's range with one global atomic per (CTA, bin),
+// then scatter.
+
+__global__ void __launch_bounds__(256) fill_kernel(ClassArgs a, int* cursor, uint2* list, uint32_t rows_per_cta) {
     extern __shared__ int s_cnt[];  // [nbins] counts, then [nbins] bases
     int* s_base = s_cnt + a.nbins;
     const Batch& b = a.b;
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_cnt[i] = 0;
     __syncthreads();
-    const int64_t n = b.nblocks();
-    const int64_t chunk = int64_t(blockDim.x) * 8;
-    const int64_t g0 = int64_t(blockIdx.x) * chunk;
-    for (int64_t g = g0 + threadIdx.x; g < min(g0 + chunk, n); g += blockDim.x) {
-        if (a.types[g] == ME_TRANSPARENT) continue;
-        int h, v, p, seq;
-        split_block(b, g, h, v, p, seq);
-        atomicAdd(&s_cnt[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
-        s_base[i] = s_cnt[i] ? atomicAdd(&cursor[i], s_cnt[i]) : 0;
-        s_cnt[i] = 0;
-    }
-    __syncthreads();
-    for (int64_t g = g0 + threadIdx.x; g < min(g0 + chunk, n); g += blockDim.x) {
-        const int ty = a.types[g];
-        if (ty == ME_TRANSPARENT) continue;
-        int h, v, p, seq;
-        split_block(b, g, h, v, p, seq);
-        const int key = a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0;
-        const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
-        list[pos] = make_uint2(uint32_t(h) | (uint32_t(v) << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u),
-                               uint32_t(p) | (uint32_t(seq) << 16));
+    const uint32_t nrows = uint32_t(b.n_seq) * uint32_t(b.pairs) * uint32_t(b.rows);
+    const uint32_t r0 = blockIdx.x * rows_per_cta, r1 = min(r0 + rows_per_cta, nrows);
+    const uint32_t cols = uint32_t(b.cols), items = (r1 - r0) * cols;
+    const uint8_t* types = a.types + size_t(r0) * cols;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (uint32_t i = threadIdx.x; i < items; i += blockDim.x) {
+            const int ty = types[i];
+            if (ty == ME_TRANSPARENT) continue;
+            const uint32_t r = r0 + i / cols, h = i - (i / cols) * cols;
+            const uint32_t pr = r / uint32_t(b.rows), v = r - pr * uint32_t(b.rows);
+            const uint32_t seq = pr / uint32_t(b.pairs), p = pr - seq * uint32_t(b.pairs);
+            {
+                const int key = a.pa ? a.key_a * int(h + 2 * v + p) + a.key_s * int(seq) : 0;
+                if (pass == 0) {
+                    atomicAdd(&s_cnt[key], 1);
+                } else {
+                    const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
+                    list[pos] = make_uint2(uint32_t(h) | (v << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u), p | (seq << 16));
+                }
+            }
+        }
+        __syncthreads();
+        if (pass == 0) {
+            for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
+                s_base[i] = s_cnt[i] ? atomicAdd(&cursor[i * kCursorStride], s_cnt[i]) : 0;
+                s_cnt[i] = 0;
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -2434,7 +2438,7 @@ Scratch carve(const Batch& b, int nbins, void* base) {
     s.offs = reinterpret_cast<int*>(p);
     p += align_up(size_t(nbins + 1) * 4);
     s.cursor = reinterpret_cast<int*>(p);
-    p += align_up(size_t(nbins) * 4);
+    p += align_up(size_t(nbins) * 4 * kCursorStride);
     s.counter = reinterpret_cast<int*>(p);
     return s;
 }
@@ -2466,7 +2470,7 @@ size_t scratch_bytes(const Batch& b, int algo) {
     const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
     const size_t nb = size_t(b.nblocks());
     return align_up(nb) + align_up((nb + size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
-           align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4) + 256;
+           align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4 * kCursorStride) + 256;
 }
 
 // 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel
@@ -2531,10 +2535,14 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, pa_mode == 2 ? 2 : 1, s.offs, s.cursor, s.list);
     if ((e = cudaGetLastError())) return e;
     {
-        const int threads = 256;
-        const int64_t chunk = threads * 8;
-        const int grid = int((nb + chunk - 1) / chunk);
-        fill_kernel<<<grid, threads, 2 * hist_smem, st>>>(ca, s.cursor, s.list);
+        // <= 128 rows per CTA (fewer global atomics), >= 2 CTAs per SM
+        const int64_t nrows = int64_t(b.n_seq) * b.pairs * b.rows;
+        const int64_t rpc = std::max<int64_t>(4, std::min<int64_t>(128, nrows / (2 * num_sms)));
+        const int grid = int((nrows + rpc - 1) / rpc);
+        if (2 * hist_smem > 48 * 1024 &&
+            (e = cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * hist_smem))))
+            return e;
+        fill_kernel<<<grid, 256, 2 * hist_smem, st>>>(ca, s.cursor, s.list, uint32_t(rpc));
         if ((e = cudaGetLastError())) return e;
     }
     const int* nlist = s.offs + nbins;
