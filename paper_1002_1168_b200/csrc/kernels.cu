@@ -1541,6 +1541,12 @@ constexpr int kFastPWW = 12;       // patch row stride in words (8 used: two 16-
 constexpr int kFastPatch = kFastPR * kFastPWW;
 constexpr int kFastWarpWords = 4 * kFastPatch + 16 + 4;  // patches, current block, visited
 
+// kOff8 (estimators.cpp:33-35) arithmetically: offset k in raster order of
+// (dy, dx) with the centre skipped.  Lane-dependent indices into c_off8 would
+// serialise the constant cache.
+__device__ __forceinline__ int off8x(int k) { const int i = k + (k >= 4); return i - 3 * (i / 3) - 1; }
+__device__ __forceinline__ int off8y(int k) { const int i = k + (k >= 4); return i / 3 - 1; }
+
 // 2 words of a staged patch row: bytes [t, t + 8) of the row's 32 raw bytes.
 __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, uint32_t& r1) {
     const int q = t >> 2;
@@ -1564,7 +1570,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
     const int c = lane >> 3, sub = lane & 7;
     const int k = lane >> 2, q = lane & 3;   // PRS: neighbour k, rows q and q + 4
-    const int kx = c_off8[k][0], ky = c_off8[k][1];
+    const int kx = off8x(k), ky = off8y(k);
     // static round-robin over the wavefront-sorted list (see pa_kernel)
     // Items are taken in list (wavefront) order, statically round robin or
     // dynamically from a counter; either way the least unfinished item's
@@ -1757,8 +1763,8 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                     }
                 }
             }
-            ci += c_off8[w][0];
-            cj += c_off8[w][1];
+            ci += off8x(w);
+            cj += off8y(w);
             ccost = m;
             ++iters;
         }
@@ -1821,7 +1827,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     const uint32_t plane = uint32_t(W) * uint32_t(H);
     const int c = hl >> 2, q4 = hl & 3;  // BRS: candidate c, block rows q4 and q4 + 4
     const int k = hl >> 1, q2 = hl & 1;  // PRS: neighbour k, block rows q2 + {0, 2, 4, 6}
-    const int kx = c_off8[k][0], ky = c_off8[k][1];
+    const int kx = off8x(k), ky = off8y(k);
     for (int item = 2 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 2 * nwarps) {
         const uint2 e = __ldg(a.list + item + hf);
         const bool act = e.x != kInvalidEntry;  // uniform per half
@@ -2045,8 +2051,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             if (it == 1) pc1 = pc;
             if (it == 2) pc2 = pc;
             if (move) {
-                ci += c_off8[w][0];
-                cj += c_off8[w][1];
+                ci += off8x(w);
+                cj += off8y(w);
                 ccost = m;
                 ++iters;
             }
