@@ -240,3 +240,16 @@ class Oracle:
         cmp = C.c_int64()
         self._chk(self._f("time_blocks")(C.byref(cfg), W, H, _vp(cur), _vp(ref), _vp(xy), n, threads, C.byref(cmp)))
         return cmp.value
+
+    def run_experiment(self, path, fmt, W, H, mask_pattern, algos, cfg: _Cfg, block_size_auto=True, frame_limit=0, csv_path=None, dump_dir=None):
+        """The reference's own run_experiment (bench.cpp:120-227) on a sequence
+        file (reference build only).  Returns the AlgoSummary values per algo
+        (10 doubles, NaN for absent optionals); the CSV goes to csv_path."""
+        if self.kind != "reference":
+            raise OracleError(1, "run_experiment needs the reference build")
+        a = (C.c_int * len(algos))(*algos)
+        out = np.zeros((len(algos), 10), np.float64)
+        enc = lambda s: None if s is None else s.encode()
+        self._chk(self._f("run_experiment")(enc(path), fmt, W, H, enc(mask_pattern), a, len(algos), C.byref(cfg),
+                                            int(block_size_auto), frame_limit, enc(csv_path), enc(dump_dir), _vp(out)))
+        return out

@@ -14,6 +14,9 @@
 //     brs_select + prs_refine with a descent_log), and the replayed vector is
 //     checked against estimate_field's; the aggregate SearchStats of the
 //     replay must equal estimate_field's too (returns -1 otherwise).
+//   * ref_run_experiment — the reference's own run_experiment (bench.cpp:120-227)
+//       on a sequence file: writes its CSV and returns the AlgoSummary values
+//       (golden source for the experiment-report tests).
 //   * ref_* per-block wrappers used by the unit-level parity tests.
 // Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline
 // legs load this library.
@@ -29,8 +32,10 @@
 #include <thread>
 #include <vector>
 
+#include "me/bench.hpp"
 #include "me/compensation.hpp"
 #include "me/estimators.hpp"
+#include "me/video_io.hpp"
 #include "me/frame.hpp"
 #include "me/metrics.hpp"
 #include "me_b200.h"
@@ -536,6 +541,57 @@ int ref_psnr(int w, int h, const uint8_t* a, const uint8_t* b, double* mse, doub
     *infinite = r.infinite() ? 1 : 0;
     *db = r.psnr_db ? *r.psnr_db : 0.0;
     return 0;
+}
+
+
+// run_experiment (bench.cpp:120-227) on an I420 (format 0) or Y4M (1) file.
+// summaries: n_algos x 10 doubles {frame_pairs, mean_mse, mean_psnr_db,
+// psnr_db_of_mean_mse, mean_psnr_linear, avg_search_points, indicator,
+// total_comparisons, total_dpd_steps, total_blocks_estimated}; absent
+// optionals are NaN.
+int ref_run_experiment(const char* path, int format, int w, int h, const char* mask_pattern,
+                       const int* algos, int n_algos, const me_config* c, int block_size_auto,
+                       int frame_limit, const char* csv_path, const char* dump_dir, double* summaries) {
+    try {
+        ExperimentConfig cfg;
+        cfg.source = format ? open_y4m(path) : open_i420(path, w, h);
+        if (mask_pattern) cfg.masks.pattern = mask_pattern;
+        for (int i = 0; i < n_algos; ++i) cfg.algos.push_back(static_cast<Algo>(algos[i]));
+        cfg.search.search_range = c->search_range;
+        cfg.search.block_size = c->block_size;
+        cfg.search.ref_distance = c->ref_distance;
+        cfg.search.halfpel = c->halfpel != 0;
+        cfg.prs.epsilon = c->epsilon;
+        cfg.prs.theta = c->theta;
+        cfg.prs.max_iterations = c->max_iterations;
+        cfg.prs.step = c->step;
+        cfg.boundary_temporal = c->boundary_temporal ? BoundaryTemporal::Shape : BoundaryTemporal::Texture;
+        cfg.block_size_auto = block_size_auto != 0;
+        cfg.frame_limit = frame_limit;
+        if (csv_path) cfg.csv_path = csv_path;
+        if (dump_dir) cfg.dump_dir = dump_dir;
+        const ExperimentResult r = run_experiment(cfg);
+        const double nan = std::nan("");
+        for (std::size_t i = 0; i < r.summaries.size(); ++i) {
+            const AlgoSummary& s = r.summaries[i];
+            double* o = summaries + 10 * i;
+            o[0] = s.frame_pairs;
+            o[1] = s.mean_mse;
+            o[2] = s.mean_psnr_db ? *s.mean_psnr_db : nan;
+            o[3] = s.psnr_db_of_mean_mse ? *s.psnr_db_of_mean_mse : nan;
+            o[4] = s.mean_psnr_linear ? *s.mean_psnr_linear : nan;
+            o[5] = s.avg_search_points;
+            o[6] = s.indicator ? *s.indicator : nan;
+            o[7] = double(s.total_comparisons);
+            o[8] = double(s.total_dpd_steps);
+            o[9] = double(s.total_blocks_estimated);
+        }
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
 }
 
 }  // extern "C"

@@ -341,7 +341,8 @@ def figure_of_merit(psnr_linear: float, s: int, c: float) -> float:  # metrics.c
         raise ValueError("figure_of_merit: search range must be >= 1")
     if not (c > 0.0):
         raise ValueError("figure_of_merit: average compared blocks must be > 0")
-    return psnr_linear * float(2 * s + 1) * float(2 * s + 1) / c
+    window = float(2 * s + 1) * float(2 * s + 1)
+    return psnr_linear * window / c
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,200 @@
+"""Sequence and mask I/O of the reference (video_io.cpp), host side.
+
+Frames are read whole into pinned-friendly contiguous numpy arrays
+(``[frames, H, W]`` luma, chroma optional) so a sequence goes to the GPU in
+one batched call.  Formats and error behaviour follow the reference:
+
+* I420 raw (``open_i420``, video_io.cpp:126-138): frame count from the file
+  size, which must be a multiple of W*H*3/2.
+* Y4M (``open_y4m`` / ``parse_y4m_header``, :79-159): only ``C420*``
+  colourspaces, W and H tags required, a fixed-length ``FRAME`` marker.
+* P5 PGM masks (``read_pgm``, :194-214; '#' comments skipped) binarised at a
+  threshold (``read_mask``, :184-192; ``binarize`` frame.cpp:50-56), file
+  names from a printf-style pattern (``MaskSource::path_for``, :71-77).
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .api import check_dimensions  # frame.cpp:34-40
+
+I420, Y4M = 0, 1
+
+
+@dataclass
+class SequenceSource:  # video_io.hpp:32-45
+    path: str = ""
+    format: int = I420
+    width: int = 0
+    height: int = 0
+    frame_count: int = 0
+    header_bytes: int = 0
+    frame_marker_bytes: int = 0
+
+    def frame_bytes(self) -> int:
+        return self.width * self.height * 3 // 2
+
+
+@dataclass
+class MaskSource:  # video_io.hpp:49-55
+    pattern: str = ""
+    threshold: int = 128
+
+    def present(self) -> bool:
+        return bool(self.pattern)
+
+    def path_for(self, index: int) -> str:
+        return self.pattern % index
+
+
+def parse_y4m_header(line: str) -> SequenceSource:
+    tags = line.split()
+    if not tags or tags[0] != "YUV4MPEG2":
+        raise RuntimeError("not a Y4M stream (missing YUV4MPEG2 signature)")
+    src = SequenceSource(format=Y4M)
+    have_w = have_h = False
+    for tag in tags[1:]:
+        if tag[0] == "W":
+            src.width, have_w = int(tag[1:]), True
+        elif tag[0] == "H":
+            src.height, have_h = int(tag[1:]), True
+        elif tag[0] == "C" and not tag.startswith("C420"):
+            raise RuntimeError(f"unsupported Y4M colorspace {tag} (only 4:2:0 accepted)")
+    if not (have_w and have_h):
+        raise RuntimeError("Y4M header missing W or H tag")
+    check_dimensions(src.width, src.height)
+    return src
+
+
+def open_i420(path: str, width: int, height: int) -> SequenceSource:
+    check_dimensions(width, height)
+    src = SequenceSource(path=path, format=I420, width=width, height=height)
+    size = os.path.getsize(path)
+    if size % src.frame_bytes():
+        raise RuntimeError(f"{path}: size is not a multiple of the I420 frame size")
+    src.frame_count = size // src.frame_bytes()
+    return src
+
+
+def open_y4m(path: str) -> SequenceSource:
+    with open(path, "rb") as f:
+        header = f.readline()
+        if not header.endswith(b"\n"):
+            raise RuntimeError(f"cannot read Y4M header from {path}")
+        src = parse_y4m_header(header[:-1].decode("latin-1"))
+        marker = f.readline()
+    src.path = path
+    src.header_bytes = len(header)
+    if not marker:
+        raise RuntimeError(f"{path}: Y4M stream has no frames")
+    if not marker.startswith(b"FRAME"):
+        raise RuntimeError(f"{path}: expected FRAME marker")
+    src.frame_marker_bytes = len(marker)
+    stride = src.frame_marker_bytes + src.frame_bytes()
+    payload = os.path.getsize(path) - src.header_bytes
+    if payload % stride:
+        raise RuntimeError(f"{path}: truncated or irregular Y4M stream")
+    src.frame_count = payload // stride
+    return src
+
+
+def open_sequence(path: str, width: int = 0, height: int = 0) -> SequenceSource:
+    """Y4M by extension (``.y4m``), else headerless I420 of the given size."""
+    if path.lower().endswith(".y4m"):
+        return open_y4m(path)
+    return open_i420(path, width, height)
+
+
+def read_frames(src: SequenceSource, count: Optional[int] = None, chroma: bool = False):
+    """Frames 0..count-1 as a ``[count, H, W]`` uint8 luma array (and, with
+    ``chroma``, ``[count, 2, H/2, W/2]``), one sequential read of the file."""
+    n = src.frame_count if count is None else count
+    if n < 0 or n > src.frame_count:
+        raise IndexError(f"frame index {n - 1} out of range [0,{src.frame_count})")
+    W, H, fb = src.width, src.height, src.frame_bytes()
+    stride = fb + (src.frame_marker_bytes if src.format == Y4M else 0)
+    raw = np.fromfile(src.path, dtype=np.uint8, count=src.header_bytes + n * stride)
+    body = raw[src.header_bytes:].reshape(n, stride) if n else np.zeros((0, stride), np.uint8)
+    if src.format == Y4M:
+        m = body[:, : src.frame_marker_bytes]
+        if n and (not (m[:, :5] == np.frombuffer(b"FRAME", np.uint8)).all() or not (m[:, -1] == 10).all()):
+            bad = int(np.flatnonzero(~((m[:, :5] == np.frombuffer(b"FRAME", np.uint8)).all(1) & (m[:, -1] == 10)))[0])
+            raise RuntimeError(f"{src.path}: irregular FRAME marker at index {bad}")
+        body = body[:, src.frame_marker_bytes:]
+    luma = np.ascontiguousarray(body[:, : W * H].reshape(n, H, W))
+    if not chroma:
+        return luma
+    c = np.ascontiguousarray(body[:, W * H:].reshape(n, 2, H // 2, W // 2))
+    return luma, c
+
+
+def read_pgm(path: str) -> np.ndarray:
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:2] != b"P5":
+        raise RuntimeError(f"{path}: not a binary P5 PGM")
+    pos, vals = 2, []
+    for _ in range(3):
+        while pos < len(data) and data[pos:pos + 1] in (b" ", b"\t", b"\r", b"\n", b"#"):
+            if data[pos:pos + 1] == b"#":
+                nl = data.find(b"\n", pos)
+                pos = len(data) if nl < 0 else nl + 1
+            else:
+                pos += 1
+        start = pos
+        while pos < len(data) and data[pos:pos + 1].isdigit():
+            pos += 1
+        if start == pos:
+            raise RuntimeError(f"malformed PGM header in {path}")
+        vals.append(int(data[start:pos]))
+    w, h, maxval = vals
+    if w <= 0 or h <= 0 or maxval <= 0 or maxval > 255:
+        raise RuntimeError(f"{path}: unsupported PGM geometry or maxval")
+    pos += 1  # single whitespace byte after maxval
+    payload = np.frombuffer(data, dtype=np.uint8, count=min(w * h, max(0, len(data) - pos)), offset=pos)
+    if payload.size != w * h:
+        raise RuntimeError(f"{path}: truncated PGM payload")
+    return payload.reshape(h, w).copy()
+
+
+def write_gray_pgm(plane: np.ndarray, path: str):  # video_io.cpp:216-223
+    h, w = plane.shape
+    with open(path, "wb") as f:
+        f.write(b"P5\n%d %d\n255\n" % (w, h))
+        f.write(np.ascontiguousarray(plane, dtype=np.uint8).tobytes())
+
+
+def binarize(gray: np.ndarray, threshold: int = 128) -> np.ndarray:  # frame.cpp:50-56
+    return np.where(gray >= threshold, 255, 0).astype(np.uint8)
+
+
+def read_masks(src: MaskSource, count: int, width: int, height: int) -> np.ndarray:
+    """``[count, H, W]`` binarised masks (read_mask, video_io.cpp:184-192)."""
+    if not src.present():
+        raise RuntimeError("read_mask called without a mask pattern")
+    out = np.empty((count, height, width), np.uint8)
+    for i in range(count):
+        gray = read_pgm(src.path_for(i))
+        if gray.shape != (height, width):
+            raise RuntimeError(f"mask {src.path_for(i)} is {gray.shape[1]}x{gray.shape[0]}, video is {width}x{height}")
+        out[i] = binarize(gray, src.threshold)
+    return out
+
+
+def write_i420(path: str, luma: np.ndarray, chroma: Optional[np.ndarray] = None, y4m: bool = False):
+    """Writes frames (gray chroma 128 when absent, append_i420_frame
+    video_io.cpp:225-240); ``y4m`` adds the stream header and FRAME markers."""
+    n, H, W = luma.shape
+    gray = np.full((2, H // 2, W // 2), 128, np.uint8)
+    with open(path, "wb") as f:
+        if y4m:
+            f.write(b"YUV4MPEG2 W%d H%d F25:1 Ip A1:1 C420jpeg\n" % (W, H))
+        for i in range(n):
+            if y4m:
+                f.write(b"FRAME\n")
+            f.write(np.ascontiguousarray(luma[i]).tobytes())
+            f.write((gray if chroma is None else np.ascontiguousarray(chroma[i])).tobytes())
