@@ -2480,14 +2480,21 @@ size_t scratch_bytes(const Batch& b, int algo) {
 }
 
 // 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel
-int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0) {
+// Wide wavefront steps (many independent blocks per step) are throughput-
+// bound: two blocks per warp (duo) keep more blocks in flight.  Narrow ones
+// (single sequences, small batches) are latency-bound: a whole warp per block
+// (fast) finishes each block sooner.  Measured crossover (CIF, 148 SMs):
+// between 64 and 128 sequences, i.e. ~25 000 blocks per step.
+int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, int num_sms) {
     const int step = cfg.halfpel ? 1 : cfg.step;
     const bool fast = b.bs == 8 && step == 2 && cfg.max_iterations <= 4 && !prev0 &&
                       size_t(b.n_seq) * b.F * b.W * b.H < (size_t(1) << 32);
     const char* mode = getenv("ME_PA_MODE");
-    const std::string m = mode ? mode : "duo";
-    if (!fast || m == "warp") return 0;
-    return m == "fast" ? 1 : 2;
+    if (!fast || (mode && std::string(mode) == "warp")) return 0;
+    if (mode && std::string(mode) == "fast") return 1;
+    if (mode && std::string(mode) == "duo") return 2;
+    const int64_t per_step = b.nblocks() / std::max(1, b.steps());
+    return per_step >= int64_t(num_sms) * 160 ? 2 : 1;
 }
 
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
@@ -2537,7 +2544,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     // (ME_PA_MODE=fast); ME_PA_MODE=warp forces the generic pa_kernel.  The duo
     // kernel takes list entries in pairs: every wavefront step is padded to an
     // even count.
-    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0) : 0;
+    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, num_sms) : 0;
     scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, pa_mode == 2 ? 2 : 1, s.offs, s.cursor, s.list);
     if ((e = cudaGetLastError())) return e;
     {
@@ -2608,7 +2615,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         const char* minb = getenv("ME_PA_MINB");
         auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
         if (pa_mode == 1) {
-            const int mb = minb ? atoi(minb) : 5;
+            const int mb = minb ? atoi(minb) : 4;
             kern = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         } else if (pa_mode == 2) {
             const int mb = minb ? atoi(minb) : 4;
