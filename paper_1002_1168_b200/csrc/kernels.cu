@@ -460,16 +460,34 @@ constexpr uint32_t kInvalidEntry = 0xFFFFFFFFu;
 // otherwise queue on a handful of L2 lines
 constexpr int kCursorStride = 32;
 
+// ranges (optional): the list split at the first and after the last step
+// holding >= wide blocks: {0, b1}, {b1, b2}, {b2, total} (narrow, wide, narrow).
 __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
-                            uint2* list) {
+                            uint2* list, int wide, int* ranges) {
     __shared__ int s_part[1024];
+    __shared__ int s_lo, s_hi;  // first / last wide step
     const int T = blockDim.x;
     const int per = (nbins + T - 1) / T;
     const int lo = threadIdx.x * per, hi = min(lo + per, nbins);
     auto padded = [&](int v) { return (v + pad - 1) / pad * pad; };
-    int sum = 0;
-    for (int i = lo; i < hi; ++i) sum += padded(hist[i]);
+    if (threadIdx.x == 0) {
+        s_lo = nbins;
+        s_hi = -1;
+    }
+    __syncthreads();
+    int sum = 0, my_lo = nbins, my_hi = -1;
+    for (int i = lo; i < hi; ++i) {
+        sum += padded(hist[i]);
+        if (hist[i] >= wide) {
+            my_lo = min(my_lo, i);
+            my_hi = max(my_hi, i);
+        }
+    }
     s_part[threadIdx.x] = sum;
+    if (ranges && my_hi >= 0) {
+        atomicMin(&s_lo, my_lo);
+        atomicMax(&s_hi, my_hi);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         int acc = 0;
@@ -487,6 +505,19 @@ __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int*
         cursor[i * kCursorStride] = acc;
         for (int k = hist[i]; k < padded(hist[i]); ++k) list[acc + k] = make_uint2(kInvalidEntry, kInvalidEntry);
         acc += padded(hist[i]);
+    }
+    if (ranges) {
+        __syncthreads();  // offs[] complete
+        if (threadIdx.x == 0) {
+            const int total = offs[nbins];
+            const int b1 = s_hi >= 0 ? offs[s_lo] : total, b2 = s_hi >= 0 ? offs[s_hi + 1] : total;
+            ranges[0] = 0;
+            ranges[1] = b1;
+            ranges[2] = b1;
+            ranges[3] = b2;
+            ranges[4] = b2;
+            ranges[5] = total;
+        }
     }
 }
 
@@ -1211,7 +1242,7 @@ struct PaArgs {
     int fast;              // patch fast path allowed (step 2, max_iter <= 4)
     int warp_words;        // shared words per warp
     int poll_ns;           // dependency poll interval
-    int* counter;          // dynamic item counter (zeroed) or null: static round robin
+    const int* range;      // [begin, end) of the list for this launch (device) or null: [0, *nlist)
     unsigned long long* trace;  // debug: per entry {claimed, deps ready, done, smid} (ns)
 };
 
@@ -1565,36 +1596,15 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     uint32_t* cw = ws + 4 * kFastPatch;      // [8][2] current block
     uint32_t* vis = cw + 16;                 // [3] visited lattice bits
     const int nwarps = gridDim.x * (blockDim.x >> 5);
-    const int n = *a.nlist;
+    const int beg = a.range ? a.range[0] : 0, n = a.range ? a.range[1] : *a.nlist;
     const int W = a.b.W, H = a.b.H, S = a.P.S;
     const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
     const int c = lane >> 3, sub = lane & 7;
     const int k = lane >> 2, q = lane & 3;   // PRS: neighbour k, rows q and q + 4
     const int kx = off8x(k), ky = off8y(k);
     // static round-robin over the wavefront-sorted list (see pa_kernel)
-    // Items are taken in list (wavefront) order, statically round robin or
-    // dynamically from a counter; either way the least unfinished item's
-    // dependencies are finished, so the wait below always makes progress.
-    // The next item is claimed one item ahead to hide the claim latency.
-    int* const ctr = a.counter;
-    int item = blockIdx.x * (blockDim.x >> 5) + wid, nxt = item + nwarps;
-    if (ctr) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(ctr, 2);
-        t = __shfl_sync(0xFFFFFFFFu, t, 0);
-        item = t;
-        nxt = t + 1;
-    }
-    for (; item < n;) {
+    for (int item = beg + blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
         const uint2 e = __ldg(a.list + item);
-        item = nxt;
-        if (ctr) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(ctr, 1);
-            nxt = __shfl_sync(0xFFFFFFFFu, t, 0);
-        } else {
-            nxt += nwarps;
-        }
         if (e.x == kInvalidEntry) continue;
         const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
         const uint32_t seq = e.y >> 16;
@@ -1821,14 +1831,14 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     uint32_t* patch = ws + hf * kDuoTaskWords;  // [4][16][12]
     uint32_t* cw = patch + 4 * kDuoPatch;      // [8][2] current block
     const int nwarps = gridDim.x * (blockDim.x >> 5);
-    const int n = *a.nlist;
+    const int beg = a.range ? a.range[0] : 0, n = a.range ? a.range[1] : *a.nlist;  // beg, n even
     const int W = a.b.W, H = a.b.H, S = a.P.S;
     const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
     const uint32_t plane = uint32_t(W) * uint32_t(H);
     const int c = hl >> 2, q4 = hl & 3;  // BRS: candidate c, block rows q4 and q4 + 4
     const int k = hl >> 1, q2 = hl & 1;  // PRS: neighbour k, block rows q2 + {0, 2, 4, 6}
     const int kx = off8x(k), ky = off8y(k);
-    for (int item = 2 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 2 * nwarps) {
+    for (int item = beg + 2 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 2 * nwarps) {
         const uint2 e = __ldg(a.list + item + hf);
         const bool act = e.x != kInvalidEntry;  // uniform per half
         unsigned long long t_claim = 0, t_ready = 0;
@@ -2485,6 +2495,12 @@ size_t scratch_bytes(const Batch& b, int algo) {
 // (single sequences, small batches) are latency-bound: a whole warp per block
 // (fast) finishes each block sooner.  Measured crossover (CIF, 148 SMs):
 // between 64 and 128 sequences, i.e. ~25 000 blocks per step.
+// Steps with at least this many estimated blocks run two blocks per warp.
+int pa_wide_threshold(int num_sms) {
+    const char* e = getenv("ME_PA_WIDE");
+    return e ? atoi(e) : num_sms * 40;  // measured: 3000-9000 within 1 %, duo-only 3 % slower
+}
+
 int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, int num_sms) {
     const int step = cfg.halfpel ? 1 : cfg.step;
     const bool fast = b.bs == 8 && step == 2 && cfg.max_iterations <= 4 && !prev0 &&
@@ -2494,7 +2510,7 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, i
     if (mode && std::string(mode) == "fast") return 1;
     if (mode && std::string(mode) == "duo") return 2;
     const int64_t per_step = b.nblocks() / std::max(1, b.steps());
-    return per_step >= int64_t(num_sms) * 160 ? 2 : 1;
+    return per_step >= int64_t(num_sms) * 160 ? 3 : 1;
 }
 
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
@@ -2545,7 +2561,11 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     // kernel takes list entries in pairs: every wavefront step is padded to an
     // even count.
     const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, num_sms) : 0;
-    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, pa_mode == 2 ? 2 : 1, s.offs, s.cursor, s.list);
+    // hybrid: narrow steps (fewer than `wide` blocks) on the fast kernel, the
+    // wide middle of the wavefront on the duo kernel
+    int* ranges = pa_mode == 3 ? s.counter + 8 : nullptr;
+    scan_kernel<<<1, 1024, 0, st>>>(s.hist, nbins, pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
+                                    pa_wide_threshold(num_sms), ranges);
     if ((e = cudaGetLastError())) return e;
     {
         // <= 128 rows per CTA (fewer global atomics), >= 2 CTAs per SM
@@ -2590,8 +2610,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         pa_args.P = make_pa_params(b, cfg);
         pa_args.list = s.list;
         pa_args.nlist = nlist;
-        const char* sched = getenv("ME_PA_SCHED");
-        pa_args.counter = (sched && std::string(sched) == "dyn") ? s.counter : nullptr;
+        pa_args.range = nullptr;
         pa_args.recs = recs;
         pa_args.prev0 = prev0;
         pa_args.stats = stats;
@@ -2607,31 +2626,50 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             cudaMemset(pa_args.trace, 0, size_t(n_host) * 32);
         }
         const char* cta = getenv("ME_PA_CTA");
-        const int threads = pa_mode == 2 && cta ? atoi(cta) : 256;
-        pa_args.warp_words = pa_mode == 2   ? std::max(pa_args.P.bm_words, kDuoWarpWords)
-                             : pa_mode == 1 ? std::max(pa_args.P.bm_words, kFastWarpWords)
-                                            : std::max(pa_args.P.bm_words, b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS);
-        const size_t smem = size_t(threads / 32) * pa_args.warp_words * 4;
         const char* minb = getenv("ME_PA_MINB");
-        auto kern = b.bs == 8 ? pa_kernel<8> : pa_kernel<16>;
-        if (pa_mode == 1) {
+        using PaKernel = void (*)(const PaArgs);
+        // persistent grids: every warp of a launch must be co-resident (dependency spinning)
+        auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range) -> cudaError_t {
+            PaArgs la = pa_args;
+            la.range = range;
+            la.warp_words = std::max(la.P.bm_words, warp_words);
+            const size_t smem = size_t(threads / 32) * la.warp_words * 4;
+            cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e2) return e2;
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+            kern<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(la);
+            return cudaGetLastError();
+        };
+        PaKernel fast = pa_fast_kernel<4>;
+        {
             const int mb = minb ? atoi(minb) : 4;
-            kern = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
-        } else if (pa_mode == 2) {
+            fast = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
+        }
+        const int duo_threads = cta ? atoi(cta) : 256;
+        PaKernel duo = pa_duo_kernel<256, 4>;
+        {
             const int mb = minb ? atoi(minb) : 4;
             if (trace_path)
-                kern = pa_duo_kernel<256, 4, true>;
-            else if (threads == 128)
-                kern = mb == 8 ? pa_duo_kernel<128, 8> : mb == 6 ? pa_duo_kernel<128, 6> : pa_duo_kernel<128, 7>;
-            else
-                kern = mb == 4 ? pa_duo_kernel<256, 4> : pa_duo_kernel<256, 3>;
+                duo = pa_duo_kernel<256, 4, true>;
+            else if (duo_threads == 128)
+                duo = mb == 8 ? pa_duo_kernel<128, 8> : mb == 6 ? pa_duo_kernel<128, 6> : pa_duo_kernel<128, 7>;
+            else if (mb == 3)
+                duo = pa_duo_kernel<256, 3>;
         }
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-        // persistent: every warp must be co-resident (dependency spinning)
-        kern<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(pa_args);
-        if ((e = cudaGetLastError())) return e;
+        if (pa_mode == 0) {
+            e = launch(b.bs == 8 ? pa_kernel<8> : pa_kernel<16>, 256,
+                       b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS, nullptr);
+        } else if (pa_mode == 1) {
+            e = launch(fast, 256, kFastWarpWords, nullptr);
+        } else if (pa_mode == 2) {
+            e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, nullptr);
+        } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast
+            if (!(e = launch(fast, 256, kFastWarpWords, ranges)) &&
+                !(e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, ranges + 2)))
+                e = launch(fast, 256, kFastWarpWords, ranges + 4);
+        }
+        if (e) return e;
         if (trace_path) {
             std::vector<unsigned long long> h(size_t(n_host) * 4);
             std::vector<uint2> lst(n_host);
