@@ -3,12 +3,14 @@ arXiv 1002.1168, a drop-in for the reference's me:: estimation entry points.
 
 Layers:
   include/me_b200.h           C ABI (the drop-in boundary)
-  csrc/kernels.cu             sm_100a kernels (classify, ES, rings, PA wavefront, MC+PSNR)
+  csrc/*.cu                   sm_100a kernels: wavefront.cu (classify, sort), es.cu, ring.cu,
+                              pa.cu (PA wavefront), frame_ops.cu (MC+PSNR, masks), batch.cu (pipeline)
   csrc/capi.cu                validation, contexts, staging, dispatch
   shim/me_drop_in.cpp         C++ me:: definitions over the C ABI (reference headers)
   api.py                      Python mirror of the reference API (tests, users)
   batch.py                    batched sequence pipeline (benchmark path)
   synth.py                    seeded synthetic configs 1..5
+  experiment.py, seqio.py     run_experiment (CSV / summaries) and sequence I/O
 """
 from ._lib import LIB_PATH, lib, rec_dtype, stats_dtype  # noqa: F401
 from .api import (  # noqa: F401

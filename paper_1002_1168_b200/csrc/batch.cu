@@ -1,0 +1,147 @@
+// batch.cu — the device pipeline of a batch of sequences (run_batch:
+// classify -> wavefront sort -> search -> prediction) and the dispatch of the
+// single-block searches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+
+namespace mek {
+
+namespace {
+
+struct Scratch {
+    uint8_t* types;
+    uint2* list;
+    int* hist;
+    int* offs;
+    int* cursor;
+    int* counter;
+};
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+Scratch carve(const Batch& b, int nbins, void* base) {
+    Scratch s;
+    uint8_t* p = static_cast<uint8_t*>(base);
+    const size_t nb = size_t(b.nblocks());
+    s.types = p;
+    p += align_up(nb);
+    s.list = reinterpret_cast<uint2*>(p);
+    p += align_up((nb + size_t(nbins)) * 8);
+    s.hist = reinterpret_cast<int*>(p);
+    p += align_up(size_t(nbins) * 4);
+    s.offs = reinterpret_cast<int*>(p);
+    p += align_up(size_t(nbins + 1) * 4);
+    s.cursor = reinterpret_cast<int*>(p);
+    p += align_up(size_t(nbins) * 4 * kCursorStride);
+    s.counter = reinterpret_cast<int*>(p);
+    return s;
+}
+
+}  // namespace
+
+// Ordering of the PA work list: key = A * t + S * seq, t = h + 2v + p.  Any
+// A >= 1 keeps every dependency (key - A or key - 2A) strictly earlier; S > 0
+// staggers the sequences' wavefronts.  Overridable for experiments through
+// ME_PA_KEY_A / ME_PA_KEY_S.
+struct KeyParams {
+    int a, s;
+};
+
+KeyParams pa_key(const Batch& b) {
+    KeyParams k{1, 0};
+    if (const char* e = getenv("ME_PA_KEY_A")) k.a = std::max(1, atoi(e));
+    if (const char* e = getenv("ME_PA_KEY_S")) k.s = std::max(0, atoi(e));
+    if (int64_t(k.a) * (b.steps() - 1) + int64_t(k.s) * (b.n_seq - 1) + 1 > 12288) k = KeyParams{1, 0};
+    return k;
+}
+
+int pa_bins(const Batch& b) {
+    const KeyParams k = pa_key(b);
+    return k.a * (b.steps() - 1) + k.s * (b.n_seq - 1) + 1;
+}
+
+size_t scratch_bytes(const Batch& b, int algo) {
+    const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
+    const size_t nb = size_t(b.nblocks());
+    return align_up(nb) + align_up((nb + size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
+           align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4 * kCursorStride) + 256;
+}
+
+// 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel
+// Wide wavefront steps (many independent blocks per step) are throughput-
+// bound: two blocks per warp (duo) keep more blocks in flight.  Narrow ones
+// (single sequences, small batches) are latency-bound: a whole warp per block
+// (fast) finishes each block sooner.  Measured crossover (CIF, 148 SMs):
+// between 64 and 128 sequences, i.e. ~25 000 blocks per step.
+
+cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
+                      me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
+                      size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events) {
+    const int algo = cfg.algo;
+    const bool pa = algo == ME_ALGO_PA;
+    const int nbins = pa ? pa_bins(b) : 1;
+    if (scratch_size < scratch_bytes(b, algo)) return cudaErrorInvalidValue;
+    Scratch s = carve(b, nbins, scratch);
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(s.hist, 0, size_t(nbins) * 4, st))) return e;
+    if ((e = cudaMemsetAsync(s.counter, 0, 4, st))) return e;
+    if (stats && (e = cudaMemsetAsync(stats, 0, sizeof(me_pair_stats) * size_t(b.n_seq) * b.pairs, st)))
+        return e;
+
+    if (events) cudaEventRecord(events[0], st);
+    ClassArgs ca;
+    ca.b = b;
+    ca.pa = pa ? 1 : 0;
+    ca.recs = recs;
+    ca.types = s.types;
+    ca.hist = s.hist;
+    ca.nbins = nbins;
+    ca.stats = stats;
+    {
+        const KeyParams k = pa_key(b);
+        ca.key_a = k.a;
+        ca.key_s = k.s;
+    }
+    if ((e = launch_classify(ca, num_sms, st))) return e;
+    if (events) cudaEventRecord(events[1], st);
+    // PA kernel choice (pa.cu): the duo kernel takes list entries in pairs, so
+    // every wavefront step is padded to an even count; the hybrid splits the
+    // list into narrow / wide / narrow step ranges.
+    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, num_sms) : 0;
+    int* ranges = pa_mode == 3 ? s.counter + 8 : nullptr;
+    if ((e = launch_scan(s.hist, nbins, pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
+                         pa_wide_threshold(num_sms), ranges, st)))
+        return e;
+    if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st))) return e;
+    const int* nlist = s.offs + nbins;
+    if (events) cudaEventRecord(events[2], st);
+
+    if (algo == ME_ALGO_ES)
+        e = launch_es(b, cfg.search_range, s.list, nlist, s.counter, recs, stats, num_sms, st);
+    else if (algo == ME_ALGO_PA)
+        e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st);
+    else
+        e = launch_ring(b, algo, cfg.search_range, s.list, nlist, recs, stats, num_sms, st);
+    if (e) return e;
+
+    if (events) cudaEventRecord(events[3], st);
+    if (pred && (e = launch_mc_pred(b, recs, pred, st))) return e;
+    if (events) cudaEventRecord(events[4], st);
+    return cudaGetLastError();
+}
+
+cudaError_t block_search(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H, int x0,
+                         int y0, int size, int range, int64_t* out, cudaStream_t st) {
+    if (algo == ME_ALGO_ES) return launch_es_single(cur, ref, W, H, x0, y0, size, range, out, st);
+    return launch_ring_single(algo, cur, ref, W, H, x0, y0, size, range, out, st);
+}
+
+}  // namespace mek

@@ -1,7 +1,7 @@
 // capi.cu — the C ABI (include/me_b200.h): argument validation with the
 // reference's error semantics, per-thread contexts with device buffer caches,
 // host<->device staging for the host-pointer entry points, and dispatch into
-// the kernels of kernels.cu.  No CPU compute path exists: every entry point
+// the kernels (csrc/*.cu).  No CPU compute path exists: every entry point
 // either runs on an sm_100 device or fails with ME_ERR_NO_DEVICE.
 
 #include <cuda_runtime.h>

@@ -1,0 +1,295 @@
+// es.cu — full_search (estimators.cpp:167-187): the batched kernel over the
+// work list and the single-block kernel behind the per-block entry point.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+
+namespace mek {
+
+// ---------------------------------------------------------------------------
+// es_kernel: full_search (estimators.cpp:167-187).  One CTA per estimated
+// block (persistent CTAs pull blocks from the work list).  The reference
+// window (clipped, pel units, estimators.cpp:62-65) is staged in shared memory
+// as 4 copies pre-shifted by 0..3 bytes so every candidate row is read as
+// aligned 32-bit words; the current block lives in registers.  A thread owns
+// one dx column and a run of K consecutive dy: each staged reference row is
+// loaded once and reused for every accumulator whose current row it pairs
+// with.  The winner is the minimum packed key (SAD, |dx|+|dy|, raster index)
+// — exactly the reference's strict-< scan with the Manhattan tie-break.
+// ---------------------------------------------------------------------------
+
+struct EsArgs {
+    Batch b;
+    int S;
+    const uint2* list;
+    const int* nlist;  // device count (offs[nbins])
+    int* counter;
+    me_block_rec* recs;
+    int band_rows_max;  // staged rows per band (multiple of K, + BS - 1 added on top)
+    me_pair_stats* stats;
+};
+
+constexpr int kEsThreads = 256;
+
+template <int BS, int K>
+__device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                         int S, int band_runs_max, uint32_t* sm, unsigned long long* s_best,
+                         int& out_dx, int& out_dy, uint32_t& out_sad, uint32_t& out_cmp) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int lo_x = max(-S, -x0), hi_x = min(S, W - x0 - BS);
+    const int lo_y = max(-S, -y0), hi_y = min(S, H - y0 - BS);
+    const int WX = hi_x - lo_x + 1, WY = hi_y - lo_y + 1;
+    const int nruns = (WY + K - 1) / K;
+    const int rowbytes = WX + BS - 1;
+    const int PW = ((WX - 1) >> 2) + (BS >> 2) + 1;  // words per staged row
+    constexpr int NW = BS / 4;
+
+    uint32_t c[BS][NW];
+    if (((x0 | W) & 3) == 0) {
+#pragma unroll
+        for (int r = 0; r < BS; ++r)
+#pragma unroll
+            for (int i = 0; i < NW; ++i) c[r][i] = ldg32(cur + size_t(y0 + r) * W + x0 + 4 * i);
+    } else {
+#pragma unroll
+        for (int r = 0; r < BS; ++r)
+#pragma unroll
+            for (int i = 0; i < NW; ++i) {
+                const uint8_t* q = cur + size_t(y0 + r) * W + x0 + 4 * i;
+                c[r][i] = uint32_t(q[0]) | (uint32_t(q[1]) << 8) | (uint32_t(q[2]) << 16) |
+                          (uint32_t(q[3]) << 24);
+            }
+    }
+
+    unsigned long long best = ~0ull;
+    for (int run0 = 0; run0 < nruns; run0 += band_runs_max) {
+        const int bruns = min(band_runs_max, nruns - run0);
+        const int srows = bruns * K + BS - 1;
+        int CW = srows * PW;
+        CW += ((8 - (CW & 31)) + 32) & 31;  // copy stride = 8 (mod 32) words: conflict-free lanes
+        const int row_g0 = y0 + lo_y + run0 * K;  // frame row of staged row 0
+        const int rows_valid = min(srows, WY + BS - 1 - run0 * K);
+        const uint8_t* rb = ref + size_t(row_g0) * W + (x0 + lo_x);
+        __syncthreads();  // previous band / block done with smem
+        // staging from aligned words: copy s, word q = bytes [4q + s, 4q + s + 4)
+        // of the row segment = a funnel shift of two aligned words.  Bytes past
+        // the segment are never paired with the current block (only rows and
+        // columns of admissible positions are summed), so the loads clamp to
+        // the segment's last aligned word and rows past the window are skipped.
+        for (int row = tid / PW, q = tid - (tid / PW) * PW; row < srows;) {
+            if (row < rows_valid) {
+                const uint8_t* seg = rb + size_t(row) * W;
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(seg) & ~uintptr_t(3);
+                const uint32_t off = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3);
+                const uintptr_t last = (reinterpret_cast<uintptr_t>(seg) + rowbytes - 1) & ~uintptr_t(3);
+                uint32_t g[3];
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    const uintptr_t ad = min(a0 + 4 * uintptr_t(q + m), last);
+                    g[m] = __ldg(reinterpret_cast<const uint32_t*>(ad));
+                }
+#pragma unroll
+                for (int sft = 0; sft < 4; ++sft) {
+                    const uint32_t t = off + sft;  // 0..6
+                    const uint32_t lo = t < 4 ? g[0] : g[1], hi = t < 4 ? g[1] : g[2];
+                    sm[sft * CW + row * PW + q] = __funnelshift_r(lo, hi, (t & 3) * 8);
+                }
+            }
+            q += blockDim.x;
+            while (q >= PW) {
+                q -= PW;
+                ++row;
+            }
+        }
+        __syncthreads();
+        // tasks (run, col) in raster order, walked incrementally (no division)
+        for (int run = tid / WX, col = tid - (tid / WX) * WX; run < bruns;) {
+            const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
+            uint32_t acc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = 0;
+#pragma unroll
+            for (int j = 0; j < K + BS - 1; ++j) {
+                uint32_t w[NW];
+#pragma unroll
+                for (int i = 0; i < NW; ++i) w[i] = base[j * PW + i];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int r = j - k;
+                    if (r >= 0 && r < BS) {
+#pragma unroll
+                        for (int i = 0; i < NW; ++i) acc[k] = vad4(c[r][i], w[i], acc[k]);
+                    }
+                }
+            }
+            // min over the run's K positions of (SAD, |dx|+|dy|, k) in 32 bits
+            // (SAD < 2^16, |dx|+|dy| <= 128, k < 8), then one 64-bit key
+            const int dx = lo_x + col;
+            const int ady = (run0 + run) * K;
+            const int adx = abs(dx);
+            uint32_t m32 = ~0u;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int wy = ady + k;  // window row index
+                const uint32_t man = uint32_t(adx + abs(lo_y + wy));
+                const uint32_t kk = (acc[k] << 11) | (man << 3) | uint32_t(k);
+                m32 = wy < WY ? min(m32, kk) : m32;
+            }
+            if (m32 != ~0u) {
+                const uint32_t wy = uint32_t(ady) + (m32 & 7u);
+                const unsigned long long key = (static_cast<unsigned long long>(m32 >> 11) << 40) |
+                                               (static_cast<unsigned long long>((m32 >> 3) & 0xFFu) << 24) |
+                                               static_cast<unsigned long long>(wy * uint32_t(WX) + uint32_t(col));
+                best = key < best ? key : best;
+            }
+            col += blockDim.x;
+            while (col >= WX) {
+                col -= WX;
+                ++run;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+        best = other < best ? other : best;
+    }
+    if (lane == 0) s_best[wid] = best;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long m = s_best[0];
+        for (int i = 1; i < int(blockDim.x >> 5); ++i) m = s_best[i] < m ? s_best[i] : m;
+        const int raster = int(m & 0xFFFFFF);
+        out_dx = lo_x + raster % WX;
+        out_dy = lo_y + raster / WX;
+        out_sad = uint32_t(m >> 40);
+        out_cmp = uint32_t(WX * WY);
+    }
+}
+
+template <int BS, int K>
+__global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ unsigned long long s_best[kEsThreads / 32];
+    __shared__ int s_item;
+    __shared__ int s_res[4];
+    const Batch& b = a.b;
+    const int n = *a.nlist;
+    const size_t plane = size_t(b.W) * b.H;
+    const int band_runs = a.band_rows_max / K;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= n) return;
+        int h, v, p, seq;
+        bool boundary;
+        const uint32_t g = decode_entry(b, a.list[item], h, v, p, seq, boundary);
+        const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
+        const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
+        int dx, dy;
+        uint32_t sad, cmp;
+        es_block<BS, K>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, s_best, dx, dy,
+                        sad, cmp);
+        if (threadIdx.x == 0) {
+            s_res[0] = dx;
+            s_res[1] = dy;
+            s_res[2] = int(sad);
+            s_res[3] = int(cmp);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // fused predict_frame + psnr SSE of this block at its vector
+            const int lane = threadIdx.x;
+            const int rdx = s_res[0], rdy = s_res[1];
+            uint32_t sse = lane < BS ? row_sse_fp(cur, ref, b.W, h * BS, v * BS + lane, BS, rdx, rdy) : 0u;
+            sse = __reduce_add_sync(0xFFFFFFFFu, sse);
+            if (lane == 0) {
+                const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+                write_rec(a.recs + g, 2 * rdx, 2 * rdy, uint32_t(s_res[2]) * 4u, uint32_t(s_res[3]), 0, 0,
+                          ty, false);
+                if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, uint32_t(s_res[3]), 0, ty);
+            }
+        }
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(kEsThreads) es_single_kernel(const uint8_t* cur, const uint8_t* ref,
+                                                               int W, int H, int x0, int y0, int S,
+                                                               int band_rows, int64_t* out) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ unsigned long long s_best[kEsThreads / 32];
+    int dx, dy;
+    uint32_t sad, cmp;
+    es_block<BS, 8>(cur, ref, W, H, x0, y0, S, band_rows / 8, sm, s_best, dx, dy, sad, cmp);
+    if (threadIdx.x == 0) {
+        out[0] = 2 * dx;
+        out[1] = 2 * dy;
+        out[2] = cmp;
+        out[3] = int64_t(sad) * 4;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+
+// dy rows of candidates staged per band (a multiple of K = 8): the whole
+// window when its 4 shifted copies fit in ~110 KB (one staging pass and one
+// flat task list per block, no partial band), else bands of 64 rows
+int es_band_rows(int bs, int S, int W, int H) {
+    const int WX = min(2 * S + 1, W - bs + 1), WY = min(2 * S + 1, H - bs + 1);
+    const int PW = ((WX - 1) >> 2) + (bs >> 2) + 1;
+    int rows = (WY + 7) / 8 * 8;
+    while (rows > 64 && size_t(4) * (size_t(rows + bs - 1) * PW + 32) * 4 > 110 * 1024) rows -= 8;
+    return rows;
+}
+
+size_t es_smem_bytes(int bs, int S, int W, int H) {
+    const int WX = min(2 * S + 1, W - bs + 1);
+    const int PW = ((WX - 1) >> 2) + (bs >> 2) + 1;
+    const int srows = es_band_rows(bs, S, W, H) + bs - 1;
+    return size_t(4) * (size_t(srows) * PW + 32) * 4;
+}
+
+cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist, int* counter,
+                      me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st) {
+    EsArgs ea;
+    ea.b = b;
+    ea.S = S;
+    ea.list = list;
+    ea.nlist = nlist;
+    ea.counter = counter;
+    ea.recs = recs;
+    ea.band_rows_max = es_band_rows(b.bs, S, b.W, b.H);
+    ea.stats = stats;
+    const size_t smem = es_smem_bytes(b.bs, S, b.W, b.H);
+    auto kern = b.bs == 16 ? es_kernel<16, 8> : es_kernel<8, 8>;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEsThreads, smem);
+    kern<<<num_sms * (occ > 0 ? occ : 1), kEsThreads, smem, st>>>(ea);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_es_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
+                             int size, int range, int64_t* out, cudaStream_t st) {
+    const size_t smem = es_smem_bytes(size, range, W, H);
+    auto kern = size == 16 ? es_single_kernel<16> : es_single_kernel<8>;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+    kern<<<1, kEsThreads, smem, st>>>(cur, ref, W, H, x0, y0, range, es_band_rows(size, range, W, H), out);
+    return cudaGetLastError();
+}
+
+}  // namespace mek

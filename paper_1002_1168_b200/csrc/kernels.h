@@ -1,4 +1,5 @@
-// kernels.h — host-side launchers for the sm_100a kernels in kernels.cu.
+// kernels.h — host-side launchers of the sm_100a kernels (wavefront.cu, es.cu,
+// ring.cu, pa.cu, frame_ops.cu; the pipeline in batch.cu).
 #pragma once
 
 #include <cuda_runtime.h>

@@ -1,0 +1,313 @@
+// wavefront.cu — classify_block on every block (fused transparent-block SSE
+// and the per-pair type counts), the per-step histogram, its scan and the
+// scatter that builds the wavefront-ordered work list.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+
+namespace mek {
+
+// ---------------------------------------------------------------------------
+// classify_kernel: classify_block (frame.cpp:81-104) on every block of every
+// pair's CURRENT alpha plane (estimators.cpp:411), initialise its record
+// (transparent: final all-zero record; estimated: MV = sentinel) and build the
+// histogram of estimated blocks over the sort key (PA: wavefront step
+// t = h + 2v + p; baselines: a single bin).
+// ---------------------------------------------------------------------------
+
+// SSE of a block predicted with the zero vector (transparent blocks,
+// compensation.cpp:45): cur block vs the co-located ref block.
+__device__ __forceinline__ uint32_t block_sse0(const uint8_t* cur, const uint8_t* ref, int W,
+                                               int x0, int y0, int bs) {
+    uint32_t s = 0;
+    for (int y = 0; y < bs; ++y) {
+        const size_t o = size_t(y0 + y) * W + x0;
+        for (int i = 0; i < bs; i += 8) {
+            const uint2 c = __ldg(reinterpret_cast<const uint2*>(cur + o + i));
+            const uint2 r = __ldg(reinterpret_cast<const uint2*>(ref + o + i));
+            s = sq4(c.x, r.x, s);
+            s = sq4(c.y, r.y, s);
+        }
+    }
+    return s;
+}
+
+// One thread classifies a 16-pixel-wide column strip of one block row (two
+// 8x8 blocks or one 16x16 block): every alpha, cur and ref row of the strip is
+// fetched with 16-byte loads in a single round (the luma is loaded
+// speculatively — it is only needed for transparent blocks' zero-vector SSE,
+// and is the compulsory read of those frames anyway).
+template <int BS>
+__global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
+    extern __shared__ int s_hist[];
+    constexpr int NB = 16 / BS;  // blocks per strip
+    const Batch& b = a.b;
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const int strips = b.cols / NB;  // strips per block row
+    const int64_t n = int64_t(b.n_seq) * b.pairs * b.rows * strips;
+    const size_t plane = size_t(b.W) * b.H;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    // uniform trip count so whole warps reach the warp-level reductions
+    for (int64_t s0 = int64_t(blockIdx.x) * blockDim.x; s0 < n; s0 += stride) {
+        const int64_t si = s0 + threadIdx.x;
+        uint32_t sse = 0, n_t = 0, n_o = 0, n_b = 0;
+        int64_t gp = -1;
+        if (si < n) {
+            const int hs = int(si % strips);
+            int64_t t = si / strips;
+            const int v = int(t % b.rows);
+            gp = t / b.rows;  // seq * pairs + p
+            const int p = int(gp % b.pairs);
+            const int seq = int(gp / b.pairs);
+            const size_t fcur = size_t(seq) * b.F + p + b.d, fref = size_t(seq) * b.F + p;
+            const size_t off = size_t(v * BS) * b.W + size_t(hs) * 16;
+            const uint8_t* ac = b.alpha ? b.alpha + fcur * plane + off : nullptr;
+            const uint8_t* cc = b.luma + fcur * plane + off;
+            const uint8_t* rc = b.luma + fref * plane + off;
+            uint4 al[BS], cu[BS], re[BS];
+#pragma unroll
+            for (int y = 0; y < BS; ++y) {
+                al[y] = ac ? __ldg(reinterpret_cast<const uint4*>(ac + size_t(y) * b.W)) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                if (a.stats) {
+                    cu[y] = __ldg(reinterpret_cast<const uint4*>(cc + size_t(y) * b.W));
+                    re[y] = __ldg(reinterpret_cast<const uint4*>(rc + size_t(y) * b.W));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                // classify_block (frame.cpp:81-104): any sample set / all set
+                uint32_t any = 0, nz = 1, s = 0;
+#pragma unroll
+                for (int y = 0; y < BS; ++y) {
+                    const uint32_t w0 = NB == 2 ? (k ? al[y].z : al[y].x) : al[y].x;
+                    const uint32_t w1 = NB == 2 ? (k ? al[y].w : al[y].y) : al[y].y;
+                    any |= w0 | w1;
+                    nz &= (__vcmpeq4(w0, 0u) | __vcmpeq4(w1, 0u)) == 0u;
+                    if (NB == 1) {
+                        any |= al[y].z | al[y].w;
+                        nz &= (__vcmpeq4(al[y].z, 0u) | __vcmpeq4(al[y].w, 0u)) == 0u;
+                    }
+                    if (a.stats) {
+                        if (NB == 2) {
+                            s = sq4(k ? cu[y].z : cu[y].x, k ? re[y].z : re[y].x, s);
+                            s = sq4(k ? cu[y].w : cu[y].y, k ? re[y].w : re[y].y, s);
+                        } else {
+                            s = sq4(cu[y].x, re[y].x, s);
+                            s = sq4(cu[y].y, re[y].y, s);
+                            s = sq4(cu[y].z, re[y].z, s);
+                            s = sq4(cu[y].w, re[y].w, s);
+                        }
+                    }
+                }
+                const int ty = !any ? ME_TRANSPARENT : (nz ? ME_OPAQUE : ME_BOUNDARY);
+                const int h = hs * NB + k;
+                const int64_t g = (gp * b.rows + v) * b.cols + h;
+                a.types[g] = uint8_t(ty);
+                uint4 r;
+                r.x = ty == ME_TRANSPARENT ? 0u : kSentinel;
+                r.y = 0u;
+                r.z = 0u;
+                r.w = uint32_t(ty) << 8;
+                *reinterpret_cast<uint4*>(a.recs + g) = r;
+                if (ty != ME_TRANSPARENT) {
+                    atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
+                    n_o += ty == ME_OPAQUE;
+                    n_b += ty == ME_BOUNDARY;
+                } else {
+                    sse += s;
+                    n_t += 1;
+                }
+            }
+        }
+        if (a.stats) {
+            const int64_t gp0 = __shfl_sync(0xFFFFFFFFu, gp, 0);
+            const bool uniform = __all_sync(0xFFFFFFFFu, gp == gp0 || gp < 0);
+            if (!a.pa) n_o = n_b = 0;  // the other searches count their own blocks
+            if (uniform) {
+                const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, sse);
+                const uint32_t wn = __reduce_add_sync(0xFFFFFFFFu, n_t);
+                const uint32_t wo = __reduce_add_sync(0xFFFFFFFFu, n_o);
+                const uint32_t wb = __reduce_add_sync(0xFFFFFFFFu, n_b);
+                if (lane == 0) {
+                    unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp0);
+                    if (ws) red_add_u64(st + 5, ws);
+                    if (wn) red_add_u64(st + 4, wn);
+                    if (wo) red_add_u64(st + 2, wo);
+                    if (wb) red_add_u64(st + 3, wb);
+                    if (wo + wb) red_add_u64(st + 0, 4ull * (wo + wb));  // brs_select: 4 per block (:290)
+                }
+            } else if (gp >= 0) {
+                unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats + gp);
+                if (sse) red_add_u64(st + 5, sse);
+                if (n_t) red_add_u64(st + 4, n_t);
+                if (n_o) red_add_u64(st + 2, n_o);
+                if (n_b) red_add_u64(st + 3, n_b);
+                if (n_o + n_b) red_add_u64(st + 0, 4ull * (n_o + n_b));
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
+}
+
+// Exclusive scan of hist into offs[0..nbins] (single CTA), cursor = offs.
+// ranges (optional): the list split at the first and after the last step
+// holding >= wide blocks: {0, b1}, {b1, b2}, {b2, total} (narrow, wide, narrow).
+__global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
+                            uint2* list, int wide, int* ranges) {
+    __shared__ int s_part[1024];
+    __shared__ int s_lo, s_hi;  // first / last wide step
+    const int T = blockDim.x;
+    const int per = (nbins + T - 1) / T;
+    const int lo = threadIdx.x * per, hi = min(lo + per, nbins);
+    auto padded = [&](int v) { return (v + pad - 1) / pad * pad; };
+    if (threadIdx.x == 0) {
+        s_lo = nbins;
+        s_hi = -1;
+    }
+    __syncthreads();
+    int sum = 0, my_lo = nbins, my_hi = -1;
+    for (int i = lo; i < hi; ++i) {
+        sum += padded(hist[i]);
+        if (hist[i] >= wide) {
+            my_lo = min(my_lo, i);
+            my_hi = max(my_hi, i);
+        }
+    }
+    s_part[threadIdx.x] = sum;
+    if (ranges && my_hi >= 0) {
+        atomicMin(&s_lo, my_lo);
+        atomicMax(&s_hi, my_hi);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int i = 0; i < T; ++i) {
+            const int v = s_part[i];
+            s_part[i] = acc;
+            acc += v;
+        }
+        offs[nbins] = acc;
+    }
+    __syncthreads();
+    int acc = s_part[threadIdx.x];
+    for (int i = lo; i < hi; ++i) {
+        offs[i] = acc;
+        cursor[i * kCursorStride] = acc;
+        for (int k = hist[i]; k < padded(hist[i]); ++k) list[acc + k] = make_uint2(kInvalidEntry, kInvalidEntry);
+        acc += padded(hist[i]);
+    }
+    if (ranges) {
+        __syncthreads();  // offs[] complete
+        if (threadIdx.x == 0) {
+            const int total = offs[nbins];
+            const int b1 = s_hi >= 0 ? offs[s_lo] : total, b2 = s_hi >= 0 ? offs[s_hi + 1] : total;
+            ranges[0] = 0;
+            ranges[1] = b1;
+            ranges[2] = b1;
+            ranges[3] = b2;
+            ranges[4] = b2;
+            ranges[5] = total;
+        }
+    }
+}
+
+// Scatter estimated block ids into key order (per-CTA ranges per bin keep the
+// global atomics to one per (CTA, bin)).
+
+// Scatter estimated blocks into key order as decoded list entries
+// {h | v << 16 | boundary << 31, p | seq << 16} (per-CTA ranges per bin keep
+// the global atomics to one per (CTA, bin)).
+// One CTA per rows_per_cta block rows (32-bit index math): count into a shared
+// histogram, reserve each bin's range with one global atomic per (CTA, bin),
+// then scatter.
+
+__global__ void __launch_bounds__(256) fill_kernel(ClassArgs a, int* cursor, uint2* list, uint32_t rows_per_cta) {
+    extern __shared__ int s_cnt[];  // [nbins] counts, then [nbins] bases
+    int* s_base = s_cnt + a.nbins;
+    const Batch& b = a.b;
+    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    const uint32_t nrows = uint32_t(b.n_seq) * uint32_t(b.pairs) * uint32_t(b.rows);
+    const uint32_t r0 = blockIdx.x * rows_per_cta, r1 = min(r0 + rows_per_cta, nrows);
+    const uint32_t cols = uint32_t(b.cols), items = (r1 - r0) * cols;
+    const uint8_t* types = a.types + size_t(r0) * cols;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (uint32_t i = threadIdx.x; i < items; i += blockDim.x) {
+            const int ty = types[i];
+            if (ty == ME_TRANSPARENT) continue;
+            const uint32_t r = r0 + i / cols, h = i - (i / cols) * cols;
+            const uint32_t pr = r / uint32_t(b.rows), v = r - pr * uint32_t(b.rows);
+            const uint32_t seq = pr / uint32_t(b.pairs), p = pr - seq * uint32_t(b.pairs);
+            {
+                const int key = a.pa ? a.key_a * int(h + 2 * v + p) + a.key_s * int(seq) : 0;
+                if (pass == 0) {
+                    atomicAdd(&s_cnt[key], 1);
+                } else {
+                    const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
+                    list[pos] = make_uint2(uint32_t(h) | (v << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u), p | (seq << 16));
+                }
+            }
+        }
+        __syncthreads();
+        if (pass == 0) {
+            for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) {
+                s_base[i] = s_cnt[i] ? atomicAdd(&cursor[i * kCursorStride], s_cnt[i]) : 0;
+                s_cnt[i] = 0;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+
+cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
+    const Batch& b = ca.b;
+    const int threads = 256;
+    // a 16-pixel strip per thread: two 8x8 blocks or one 16x16 block (W % 16 == 0)
+    const int64_t strips = b.nblocks() / (16 / b.bs);
+    int grid = int(std::min<int64_t>((strips + threads - 1) / threads, int64_t(num_sms) * 8));
+    if (grid < 1) grid = 1;
+    const size_t hist_smem = size_t(ca.nbins) * 4;
+    if (b.bs == 8)
+        classify_kernel<8><<<grid, threads, hist_smem, st>>>(ca);
+    else
+        classify_kernel<16><<<grid, threads, hist_smem, st>>>(ca);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
+                        int wide, int* ranges, cudaStream_t st) {
+    scan_kernel<<<1, 1024, 0, st>>>(hist, nbins, pad, offs, cursor, list, wide, ranges);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st) {
+    const Batch& b = ca.b;
+    // <= 128 rows per CTA (fewer global atomics), >= 2 CTAs per SM
+    const int64_t nrows = int64_t(b.n_seq) * b.pairs * b.rows;
+    const int64_t rpc = std::max<int64_t>(4, std::min<int64_t>(128, nrows / (2 * num_sms)));
+    const int grid = int((nrows + rpc - 1) / rpc);
+    const size_t smem = 2 * size_t(ca.nbins) * 4;
+    cudaError_t e;
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
+        return e;
+    fill_kernel<<<grid, 256, smem, st>>>(ca, cursor, list, uint32_t(rpc));
+    return cudaGetLastError();
+}
+
+}  // namespace mek
