@@ -84,7 +84,8 @@ size_t scratch_bytes(const Batch& b, int algo) {
 
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
-                      size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events) {
+                      size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events,
+                      bool prev0_integer) {
     const int algo = cfg.algo;
     const bool pa = algo == ME_ALGO_PA;
     const int nbins = pa ? pa_bins(b) : 1;
@@ -115,7 +116,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     // PA kernel choice (pa.cu): the duo kernel takes list entries in pairs, so
     // every wavefront step is padded to an even count; the hybrid splits the
     // list into narrow / wide / narrow step ranges.
-    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, num_sms) : 0;
+    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, prev0_integer, num_sms) : 0;
     int* ranges = pa_mode == 3 ? s.counter + 8 : nullptr;
     if ((e = launch_scan(s.hist, nbins, pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
                          pa_wide_threshold(num_sms), ranges, st)))

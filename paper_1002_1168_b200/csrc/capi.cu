@@ -451,6 +451,9 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
         }
     }
     int32_t* prev_dev = nullptr;
+    bool prev_integer = true;  // integer-pel prev fields can take the fast PA kernels
+    if (prev_mv)
+        for (size_t i = 0; i < size_t(cols) * rows * 2 && prev_integer; ++i) prev_integer = (prev_mv[i] & 1) == 0;
     if (prev_mv) {
         prev_dev = static_cast<int32_t*>(ctx->aux.p);
         ME_CUDA(cudaMemcpyAsync(prev_dev, prev_mv, size_t(cols) * rows * 8, cudaMemcpyHostToDevice,
@@ -460,7 +463,7 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
     ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
     ME_CUDA(mek::run_batch(b, c1, prev_dev, static_cast<me_block_rec*>(ctx->out_recs.p),
                            static_cast<me_pair_stats*>(ctx->out_stats.p), nullptr, ctx->tasks.p,
-                           ctx->tasks.cap, ctx->num_sms, ctx->stream));
+                           ctx->tasks.cap, ctx->num_sms, ctx->stream, nullptr, prev_integer));
     ME_CUDA(cudaMemcpyAsync(recs, ctx->out_recs.p, size_t(cols) * rows * sizeof(me_block_rec),
                             cudaMemcpyDeviceToHost, ctx->stream));
     ME_CUDA(cudaMemcpyAsync(stats, ctx->out_stats.p, sizeof(me_pair_stats), cudaMemcpyDeviceToHost,

@@ -29,10 +29,12 @@ size_t scratch_bytes(const Batch& b, int algo);
 // entries; pred is nullable.
 // `events` (nullable) = 5 events recorded before classify, before the sort,
 // before the search, before MC+PSNR and at the end.
+// `prev0_integer`: every prev0 vector is integer-pel (even), which lets the
+// fast PA kernels take it.
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
                       size_t scratch_size, int num_sms, cudaStream_t st,
-                      cudaEvent_t* events = nullptr);
+                      cudaEvent_t* events = nullptr, bool prev0_integer = false);
 
 // Single-block entry points (all pointers device pointers; outputs in `out`,
 // an int64 array whose layout is documented at each launcher).

@@ -635,8 +635,8 @@ __global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
 // block staged once in shared memory, 16-byte-chunk patch staging (two lanes
 // per patch row), lazy PRS on the staged patch.  Same algorithm and
 // dependency protocol as pa_kernel.  All candidates are integer-pel: A, B, C
-// and T come from this integer-pel search (no external prev field, which may
-// be half-pel and is routed to pa_kernel).
+// and T come from this integer-pel search or from an external prev field the
+// host checked to be integer-pel (a half-pel one is routed to pa_kernel).
 // ---------------------------------------------------------------------------
 
 constexpr int kFastPR = 16;        // patch rows (8 + 2R)
@@ -704,6 +704,10 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             if (lane == 3 && p > 0) back = int(rows * cols);
             const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
             if (back >= 0) mvw = ld_relaxed(src);
+            if (lane == 3 && p == 0 && a.prev0) {  // pair 0: T from the external (integer-pel) field
+                const int i = v * int(cols) + h;
+                mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+            }
             // warp-uniform wait (a vote per poll keeps the warp converged)
             while (__any_sync(0xFFFFFFFFu, back >= 0 && mvw == kSentinel)) {
                 __nanosleep(a.poll_ns);
@@ -951,6 +955,10 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             if (act && hl == 3 && p > 0) back = int(rows * cols);
             const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
             if (back >= 0) mvw = ld_relaxed(src);
+            if (act && hl == 3 && p == 0 && a.prev0) {  // pair 0: T from the external (integer-pel) field
+                const int i = v * int(cols) + h;
+                mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+            }
             // B lies two wavefront steps back and is usually final already: its
             // patch (slot 1) goes out before the wait for A, C and T
             const uint32_t mb = __shfl_sync(FULL, mvw, hb + 1);
@@ -1290,9 +1298,10 @@ int pa_wide_threshold(int num_sms) {
     return e ? atoi(e) : num_sms * 40;  // measured: 3000-9000 within 1 %, duo-only 3 % slower
 }
 
-int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, int num_sms) {
+int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
+                   int num_sms) {
     const int step = cfg.halfpel ? 1 : cfg.step;
-    const bool fast = b.bs == 8 && step == 2 && cfg.max_iterations <= 4 && !prev0 &&
+    const bool fast = b.bs == 8 && step == 2 && cfg.max_iterations <= 4 && (!prev0 || prev0_integer) &&
                       size_t(b.n_seq) * b.F * b.W * b.H < (size_t(1) << 32);
     const char* mode = getenv("ME_PA_MODE");
     if (!fast || (mode && std::string(mode) == "warp")) return 0;

@@ -227,3 +227,20 @@ def test_host_path_mask_packing(me_gpu, port, levels):
         want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
         assert_recs(recs[i], want_r, f"seq {i}")
         assert np.array_equal(stats[i], want_s)
+
+
+@pytest.mark.parametrize("odd", [False, True])
+def test_estimate_field_random_prev(me_gpu, port, odd):
+    """External prev fields: integer-pel ones take the fast PA kernels, a
+    half-pel one the generic kernel; both bit-exact."""
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config_sequence(1, 77, 4)
+    rng = np.random.default_rng(3 + odd)
+    prev = rng.integers(-12, 13, size=(22 * 18, 2)).astype(np.int32)
+    prev = prev | 1 if odd else prev & ~1
+    pf = me_gpu.MotionField(22, 18, 8, vectors=prev.copy())
+    f, st, recs = me_gpu.estimate_field(me_gpu.Algo.PA, luma[2], luma[0], alpha[2], alpha[0], pf,
+                                        me_gpu.SearchConfig(search_range=16, block_size=8), me_gpu.PrsConfig(), return_records=True)
+    want, wst = port.estimate_field(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[2], luma[0], alpha[2], alpha[0], prev_mv=prev)
+    assert_recs(recs, want)
