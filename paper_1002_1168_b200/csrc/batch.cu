@@ -88,6 +88,21 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
                       bool prev0_integer) {
     const int algo = cfg.algo;
     const bool pa = algo == ME_ALGO_PA;
+    if (pa) {  // one small pair: the whole pipeline in one shared-memory-resident CTA
+        if (events)
+            for (int i = 0; i < 3; ++i) cudaEventRecord(events[i], st);
+        const cudaError_t e0 = launch_pa_smem(b, cfg, prev0, prev0_integer, recs, stats, st);
+        if (e0 == cudaSuccess) {
+            if (events) cudaEventRecord(events[3], st);
+            if (pred) {
+                const cudaError_t e1 = launch_mc_pred(b, recs, pred, st);
+                if (e1) return e1;
+            }
+            if (events) cudaEventRecord(events[4], st);
+            return cudaGetLastError();
+        }
+        if (e0 != cudaErrorNotSupported) return e0;
+    }
     const int nbins = pa ? pa_bins(b) : 1;
     if (scratch_size < scratch_bytes(b, algo)) return cudaErrorInvalidValue;
     Scratch s = carve(b, nbins, scratch);

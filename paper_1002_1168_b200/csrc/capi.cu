@@ -123,20 +123,23 @@ me_status sync(me_ctx* ctx) {
 
 // Stages up to 4 host planes of n bytes each into ctx->in_luma (contiguous,
 // 16-byte padded slots); returns device pointers (null for null inputs).
+// The planes are gathered into pinned staging memory (zero padded) and cross
+// PCIe in ONE copy: separate copies from pageable memory cost ~10 us each,
+// more than the per-block kernels themselves.  Every entry point synchronises
+// before returning, so the staging buffer is free again on the next call.
 me_status stage_planes(me_ctx* ctx, size_t n, const uint8_t* const* host, const uint8_t** dev,
                        int count) {
     const size_t slot = pad16(n) + 256;
     ME_CUDA(ctx->in_luma.reserve(slot * count));
-    ME_CUDA(cudaMemsetAsync(ctx->in_luma.p, 0, slot * count, ctx->stream));
+    ME_CUDA(ctx->pin_a.reserve(slot * count));
+    uint8_t* hs = static_cast<uint8_t*>(ctx->pin_a.p);
     for (int i = 0; i < count; ++i) {
-        if (!host[i]) {
-            dev[i] = nullptr;
-            continue;
-        }
-        me_status s = upload(ctx, ctx->in_luma, slot * i, host[i], n);
-        if (s) return s;
-        dev[i] = static_cast<const uint8_t*>(ctx->in_luma.p) + slot * i;
+        uint8_t* d = hs + slot * i;
+        if (host[i]) std::memcpy(d, host[i], n);
+        std::memset(d + (host[i] ? n : 0), 0, slot - (host[i] ? n : 0));
+        dev[i] = host[i] ? static_cast<const uint8_t*>(ctx->in_luma.p) + slot * i : nullptr;
     }
+    ME_CUDA(cudaMemcpyAsync(ctx->in_luma.p, hs, slot * count, cudaMemcpyHostToDevice, ctx->stream));
     return ME_OK;
 }
 
@@ -417,25 +420,33 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
     // frame 0 = ref, frame 1 = cur (one pair at ref_distance 1)
     me_config c1 = *cfg;
     c1.ref_distance = 1;
-    const size_t slot = pad16(plane) + 256;
-    ME_CUDA(ctx->in_luma.reserve(2 * slot));
-    ME_CUDA(ctx->in_alpha.reserve(2 * slot));
-    ME_CUDA(ctx->out_recs.reserve(size_t(cols) * rows * sizeof(me_block_rec)));
-    ME_CUDA(ctx->out_stats.reserve(sizeof(me_pair_stats)));
-    ME_CUDA(ctx->aux.reserve(size_t(cols) * rows * 8 + 256));
-    uint8_t* L = static_cast<uint8_t*>(ctx->in_luma.p);
-    uint8_t* A = static_cast<uint8_t*>(ctx->in_alpha.p);
+    // one pinned staging buffer -> one H2D: [ref, cur, ref alpha, cur alpha, prev]
+    const size_t prev_bytes = prev_mv ? size_t(cols) * rows * 8 : 0;
+    const size_t total = (cur_alpha ? 4 : 2) * plane + prev_bytes;
+    const size_t out_bytes = size_t(cols) * rows * sizeof(me_block_rec) + sizeof(me_pair_stats);
+    ME_CUDA(ctx->in_luma.reserve(total + 256));
+    ME_CUDA(ctx->out_recs.reserve(out_bytes));
+    ME_CUDA(ctx->aux.reserve(size_t(cols) * rows + 256));
+    ME_CUDA(ctx->pin_a.reserve(total + 256));
+    ME_CUDA(ctx->pin_b.reserve(out_bytes));
     // the batch layout expects frames back to back; pad-free when plane % 16 == 0
     if (plane % 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "frame area must be a multiple of 16");
-    ME_CUDA(cudaMemcpyAsync(L, ref, plane, cudaMemcpyHostToDevice, ctx->stream));
-    ME_CUDA(cudaMemcpyAsync(L + plane, cur, plane, cudaMemcpyHostToDevice, ctx->stream));
-    const uint8_t* alpha_dev = nullptr;
+    uint8_t* hs = static_cast<uint8_t*>(ctx->pin_a.p);
+    std::memcpy(hs, ref, plane);
+    std::memcpy(hs + plane, cur, plane);
     if (cur_alpha) {
         if (ref_alpha)
-            ME_CUDA(cudaMemcpyAsync(A, ref_alpha, plane, cudaMemcpyHostToDevice, ctx->stream));
+            std::memcpy(hs + 2 * plane, ref_alpha, plane);
         else
-            ME_CUDA(cudaMemsetAsync(A, 0, plane, ctx->stream));
-        ME_CUDA(cudaMemcpyAsync(A + plane, cur_alpha, plane, cudaMemcpyHostToDevice, ctx->stream));
+            std::memset(hs + 2 * plane, 0, plane);
+        std::memcpy(hs + 3 * plane, cur_alpha, plane);
+    }
+    if (prev_mv) std::memcpy(hs + total - prev_bytes, prev_mv, prev_bytes);
+    ME_CUDA(cudaMemcpyAsync(ctx->in_luma.p, hs, total, cudaMemcpyHostToDevice, ctx->stream));
+    uint8_t* L = static_cast<uint8_t*>(ctx->in_luma.p);
+    uint8_t* A = L + 2 * plane;
+    const uint8_t* alpha_dev = nullptr;
+    if (cur_alpha) {
         alpha_dev = A;
         if (!ref_alpha && cfg->algo == ME_ALGO_PA) {
             // brs_select throws on a boundary block without both planes
@@ -450,26 +461,24 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
                     return me_fail(ME_ERR_INVALID_ARGUMENT, "boundary block requires both alpha planes");
         }
     }
-    int32_t* prev_dev = nullptr;
+    int32_t* prev_dev = prev_mv ? reinterpret_cast<int32_t*>(L + total - prev_bytes) : nullptr;
     bool prev_integer = true;  // integer-pel prev fields can take the fast PA kernels
     if (prev_mv)
         for (size_t i = 0; i < size_t(cols) * rows * 2 && prev_integer; ++i) prev_integer = (prev_mv[i] & 1) == 0;
-    if (prev_mv) {
-        prev_dev = static_cast<int32_t*>(ctx->aux.p);
-        ME_CUDA(cudaMemcpyAsync(prev_dev, prev_mv, size_t(cols) * rows * 8, cudaMemcpyHostToDevice,
-                                ctx->stream));
-    }
     const mek::Batch b = make_batch(&c1, 1, 2, W, H, L, alpha_dev);
     ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
-    ME_CUDA(mek::run_batch(b, c1, prev_dev, static_cast<me_block_rec*>(ctx->out_recs.p),
-                           static_cast<me_pair_stats*>(ctx->out_stats.p), nullptr, ctx->tasks.p,
-                           ctx->tasks.cap, ctx->num_sms, ctx->stream, nullptr, prev_integer));
-    ME_CUDA(cudaMemcpyAsync(recs, ctx->out_recs.p, size_t(cols) * rows * sizeof(me_block_rec),
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    ME_CUDA(cudaMemcpyAsync(stats, ctx->out_stats.p, sizeof(me_pair_stats), cudaMemcpyDeviceToHost,
-                            ctx->stream));
+    // records and stats in one device buffer -> one D2H into pinned memory
+    me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
+    me_pair_stats* ds = reinterpret_cast<me_pair_stats*>(dr + size_t(cols) * rows);
+    ME_CUDA(mek::run_batch(b, c1, prev_dev, dr, ds, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
+                           ctx->stream, nullptr, prev_integer));
+    ME_CUDA(cudaMemcpyAsync(ctx->pin_b.p, dr, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     s = sync(ctx);
-    return s ? s : ok();
+    if (s) return s;
+    std::memcpy(recs, ctx->pin_b.p, size_t(cols) * rows * sizeof(me_block_rec));
+    std::memcpy(stats, static_cast<uint8_t*>(ctx->pin_b.p) + size_t(cols) * rows * sizeof(me_block_rec),
+                sizeof(me_pair_stats));
+    return ok();
 }
 
 me_status me_b200_block_search(me_ctx* ctx, int algo, int W, int H, const uint8_t* cur,

@@ -1265,6 +1265,271 @@ __global__ void prs_update_kernel(const uint8_t* cur, const uint8_t* ref, int W,
 }
 
 // ---------------------------------------------------------------------------
+// pa_smem_kernel: one small frame pair (estimate_field on e.g. QCIF) in ONE
+// CTA with both frames (and alpha planes) resident in shared memory.  The
+// wavefront steps t = h + 2v are separated by __syncthreads instead of
+// global-memory dependency polls, candidates come from a shared MV array and
+// every pixel read is a shared-memory load, so a step costs one block's
+// compute instead of a global round trip plus compute.  Same algorithm and
+// results as the batched kernels (classify + BRS + PRS + fused SSE); the
+// per-pair API's latency path.
+// ---------------------------------------------------------------------------
+
+// 8 bytes at byte offset x of a shared-memory row (4-byte aligned row start)
+__device__ __forceinline__ void srow8(const uint8_t* row, int x, uint32_t& r0, uint32_t& r1) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (x >> 2);
+    const uint32_t sh = uint32_t(x & 3) * 8;
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+    r0 = __funnelshift_r(w0, w1, sh);
+    r1 = __funnelshift_r(w1, w2, sh);
+}
+
+struct PaSmemArgs {
+    Batch b;  // n_seq = 1, one pair (frame 0 = ref, frame 1 = cur)
+    PaParams P;
+    const int32_t* prev0;  // integer-pel T candidates or null
+    me_block_rec* recs;
+    me_pair_stats* stats;
+    int plane_pad;  // bytes per staged plane (plane + 16)
+};
+
+__global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
+    extern __shared__ __align__(16) uint8_t s_frames[];
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    __shared__ unsigned long long s_sse, s_dpd;
+    __shared__ unsigned s_cnt[3];  // opaque, boundary, transparent
+    const Batch& b = a.b;
+    const int W = b.W, H = b.H, S = a.P.S, cols = b.cols, rows = b.rows;
+    const int plane = W * H, pp = a.plane_pad;
+    const bool has_alpha = b.alpha != nullptr;
+    uint8_t* s_ref = s_frames;
+    uint8_t* s_cur = s_ref + pp;
+    uint8_t* s_ra = s_cur + pp;  // alpha planes only when present
+    uint8_t* s_ca = s_ra + pp;
+    uint32_t* s_mv = reinterpret_cast<uint32_t*>(s_frames + (has_alpha ? 4 : 2) * size_t(pp));
+    uint8_t* s_type = reinterpret_cast<uint8_t*>(s_mv + cols * rows);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    // stage the planes (16-byte copies) and clear the MV words
+    {
+        const uint4* g = reinterpret_cast<const uint4*>(b.luma);
+        for (int i = tid; i < 2 * plane / 16; i += blockDim.x) {
+            const int f = i / (plane / 16), o = i - f * (plane / 16);
+            reinterpret_cast<uint4*>(s_frames + f * size_t(pp))[o] = __ldg(g + i);
+        }
+        if (has_alpha) {
+            const uint4* ga = reinterpret_cast<const uint4*>(b.alpha);
+            for (int i = tid; i < 2 * plane / 16; i += blockDim.x) {
+                const int f = i / (plane / 16), o = i - f * (plane / 16);
+                reinterpret_cast<uint4*>(s_ra + f * size_t(pp))[o] = __ldg(ga + i);
+            }
+        }
+        for (int i = tid; i < cols * rows; i += blockDim.x) s_mv[i] = 0u;
+        if (tid == 0) {
+            s_sse = s_dpd = 0ull;
+            s_cnt[0] = s_cnt[1] = s_cnt[2] = 0u;
+        }
+    }
+    __syncthreads();
+    unsigned long long my_sse = 0, my_dpd = 0;
+    unsigned my_cnt[3] = {0u, 0u, 0u};
+    // phase 1: classify every block (cur alpha, frame.cpp:81-104); transparent
+    // blocks are final here (MV 0, SSE at the zero vector)
+    for (int g = wid; g < cols * rows; g += nw) {
+        const int h = g % cols, v = g / cols, x0 = h * 8, y0 = v * 8;
+        int ty = ME_OPAQUE;
+        if (has_alpha) {
+            uint32_t r0 = 0, r1 = 0;
+            if (lane < 8) {
+                const uint2 w = *reinterpret_cast<const uint2*>(s_ca + (y0 + lane) * W + x0);
+                r0 = w.x;
+                r1 = w.y;
+            }
+            const bool any = __any_sync(FULL, (r0 | r1) != 0u);
+            const bool allnz = __all_sync(FULL, lane >= 8 || (__vcmpeq4(r0, 0u) | __vcmpeq4(r1, 0u)) == 0u);
+            ty = !any ? ME_TRANSPARENT : (allnz ? ME_OPAQUE : ME_BOUNDARY);
+        }
+        if (lane == 0) s_type[g] = uint8_t(ty);
+        if (ty == ME_TRANSPARENT) {
+            uint32_t se = 0;
+            if (lane < 8) {
+                const uint2 c = *reinterpret_cast<const uint2*>(s_cur + (y0 + lane) * W + x0);
+                const uint2 r = *reinterpret_cast<const uint2*>(s_ref + (y0 + lane) * W + x0);
+                se = sq4(c.y, r.y, sq4(c.x, r.x, 0u));
+            }
+            se = __reduce_add_sync(FULL, se);
+            if (lane == 0) {
+                write_rec(a.recs + g, 0, 0, 0u, 0u, 0u, 0u, ME_TRANSPARENT, false);
+                my_sse += se;
+                ++my_cnt[2];
+            }
+        }
+    }
+    __syncthreads();
+    // phase 2: the wavefront, one step per barrier
+    const int c = lane >> 3, sub = lane & 7;  // BRS: candidate c, row sub
+    const int k = lane >> 2, q = lane & 3;    // PRS: neighbour k, rows q and q + 4
+    const int kx = off8x(k), ky = off8y(k);
+    const int nsteps = (cols - 1) + 2 * (rows - 1) + 1;
+    for (int t = 0; t < nsteps; ++t) {
+        const int vmin = max(0, (t - (cols - 1) + 1) / 2), vmax = min(rows - 1, t / 2);
+        for (int i = wid; i <= vmax - vmin; i += nw) {
+            const int v = vmin + i, h = t - 2 * v, g = v * cols + h;
+            const int ty = s_type[g];
+            if (ty == ME_TRANSPARENT) continue;  // warp-uniform
+            const bool boundary = ty == ME_BOUNDARY;
+            const int x0 = h * 8, y0 = v * 8;
+            const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
+            const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
+            // gather_candidates (estimators.cpp:238-255): A, B, C, T
+            uint32_t mw = 0;
+            if (c == 0 && h > 0) mw = s_mv[g - 1];
+            if (c == 1 && v > 0) mw = s_mv[g - cols];
+            if (c == 2 && v > 0 && h + 1 < cols) mw = s_mv[g - cols + 1];
+            if (c == 3 && a.prev0) mw = pack_mv(a.prev0[2 * g], a.prev0[2 * g + 1]);
+            const int myx = clip_comp(mv_dx(mw), lo_x, hi_x), myy = clip_comp(mv_dy(mw), lo_y, hi_y);
+            // brs_select (estimators.cpp:257-301): row `sub` of candidate c
+            uint32_t s;
+            const int ry = y0 + sub + (myy >> 1), rx = x0 + (myx >> 1);
+            if (boundary && (c < 3 || a.P.bt_shape)) {
+                const uint2 ca = *reinterpret_cast<const uint2*>(s_ca + (y0 + sub) * W + x0);
+                uint32_t r0, r1;
+                srow8(s_ra + ry * W, rx, r0, r1);
+                s = ((__popc(__vcmpne4(ca.x, r0)) + __popc(__vcmpne4(ca.y, r1))) >> 3) * (255u * 4u);
+            } else {
+                const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + sub) * W + x0);
+                uint32_t r0, r1;
+                srow8(s_ref + ry * W, rx, r0, r1);
+                s = vad4(cr.y, r1, vad4(cr.x, r0, 0u)) * 4u;
+            }
+            s += __shfl_xor_sync(FULL, s, 1);
+            s += __shfl_xor_sync(FULL, s, 2);
+            s += __shfl_xor_sync(FULL, s, 4);
+            uint32_t best = __shfl_sync(FULL, s, 0);
+            int win = 0;
+#pragma unroll
+            for (int j = 1; j < 4; ++j) {
+                const uint32_t sj = __shfl_sync(FULL, s, 8 * j);
+                if (sj < best) {  // strict <: A, B, C, T tie order (:295)
+                    best = sj;
+                    win = j;
+                }
+            }
+            const int wx = __shfl_sync(FULL, myx, 8 * win), wy = __shfl_sync(FULL, myy, 8 * win);
+            // my two PRS rows of the block
+            const uint2 ca_ = *reinterpret_cast<const uint2*>(s_cur + (y0 + q) * W + x0);
+            const uint2 cb_ = *reinterpret_cast<const uint2*>(s_cur + (y0 + q + 4) * W + x0);
+            uint32_t ccost = best;
+            if (boundary && (win < 3 || a.P.bt_shape)) {  // the centre's texture cost
+                uint32_t tsum = 0;
+                if (lane < 8) {
+                    const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + lane) * W + x0);
+                    uint32_t r0, r1;
+                    srow8(s_ref + (y0 + lane + (wy >> 1)) * W, x0 + (wx >> 1), r0, r1);
+                    tsum = vad4(cr.y, r1, vad4(cr.x, r0, 0u));
+                }
+                ccost = 4u * __reduce_add_sync(FULL, tsum);
+            }
+            // prs_refine (estimators.cpp:311-382); unique evaluations: a neighbour
+            // is new iff it is at Chebyshev distance >= 2 from every earlier centre
+            int ci = 0, cj = 0, pc0 = 0, pc1 = 0, pc2 = 0;
+            uint32_t dpd = 1, iters = 0;
+            for (int it = 0; it < a.P.max_iter; ++it) {
+                if (ccost == 0) break;  // already a global minimum (:341)
+                const int px = ci + kx, py = cj + ky;
+                const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
+                uint32_t part = 0;
+                if (adm) {
+                    const int bx = x0 + (wx >> 1) + px, by = y0 + (wy >> 1) + py;
+                    uint32_t r0, r1, r2, r3;
+                    srow8(s_ref + (by + q) * W, bx, r0, r1);
+                    srow8(s_ref + (by + q + 4) * W, bx, r2, r3);
+                    part = vad4(cb_.y, r3, vad4(cb_.x, r2, vad4(ca_.y, r1, vad4(ca_.x, r0, 0u))));
+                }
+                part += __shfl_xor_sync(FULL, part, 1);
+                part += __shfl_xor_sync(FULL, part, 2);
+                const uint32_t cost = 4u * part;
+                const bool lead = adm && q == 0;
+                auto far = [&](int pc) { return max(abs(px + 8 - (pc & 15)), abs(py + 8 - (pc >> 4))) >= 2; };
+                bool fresh = lead;
+                if (it >= 1) fresh = fresh && far(pc0);
+                if (it >= 2) fresh = fresh && far(pc1);
+                if (it >= 3) fresh = fresh && far(pc2);
+                dpd += __popc(__ballot_sync(FULL, fresh));
+                const uint32_t m = __reduce_min_sync(FULL, lead ? cost : kInf);
+                if (m >= ccost) break;  // centre kept (:376)
+                const uint32_t ties = __ballot_sync(FULL, lead && cost == m);
+                int w;
+                if (__popc(ties) == 1) {
+                    w = (__ffs(ties) - 1) >> 2;
+                } else {
+                    // stable descending sort by off . dir (:357-362)
+                    PaBlock B;
+                    B.cur = b.luma + plane;
+                    B.ref = b.luma;
+                    B.ca = B.ra = nullptr;
+                    B.x0 = x0;
+                    B.y0 = y0;
+                    double dir_x, dir_y;
+                    prs_direction(a.P, B, lane, wx + 2 * ci, wy + 2 * cj, dir_x, dir_y);
+                    w = -1;
+                    double bestkey = 0.0;
+                    for (int o = 0; o < 8; ++o) {
+                        if (!((ties >> (4 * o)) & 1u)) continue;
+                        const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x), __dmul_rn(double(c_off8[o][1]), dir_y));
+                        if (w < 0 || key > bestkey) {
+                            w = o;
+                            bestkey = key;
+                        }
+                    }
+                }
+                const int pc = (ci + 8) | ((cj + 8) << 4);
+                if (it == 0) pc0 = pc;
+                if (it == 1) pc1 = pc;
+                if (it == 2) pc2 = pc;
+                ci += off8x(w);
+                cj += off8y(w);
+                ccost = m;
+                ++iters;
+            }
+            // fused predict_frame + psnr SSE at the final vector
+            const int fx = wx + 2 * ci, fy = wy + 2 * cj;
+            uint32_t se = 0;
+            if (lane < 8) {
+                const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + lane) * W + x0);
+                uint32_t r0, r1;
+                srow8(s_ref + (y0 + lane + (fy >> 1)) * W, x0 + (fx >> 1), r0, r1);
+                se = sq4(cr.y, r1, sq4(cr.x, r0, 0u));
+            }
+            se = __reduce_add_sync(FULL, se);
+            if (lane == 0) {
+                s_mv[g] = pack_mv(fx, fy);
+                write_rec(a.recs + g, fx, fy, ccost, 4, dpd, iters, uint32_t(ty), false);
+                my_sse += se;
+                my_dpd += dpd;
+                ++my_cnt[boundary ? 1 : 0];
+            }
+        }
+        __syncthreads();
+    }
+    if (lane == 0) {
+        atomicAdd(&s_sse, my_sse);
+        atomicAdd(&s_dpd, my_dpd);
+        for (int i = 0; i < 3; ++i) atomicAdd(&s_cnt[i], my_cnt[i]);
+    }
+    __syncthreads();
+    if (tid == 0 && a.stats) {
+        me_pair_stats st;
+        st.block_comparisons = 4 * int64_t(s_cnt[0] + s_cnt[1]);  // brs_select: 4 per block (:290)
+        st.dpd_refinement_steps = int64_t(s_dpd);
+        st.blocks_opaque = s_cnt[0];
+        st.blocks_boundary = s_cnt[1];
+        st.blocks_transparent = s_cnt[2];
+        st.sse = int64_t(s_sse);
+        *a.stats = st;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
 
@@ -1309,6 +1574,36 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
     if (mode && std::string(mode) == "duo") return 2;
     const int64_t per_step = b.nblocks() / std::max(1, b.steps());
     return per_step >= int64_t(num_sms) * 160 ? 3 : 1;
+}
+
+// One small pair in one CTA (pa_smem_kernel) when it fits in shared memory;
+// returns cudaErrorNotSupported when not eligible (the caller runs the
+// batched pipeline instead).
+cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
+                           me_block_rec* recs, me_pair_stats* stats, cudaStream_t st) {
+    const int step = cfg.halfpel ? 1 : cfg.step;
+    if (!(b.n_seq == 1 && b.pairs == 1 && b.bs == 8 && step == 2 && cfg.max_iterations <= 4 &&
+          (!prev0 || prev0_integer) && (size_t(b.W) * b.H) % 16 == 0) ||
+        getenv("ME_PA_NO_SMEM"))
+        return cudaErrorNotSupported;
+    const int plane_pad = b.W * b.H + 16;
+    const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * 5 + 16;
+    if (smem > 200 * 1024) return cudaErrorNotSupported;
+    PaSmemArgs a;
+    a.b = b;
+    a.P = make_pa_params(b, cfg);
+    a.prev0 = prev0;
+    a.recs = recs;
+    a.stats = stats;
+    a.plane_pad = plane_pad;
+    static thread_local size_t attr_smem = 0;  // the attribute call costs microseconds: set once per size
+    if (smem > attr_smem) {
+        cudaError_t e = cudaFuncSetAttribute(pa_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e) return e;
+        attr_smem = smem;
+    }
+    pa_smem_kernel<<<1, 1024, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0, const uint2* list,

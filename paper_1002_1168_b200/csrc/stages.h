@@ -52,6 +52,8 @@ cudaError_t launch_ring_single(int algo, const uint8_t* cur, const uint8_t* ref,
 int pa_wide_threshold(int num_sms);
 int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
                    int num_sms);
+cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
+                           me_block_rec* recs, me_pair_stats* stats, cudaStream_t st);
 cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0, const uint2* list,
                       const int* nlist, const int* ranges, int pa_mode, me_block_rec* recs,
                       me_pair_stats* stats, int num_sms, cudaStream_t st);
