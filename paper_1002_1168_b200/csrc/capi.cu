@@ -471,7 +471,8 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
     me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
     me_pair_stats* ds = reinterpret_cast<me_pair_stats*>(dr + size_t(cols) * rows);
     ME_CUDA(mek::run_batch(b, c1, prev_dev, dr, ds, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
-                           ctx->stream, nullptr, prev_integer));
+                           ctx->stream, ctx->events(), prev_integer));
+    ctx->ev_valid = ctx->profiling;
     ME_CUDA(cudaMemcpyAsync(ctx->pin_b.p, dr, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     s = sync(ctx);
     if (s) return s;

@@ -1267,10 +1267,9 @@ __global__ void prs_update_kernel(const uint8_t* cur, const uint8_t* ref, int W,
 // ---------------------------------------------------------------------------
 // pa_smem_kernel: one small frame pair (estimate_field on e.g. QCIF) in ONE
 // CTA with both frames (and alpha planes) resident in shared memory.  The
-// wavefront steps t = h + 2v are separated by __syncthreads instead of
-// global-memory dependency polls, candidates come from a shared MV array and
-// every pixel read is a shared-memory load, so a step costs one block's
-// compute instead of a global round trip plus compute.  Same algorithm and
+// wavefront runs as dataflow on a shared MV array (dependency waits cost a
+// shared-memory load instead of a global round trip) and every pixel read is
+// a shared-memory load; SSE and records are produced after the wavefront.  Same algorithm and
 // results as the batched kernels (classify + BRS + PRS + fused SSE); the
 // per-pair API's latency path.
 // ---------------------------------------------------------------------------
@@ -1307,7 +1306,9 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
     uint8_t* s_ra = s_cur + pp;  // alpha planes only when present
     uint8_t* s_ca = s_ra + pp;
     uint32_t* s_mv = reinterpret_cast<uint32_t*>(s_frames + (has_alpha ? 4 : 2) * size_t(pp));
-    uint8_t* s_type = reinterpret_cast<uint8_t*>(s_mv + cols * rows);
+    uint32_t* s_cost = s_mv + cols * rows;  // final cost_q4 of estimated blocks
+    uint32_t* s_meta = s_cost + cols * rows;  // dpd << 8 | iterations
+    uint8_t* s_type = reinterpret_cast<uint8_t*>(s_meta + cols * rows);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     // stage the planes (16-byte copies) and clear the MV words
     {
@@ -1331,7 +1332,7 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
     }
     __syncthreads();
     unsigned long long my_sse = 0, my_dpd = 0;
-    unsigned my_cnt[3] = {0u, 0u, 0u};
+    unsigned n_opaque = 0, n_boundary = 0, n_transparent = 0;
     // phase 1: classify every block (cur alpha, frame.cpp:81-104); transparent
     // blocks are final here (MV 0, SSE at the zero vector)
     for (int g = wid; g < cols * rows; g += nw) {
@@ -1348,7 +1349,10 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
             const bool allnz = __all_sync(FULL, lane >= 8 || (__vcmpeq4(r0, 0u) | __vcmpeq4(r1, 0u)) == 0u);
             ty = !any ? ME_TRANSPARENT : (allnz ? ME_OPAQUE : ME_BOUNDARY);
         }
-        if (lane == 0) s_type[g] = uint8_t(ty);
+        if (lane == 0) {
+            s_type[g] = uint8_t(ty);
+            if (ty != ME_TRANSPARENT) s_mv[g] = kSentinel;  // published by phase 2
+        }
         if (ty == ME_TRANSPARENT) {
             uint32_t se = 0;
             if (lane < 8) {
@@ -1360,20 +1364,31 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
             if (lane == 0) {
                 write_rec(a.recs + g, 0, 0, 0u, 0u, 0u, 0u, ME_TRANSPARENT, false);
                 my_sse += se;
-                ++my_cnt[2];
+                ++n_transparent;
             }
         }
     }
     __syncthreads();
-    // phase 2: the wavefront, one step per barrier
+    // phase 2: the wavefront as shared-memory dataflow.  Warps take the blocks
+    // in wavefront order (t = h + 2v, then v) round robin and wait on their
+    // dependencies' MV words (sentinel until published); every dependency
+    // lies earlier in that order, so the least unfinished block can always
+    // proceed.  A block starts as soon as ITS dependencies are done, not when
+    // the slowest block of the previous step is.
     const int c = lane >> 3, sub = lane & 7;  // BRS: candidate c, row sub
     const int k = lane >> 2, q = lane & 3;    // PRS: neighbour k, rows q and q + 4
     const int kx = off8x(k), ky = off8y(k);
-    const int nsteps = (cols - 1) + 2 * (rows - 1) + 1;
-    for (int t = 0; t < nsteps; ++t) {
-        const int vmin = max(0, (t - (cols - 1) + 1) / 2), vmax = min(rows - 1, t / 2);
-        for (int i = wid; i <= vmax - vmin; i += nw) {
-            const int v = vmin + i, h = t - 2 * v, g = v * cols + h;
+    volatile uint32_t* vmv = s_mv;
+    for (int idx = wid, t = 0, first = 0; idx < cols * rows; idx += nw) {
+        int vmin = 0, vmax = 0;
+        for (;; ++t) {  // the step holding block number idx (monotonic per warp)
+            vmin = max(0, (t - (cols - 1) + 1) / 2);
+            vmax = min(rows - 1, t / 2);
+            if (idx < first + vmax - vmin + 1) break;
+            first += vmax - vmin + 1;
+        }
+        {
+            const int v = vmin + (idx - first), h = t - 2 * v, g = v * cols + h;
             const int ty = s_type[g];
             if (ty == ME_TRANSPARENT) continue;  // warp-uniform
             const bool boundary = ty == ME_BOUNDARY;
@@ -1381,10 +1396,12 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
             const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
             const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
             // gather_candidates (estimators.cpp:238-255): A, B, C, T
-            uint32_t mw = 0;
-            if (c == 0 && h > 0) mw = s_mv[g - 1];
-            if (c == 1 && v > 0) mw = s_mv[g - cols];
-            if (c == 2 && v > 0 && h + 1 < cols) mw = s_mv[g - cols + 1];
+            int dep = -1;
+            if (c == 0 && h > 0) dep = g - 1;
+            if (c == 1 && v > 0) dep = g - cols;
+            if (c == 2 && v > 0 && h + 1 < cols) dep = g - cols + 1;
+            uint32_t mw = dep >= 0 ? vmv[dep] : 0u;
+            while (__any_sync(FULL, mw == kSentinel)) mw = dep >= 0 ? vmv[dep] : 0u;
             if (c == 3 && a.prev0) mw = pack_mv(a.prev0[2 * g], a.prev0[2 * g + 1]);
             const int myx = clip_comp(mv_dx(mw), lo_x, hi_x), myy = clip_comp(mv_dy(mw), lo_y, hi_y);
             // brs_select (estimators.cpp:257-301): row `sub` of candidate c
@@ -1491,30 +1508,49 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
                 ccost = m;
                 ++iters;
             }
-            // fused predict_frame + psnr SSE at the final vector
-            const int fx = wx + 2 * ci, fy = wy + 2 * cj;
-            uint32_t se = 0;
-            if (lane < 8) {
-                const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + lane) * W + x0);
-                uint32_t r0, r1;
-                srow8(s_ref + (y0 + lane + (fy >> 1)) * W, x0 + (fx >> 1), r0, r1);
-                se = sq4(cr.y, r1, sq4(cr.x, r0, 0u));
-            }
-            se = __reduce_add_sync(FULL, se);
+            // only the vector is on the wavefront's critical path: the SSE and
+            // the record are produced after the last step (phase 3)
             if (lane == 0) {
-                s_mv[g] = pack_mv(fx, fy);
-                write_rec(a.recs + g, fx, fy, ccost, 4, dpd, iters, uint32_t(ty), false);
-                my_sse += se;
-                my_dpd += dpd;
-                ++my_cnt[boundary ? 1 : 0];
+                s_cost[g] = ccost;
+                s_meta[g] = (dpd << 8) | iters;
+                __threadfence_block();
+                vmv[g] = pack_mv(wx + 2 * ci, wy + 2 * cj);
             }
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    // phase 3: fused predict_frame + psnr SSE at the final vectors, records
+    for (int g = wid; g < cols * rows; g += nw) {
+        const int ty = s_type[g];
+        if (ty == ME_TRANSPARENT) continue;  // warp-uniform
+        const int h = g % cols, v = g / cols, x0 = h * 8, y0 = v * 8;
+        const uint32_t mw = s_mv[g];
+        const int fx = mv_dx(mw), fy = mv_dy(mw);
+        uint32_t se = 0;
+        if (lane < 8) {
+            const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + lane) * W + x0);
+            uint32_t r0, r1;
+            srow8(s_ref + (y0 + lane + (fy >> 1)) * W, x0 + (fx >> 1), r0, r1);
+            se = sq4(cr.y, r1, sq4(cr.x, r0, 0u));
+        }
+        se = __reduce_add_sync(FULL, se);
+        if (lane == 0) {
+            const uint32_t meta = s_meta[g];
+            write_rec(a.recs + g, fx, fy, s_cost[g], 4, meta >> 8, meta & 0xFF, uint32_t(ty), false);
+            my_sse += se;
+            my_dpd += meta >> 8;
+            if (ty == ME_BOUNDARY)
+                ++n_boundary;
+            else
+                ++n_opaque;
+        }
     }
     if (lane == 0) {
         atomicAdd(&s_sse, my_sse);
         atomicAdd(&s_dpd, my_dpd);
-        for (int i = 0; i < 3; ++i) atomicAdd(&s_cnt[i], my_cnt[i]);
+        atomicAdd(&s_cnt[0], n_opaque);
+        atomicAdd(&s_cnt[1], n_boundary);
+        atomicAdd(&s_cnt[2], n_transparent);
     }
     __syncthreads();
     if (tid == 0 && a.stats) {
@@ -1587,7 +1623,7 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
         getenv("ME_PA_NO_SMEM"))
         return cudaErrorNotSupported;
     const int plane_pad = b.W * b.H + 16;
-    const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * 5 + 16;
+    const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * 13 + 16;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
     PaSmemArgs a;
     a.b = b;
