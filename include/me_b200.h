@@ -124,6 +124,12 @@ me_status me_b200_ctx_stage_ms(me_ctx* ctx, float* out, int n);
  * device->host (binary alpha masks cross PCIe bit-packed: W*H/8 per frame). */
 me_status me_b200_ctx_transfer_bytes(me_ctx* ctx, int64_t* h2d, int64_t* d2h);
 
+/* Kernels the last batched call (me_b200_run_sequences[_dev], estimate_field)
+ * launched: the stage kernels of every chunk (classify, scan, fill, the search
+ * — three for the hybrid PA schedule — and the optional prediction pass) plus
+ * the mask expansions of the host path. */
+me_status me_b200_ctx_launches(me_ctx* ctx, int64_t* out);
+
 /* SearchConfig::validate + PrsConfig::validate (estimators.cpp:139-150). */
 me_status me_b200_validate_config(const me_config* cfg);
 
@@ -141,6 +147,10 @@ me_status me_b200_validate_config(const me_config* cfg);
  *   stats  [n_seq][pairs]
  *   pred   [n_seq][pairs][height][width] or NULL (prediction not stored; the
  *          SSE is computed either way)
+ * Device pointers; enqueued on `stream` (a cudaStream_t; NULL is the CUDA
+ * default stream, me_b200_ctx_stream gives the context's own), not
+ * synchronised.  Calls on one context share its scratch: do not run two of
+ * them concurrently on different streams.
  * ------------------------------------------------------------------------- */
 me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames,
                                     int width, int height, const uint8_t* luma,

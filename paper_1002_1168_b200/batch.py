@@ -109,3 +109,10 @@ def last_transfer_bytes(device: int = 0):
     h, d = C.c_int64(), C.c_int64()
     check(lib().me_b200_ctx_transfer_bytes(ctx(device), C.byref(h), C.byref(d)))
     return h.value, d.value
+
+
+def last_launches(device: int = 0) -> int:
+    """Kernels launched by the last batched call on this thread's context."""
+    n = C.c_int64()
+    check(lib().me_b200_ctx_launches(ctx(device), C.byref(n)))
+    return n.value

@@ -85,7 +85,7 @@ size_t scratch_bytes(const Batch& b, int algo) {
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
                       size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events,
-                      bool prev0_integer) {
+                      bool prev0_integer, int* launches) {
     const int algo = cfg.algo;
     const bool pa = algo == ME_ALGO_PA;
     if (pa) {  // one small pair: the whole pipeline in one shared-memory-resident CTA
@@ -93,6 +93,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             for (int i = 0; i < 3; ++i) cudaEventRecord(events[i], st);
         const cudaError_t e0 = launch_pa_smem(b, cfg, prev0, prev0_integer, recs, stats, st);
         if (e0 == cudaSuccess) {
+            if (launches) *launches = 1 + (pred ? 1 : 0);
             if (events) cudaEventRecord(events[3], st);
             if (pred) {
                 const cudaError_t e1 = launch_mc_pred(b, recs, pred, st);
@@ -150,6 +151,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
 
     if (events) cudaEventRecord(events[3], st);
     if (pred && (e = launch_mc_pred(b, recs, pred, st))) return e;
+    // classify, scan, fill, the search (three launches for the PA hybrid), MC
+    if (launches) *launches = 3 + (pa_mode == 3 ? 3 : 1) + (pred ? 1 : 0);
     if (events) cudaEventRecord(events[4], st);
     return cudaGetLastError();
 }

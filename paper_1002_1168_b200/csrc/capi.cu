@@ -224,6 +224,13 @@ me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable) {
     return ok();
 }
 
+me_status me_b200_ctx_launches(me_ctx* ctx, int64_t* out) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (out) *out = ctx->launches;
+    return ok();
+}
+
 me_status me_b200_ctx_transfer_bytes(me_ctx* ctx, int64_t* h2d, int64_t* d2h) {
     me_status s = check_ctx(ctx);
     if (s) return s;
@@ -301,9 +308,11 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
     const mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H, luma, alpha);
     const size_t need = mek::scratch_bytes(b, cfg->algo);
     ME_CUDA(ctx->tasks.reserve(need));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: the CUDA default stream
+    int nl = 0;
     ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, pred, ctx->tasks.p, ctx->tasks.cap,
-                           ctx->num_sms, st, ctx->events()));
+                           ctx->num_sms, st, ctx->events(), false, &nl));
+    ctx->launches = nl;
     ctx->ev_valid = ctx->profiling;
     return ok();
 }
@@ -345,12 +354,14 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
             ME_CUDA(ctx->pack_dev[i].reserve(max_chunk / 8 + 64));
         }
     ctx->h2d_bytes = ctx->d2h_bytes = 0;
+    ctx->launches = 0;
     for (int k = 0; k < nchunks; ++k) {
         const int s0 = int(int64_t(n_seq) * k / nchunks), s1 = int(int64_t(n_seq) * (k + 1) / nchunks);
         const int ns = s1 - s0;
         const size_t o = seq_bytes * s0, n = seq_bytes * ns;
         ME_CUDA(cudaMemcpyAsync(dl + o, luma + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
         ctx->h2d_bytes += int64_t(n);
+        bool packed_chunk = false;  // one expansion kernel when the mask went bit-packed
         if (alpha) {
             const int slot = k & 1;
             bool packed = false;
@@ -365,6 +376,7 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
                     ctx->h2d_bytes += int64_t(n / 8);
                     ME_CUDA(cudaEventRecord(ctx->ev_pack[slot], ctx->copy_stream));
                     ME_CUDA(mek::unpack_mask(db, da + o, n, ctx->copy_stream));
+                    packed_chunk = true;
                 }
             }
             if (!packed) {
@@ -378,9 +390,11 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
         const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, dl + seq_bytes * s0,
                                         alpha ? da + seq_bytes * s0 : nullptr);
         ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+        int nl = 0;
         ME_CUDA(mek::run_batch(b, *cfg, nullptr, dr + seq_recs * s0, ds + size_t(pairs) * s0,
                                pred ? dp + plane * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
-                               ctx->num_sms, ctx->stream, nullptr));
+                               ctx->num_sms, ctx->stream, nullptr, false, &nl));
+        ctx->launches += nl + (packed_chunk ? 1 : 0);
         ME_CUDA(cudaEventRecord(ctx->ev_out[k], ctx->stream));
         ME_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_out[k], 0));
         ME_CUDA(cudaMemcpyAsync(recs + seq_recs * s0, dr + seq_recs * s0, seq_recs * ns * sizeof(me_block_rec),
@@ -470,8 +484,10 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
     // records and stats in one device buffer -> one D2H into pinned memory
     me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
     me_pair_stats* ds = reinterpret_cast<me_pair_stats*>(dr + size_t(cols) * rows);
+    int nl = 0;
     ME_CUDA(mek::run_batch(b, c1, prev_dev, dr, ds, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
-                           ctx->stream, ctx->events(), prev_integer));
+                           ctx->stream, ctx->events(), prev_integer, &nl));
+    ctx->launches = nl;
     ctx->ev_valid = ctx->profiling;
     ME_CUDA(cudaMemcpyAsync(ctx->pin_b.p, dr, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     s = sync(ctx);

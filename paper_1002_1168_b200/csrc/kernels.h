@@ -31,10 +31,11 @@ size_t scratch_bytes(const Batch& b, int algo);
 // before the search, before MC+PSNR and at the end.
 // `prev0_integer`: every prev0 vector is integer-pel (even), which lets the
 // fast PA kernels take it.
+// `launches` (nullable) receives the number of kernels launched.
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
                       size_t scratch_size, int num_sms, cudaStream_t st,
-                      cudaEvent_t* events = nullptr, bool prev0_integer = false);
+                      cudaEvent_t* events = nullptr, bool prev0_integer = false, int* launches = nullptr);
 
 // Single-block entry points (all pointers device pointers; outputs in `out`,
 // an int64 array whose layout is documented at each launcher).

@@ -82,6 +82,7 @@ struct me_ctx {
     DevBuf pack_dev[2];
     cudaEvent_t ev_pack[2] = {};
     int64_t h2d_bytes = 0, d2h_bytes = 0;  // of the last host-pointer batch
+    int64_t launches = 0;                  // kernels launched by the last batched call
 };
 
 #endif
