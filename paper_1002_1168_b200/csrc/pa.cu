@@ -1608,6 +1608,7 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
     if (!fast || (mode && std::string(mode) == "warp")) return 0;
     if (mode && std::string(mode) == "fast") return 1;
     if (mode && std::string(mode) == "duo") return 2;
+    if (mode && std::string(mode) == "hybrid") return 3;
     const int64_t per_step = b.nblocks() / std::max(1, b.steps());
     return per_step >= int64_t(num_sms) * 160 ? 3 : 1;
 }

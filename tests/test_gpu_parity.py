@@ -244,3 +244,21 @@ def test_estimate_field_random_prev(me_gpu, port, odd):
                                         me_gpu.SearchConfig(search_range=16, block_size=8), me_gpu.PrsConfig(), return_records=True)
     want, wst = port.estimate_field(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[2], luma[0], alpha[2], alpha[0], prev_mv=prev)
     assert_recs(recs, want)
+
+
+@pytest.mark.parametrize("mode", ["fast", "duo", "hybrid", "warp"])
+def test_pa_kernel_modes(me_gpu, port, mode, monkeypatch):
+    """Every PA kernel schedule (one block per warp, two per warp, the hybrid
+    split of the sorted list, the generic kernel) on the same batch; the
+    hybrid's wide threshold is lowered so all three of its ranges are used."""
+    from paper_1002_1168_b200 import synth
+
+    monkeypatch.setenv("ME_PA_MODE", mode)
+    monkeypatch.setenv("ME_PA_WIDE", "4")
+    luma, alpha = synth.config4_batch(5, 700, frames=6)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in range(5):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"{mode} seq {i}")
+        assert np.array_equal(stats[i], want_s)
