@@ -29,62 +29,23 @@
 
 #include "me_b200.h"
 #include "me_internal.h"
+#include "synth.h"
 
 namespace {
 
 struct SplitMix {
     uint64_t s;
-    uint64_t next() {
-        uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-        return z ^ (z >> 31);
-    }
+    uint64_t next() { return mes::mix64(s += mes::kGolden); }
     int range(int lo, int hi) {  // inclusive
         return lo + int(next() % uint64_t(hi - lo + 1));
     }
+    // the state before an image's pixel draws; skips them (one draw per 8 pixels)
+    uint64_t skip_image(int w, int h) {
+        const uint64_t s0 = s;
+        s += uint64_t((int64_t(w) * h + 7) / 8) * mes::kGolden;
+        return s0;
+    }
 };
-
-uint64_t mix64(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
-}
-
-// sigma = 1.5, radius 4: round(4096 * g_k / sum g), centre adjusted to sum 4096.
-constexpr int kTaps[5] = {1092, 874, 449, 148, 31};
-
-void blur(std::vector<uint8_t>& img, int w, int h) {
-    std::vector<uint8_t> tmp(img.size());
-    for (int y = 0; y < h; ++y) {
-        const uint8_t* r = img.data() + size_t(y) * w;
-        for (int x = 0; x < w; ++x) {
-            int acc = kTaps[0] * r[x];
-            for (int k = 1; k <= 4; ++k)
-                acc += kTaps[k] * (r[std::max(x - k, 0)] + r[std::min(x + k, w - 1)]);
-            tmp[size_t(y) * w + x] = uint8_t((acc + 2048) >> 12);
-        }
-    }
-    for (int y = 0; y < h; ++y) {
-        for (int x = 0; x < w; ++x) {
-            int acc = kTaps[0] * tmp[size_t(y) * w + x];
-            for (int k = 1; k <= 4; ++k)
-                acc += kTaps[k] * (tmp[size_t(std::max(y - k, 0)) * w + x] +
-                                   tmp[size_t(std::min(y + k, h - 1)) * w + x]);
-            img[size_t(y) * w + x] = uint8_t((acc + 2048) >> 12);
-        }
-    }
-}
-
-std::vector<uint8_t> blurred_noise(int w, int h, SplitMix& rng) {
-    std::vector<uint8_t> img(size_t(w) * h);
-    for (size_t i = 0; i < img.size(); i += 8) {
-        uint64_t v = rng.next();
-        for (size_t k = 0; k < 8 && i + k < img.size(); ++k) img[i + k] = uint8_t(v >> (8 * k));
-    }
-    blur(img, w, h);
-    return img;
-}
 
 int floor_div(int64_t a, int64_t b) {  // b > 0
     int64_t q = a / b;
@@ -92,17 +53,8 @@ int floor_div(int64_t a, int64_t b) {  // b > 0
     return int(q);
 }
 
-struct Object {
-    int bw, bh;     // box size
-    bool ellipse;
-    int x0, y0;     // position at frame 0
-    int vx, vy;
-    std::vector<uint8_t> tex;
-    std::vector<uint8_t> inside;  // bw*bh membership
-};
-
 // Position of the box at frame t with reflection off [0, W-bw] x [0, H-bh].
-void object_pos(const Object& o, int W, int H, int t, int& x, int& y) {
+void object_pos(const mes::PlanObject& o, int W, int H, int t, int& x, int& y) {
     x = o.x0;
     y = o.y0;
     int vx = o.vx, vy = o.vy;
@@ -122,7 +74,108 @@ void object_pos(const Object& o, int W, int H, int t, int& x, int& y) {
     }
 }
 
+// Separable blur, edge-replicated, round-half-up per pass.
+void blur(std::vector<uint8_t>& img, int w, int h) {
+    std::vector<uint8_t> tmp(img.size());
+    for (int y = 0; y < h; ++y) {
+        const uint8_t* r = img.data() + size_t(y) * w;
+        for (int x = 0; x < w; ++x) {
+            int acc = mes::kTaps[0] * r[x];
+            for (int k = 1; k <= 4; ++k)
+                acc += mes::kTaps[k] * (r[std::max(x - k, 0)] + r[std::min(x + k, w - 1)]);
+            tmp[size_t(y) * w + x] = uint8_t((acc + 2048) >> 12);
+        }
+    }
+    for (int y = 0; y < h; ++y) {
+        for (int x = 0; x < w; ++x) {
+            int acc = mes::kTaps[0] * tmp[size_t(y) * w + x];
+            for (int k = 1; k <= 4; ++k)
+                acc += mes::kTaps[k] * (tmp[size_t(std::max(y - k, 0)) * w + x] +
+                                        tmp[size_t(std::min(y + k, h - 1)) * w + x]);
+            img[size_t(y) * w + x] = uint8_t((acc + 2048) >> 12);
+        }
+    }
+}
+
+std::vector<uint8_t> blurred_noise(int w, int h, uint64_t s0) {
+    std::vector<uint8_t> img(size_t(w) * h);
+    for (size_t i = 0; i < img.size(); ++i) img[i] = mes::noise_byte(s0, i);
+    blur(img, w, h);
+    return img;
+}
+
 }  // namespace
+
+namespace mes {
+
+me_status make_plan(const me_synth_params* p, Plan& P) {
+    if (!p) return me_fail(ME_ERR_INVALID_ARGUMENT, "null argument");
+    const int W = p->width, H = p->height, F = p->frames;
+    if (W <= 0 || H <= 0 || W % 16 || H % 16 || F < 1)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "frame dimensions must be positive multiples of 16");
+    if (p->n_objects < 0 || p->n_objects > kMaxObjects) return me_fail(ME_ERR_INVALID_ARGUMENT, "n_objects");
+    if (p->blur_sigma_q8 != 384) return me_fail(ME_ERR_INVALID_ARGUMENT, "only sigma 1.5 blur");
+    SplitMix rng{p->seed * 0x2545F4914F6CDD1DULL + 1};
+    P.W = W;
+    P.H = H;
+    P.F = F;
+    P.n_objects = p->n_objects;
+    P.noise_sigma_q8 = p->noise_sigma_q8;
+    // global offsets per frame
+    P.ox.assign(size_t(F), 0);
+    P.oy.assign(size_t(F), 0);
+    for (int t = 0; t < F; ++t) {
+        if (p->bg_jitter > 0) {
+            if (t > 0) {
+                P.ox[size_t(t)] = P.ox[size_t(t - 1)] + rng.range(-p->bg_jitter, p->bg_jitter);
+                P.oy[size_t(t)] = P.oy[size_t(t - 1)] + rng.range(-p->bg_jitter, p->bg_jitter);
+            }
+        } else {
+            P.ox[size_t(t)] = floor_div(int64_t(t) * p->bg_drift_q8[0] + 128, 256);
+            P.oy[size_t(t)] = floor_div(int64_t(t) * p->bg_drift_q8[1] + 128, 256);
+        }
+    }
+    P.M = 4;
+    for (int t = 0; t < F; ++t)
+        P.M = std::max(P.M, std::max(std::abs(P.ox[size_t(t)]), std::abs(P.oy[size_t(t)])) + 4);
+    P.BW = W + 2 * P.M;
+    P.BH = H + 2 * P.M;
+    P.bg_s0 = rng.skip_image(P.BW, P.BH);
+    P.objs.assign(size_t(p->n_objects), PlanObject{});
+    for (int i = 0; i < p->n_objects; ++i) {
+        PlanObject& o = P.objs[size_t(i)];
+        if (i < 4 && p->obj_w[i] > 0) {
+            o.bw = 2 * p->obj_w[i];
+            o.bh = 2 * p->obj_h[i];
+            o.ellipse = 1;
+        } else {
+            o.bw = rng.range(p->obj_min, p->obj_max);
+            o.bh = rng.range(p->obj_min, p->obj_max);
+            o.ellipse = p->shapes == 0 ? 1 : (rng.next() & 1) == 0;
+        }
+        o.bw = std::min(o.bw, W);
+        o.bh = std::min(o.bh, H);
+        if (p->vel_fixed && i < 4) {
+            o.vx = p->obj_v[i][0];
+            o.vy = p->obj_v[i][1];
+        } else {
+            o.vx = rng.range(-p->vmax, p->vmax);
+            o.vy = rng.range(-p->vmax, p->vmax);
+        }
+        o.x0 = rng.range(0, W - o.bw);
+        o.y0 = rng.range(0, H - o.bh);
+        o.tex_s0 = rng.skip_image(o.bw, o.bh);
+    }
+    P.noise_key = rng.next();
+    P.px.assign(size_t(F) * p->n_objects, 0);
+    P.py.assign(size_t(F) * p->n_objects, 0);
+    for (int t = 0; t < F; ++t)
+        for (int i = 0; i < p->n_objects; ++i)
+            object_pos(P.objs[size_t(i)], W, H, t, P.px[size_t(t) * p->n_objects + i], P.py[size_t(t) * p->n_objects + i]);
+    return ME_OK;
+}
+
+}  // namespace mes
 
 extern "C" me_status me_b200_synth_preset(int config_id, uint64_t seed, me_synth_params* p) {
     if (!p) return me_fail(ME_ERR_INVALID_ARGUMENT, "null params");
@@ -174,117 +227,43 @@ extern "C" me_status me_b200_synth_preset(int config_id, uint64_t seed, me_synth
 }
 
 extern "C" me_status me_b200_synth(const me_synth_params* p, uint8_t* luma, uint8_t* alpha) {
-    if (!p || !luma) return me_fail(ME_ERR_INVALID_ARGUMENT, "null argument");
-    const int W = p->width, H = p->height, F = p->frames;
-    if (W <= 0 || H <= 0 || W % 16 || H % 16 || F < 1)
-        return me_fail(ME_ERR_INVALID_ARGUMENT, "frame dimensions must be positive multiples of 16");
-    if (p->n_objects < 0 || p->n_objects > 64) return me_fail(ME_ERR_INVALID_ARGUMENT, "n_objects");
-    if (p->blur_sigma_q8 != 384) return me_fail(ME_ERR_INVALID_ARGUMENT, "only sigma 1.5 blur");
-    SplitMix rng{p->seed * 0x2545F4914F6CDD1DULL + 1};
-
-    // global offsets per frame
-    std::vector<int> ox(F), oy(F);
-    for (int t = 0; t < F; ++t) {
-        if (p->bg_jitter > 0) {
-            if (t == 0) { ox[t] = 0; oy[t] = 0; }
-            else {
-                ox[t] = ox[t - 1] + rng.range(-p->bg_jitter, p->bg_jitter);
-                oy[t] = oy[t - 1] + rng.range(-p->bg_jitter, p->bg_jitter);
-            }
-        } else {
-            ox[t] = floor_div(int64_t(t) * p->bg_drift_q8[0] + 128, 256);
-            oy[t] = floor_div(int64_t(t) * p->bg_drift_q8[1] + 128, 256);
-        }
-    }
-    int M = 4;
-    for (int t = 0; t < F; ++t) M = std::max(M, std::max(std::abs(ox[t]), std::abs(oy[t])) + 4);
-    const int BW = W + 2 * M, BH = H + 2 * M;
-    std::vector<uint8_t> bg = blurred_noise(BW, BH, rng);
-
-    std::vector<Object> objs(size_t(p->n_objects));
-    for (int i = 0; i < p->n_objects; ++i) {
-        Object& o = objs[size_t(i)];
-        if (i < 4 && p->obj_w[i] > 0) {
-            o.bw = 2 * p->obj_w[i];
-            o.bh = 2 * p->obj_h[i];
-            o.ellipse = true;
-        } else {
-            o.bw = rng.range(p->obj_min, p->obj_max);
-            o.bh = rng.range(p->obj_min, p->obj_max);
-            o.ellipse = p->shapes == 0 ? true : (rng.next() & 1) == 0;
-        }
-        o.bw = std::min(o.bw, W);
-        o.bh = std::min(o.bh, H);
-        if (p->vel_fixed && i < 4) {
-            o.vx = p->obj_v[i][0];
-            o.vy = p->obj_v[i][1];
-        } else {
-            o.vx = rng.range(-p->vmax, p->vmax);
-            o.vy = rng.range(-p->vmax, p->vmax);
-        }
-        o.x0 = rng.range(0, W - o.bw);
-        o.y0 = rng.range(0, H - o.bh);
-        o.tex = blurred_noise(o.bw, o.bh, rng);
-        o.inside.assign(size_t(o.bw) * o.bh, 0);
-        const int64_t a2 = int64_t(o.bw) * o.bw, b2 = int64_t(o.bh) * o.bh;
-        for (int y = 0; y < o.bh; ++y)
-            for (int x = 0; x < o.bw; ++x) {
-                if (!o.ellipse) { o.inside[size_t(y) * o.bw + x] = 1; continue; }
-                // pixel centre in doubled coordinates relative to the box centre
-                const int64_t ex = 2 * x + 1 - o.bw, ey = 2 * y + 1 - o.bh;
-                o.inside[size_t(y) * o.bw + x] = (ex * ex * b2 + ey * ey * a2 <= a2 * b2) ? 1 : 0;
-            }
-    }
-    const uint64_t noise_key = rng.next();
-
+    if (!luma) return me_fail(ME_ERR_INVALID_ARGUMENT, "null argument");
+    mes::Plan P;
+    const me_status st = mes::make_plan(p, P);
+    if (st) return st;
+    const int W = P.W, H = P.H, F = P.F, BW = P.BW, BH = P.BH, M = P.M, no = P.n_objects;
+    const std::vector<uint8_t> bg = blurred_noise(BW, BH, P.bg_s0);
+    std::vector<std::vector<uint8_t>> tex(static_cast<size_t>(no));
+    for (int i = 0; i < no; ++i) tex[size_t(i)] = blurred_noise(P.objs[size_t(i)].bw, P.objs[size_t(i)].bh, P.objs[size_t(i)].tex_s0);
     const size_t plane = size_t(W) * H;
     for (int t = 0; t < F; ++t) {
         uint8_t* f = luma + plane * t;
         uint8_t* a = alpha ? alpha + plane * t : nullptr;
         for (int y = 0; y < H; ++y) {
-            const int sy = std::clamp(y + M + oy[t], 0, BH - 1);
+            const int sy = std::clamp(y + M + P.oy[size_t(t)], 0, BH - 1);
             for (int x = 0; x < W; ++x) {
-                const int sx = std::clamp(x + M + ox[t], 0, BW - 1);
+                const int sx = std::clamp(x + M + P.ox[size_t(t)], 0, BW - 1);
                 f[size_t(y) * W + x] = bg[size_t(sy) * BW + sx];
             }
         }
         if (a) std::memset(a, 0, plane);
-        for (const Object& o : objs) {
-            int px, py;
-            object_pos(o, W, H, t, px, py);
+        for (int i = 0; i < no; ++i) {  // ascending index: later objects occlude
+            const mes::PlanObject& o = P.objs[size_t(i)];
+            const int px = P.px[size_t(t) * no + i], py = P.py[size_t(t) * no + i];
             for (int y = 0; y < o.bh; ++y) {
                 const int fy = py + y;
                 if (fy < 0 || fy >= H) continue;
                 for (int x = 0; x < o.bw; ++x) {
                     const int fx = px + x;
-                    if (fx < 0 || fx >= W || !o.inside[size_t(y) * o.bw + x]) continue;
-                    f[size_t(fy) * W + fx] = o.tex[size_t(y) * o.bw + x];
+                    if (fx < 0 || fx >= W || !mes::inside_box(o.ellipse, o.bw, o.bh, x, y)) continue;
+                    f[size_t(fy) * W + fx] = tex[size_t(i)][size_t(y) * o.bw + x];
                     if (a) a[size_t(fy) * W + fx] = 255;
                 }
             }
         }
-        if (p->noise_sigma_q8 > 0) {
-            const int64_t sig = p->noise_sigma_q8;
-            for (size_t i = 0; i < plane; ++i) {
-                const uint64_t base = noise_key ^ (uint64_t(t) << 40) ^ (uint64_t(i) * 3);
-                int64_t s = 0;
-                for (int k = 0; k < 3; ++k) {
-                    const uint64_t r = mix64(base + uint64_t(k) * 0x9E3779B97F4A7C15ULL);
-                    s += int64_t(r & 0xFFFF) + int64_t((r >> 16) & 0xFFFF) +
-                         int64_t((r >> 32) & 0xFFFF) + int64_t(r >> 48);
-                }
-                s -= 6 * 65535;  // centred (variance 12 * (2^32 - 1) / 12 ~ 2^32)
-                // n = s * sigma / 2^16 / 2^8, rounded half to even
-                const int64_t num = s * sig;
-                const int64_t den = int64_t(1) << 24;
-                int64_t q = num >= 0 ? num / den : -((-num) / den);
-                int64_t r = num - q * den;  // same sign as num
-                if (2 * std::abs(r) > den || (2 * std::abs(r) == den && (q & 1)))
-                    q += num >= 0 ? 1 : -1;
-                const int v = int(f[i]) + int(q);
-                f[i] = uint8_t(std::clamp(v, 0, 255));
-            }
-        }
+        if (P.noise_sigma_q8 > 0)
+            for (size_t i = 0; i < plane; ++i)
+                f[i] = uint8_t(std::clamp(int(f[i]) + mes::noise_delta(P.noise_key, t, i, P.noise_sigma_q8), 0, 255));
     }
     return ME_OK;
 }
