@@ -270,6 +270,13 @@ typedef struct me_synth_params {
 me_status me_b200_synth_preset(int config_id, uint64_t seed, me_synth_params* out);
 /* luma/alpha: [frames][height][width] each (alpha = union of object masks). */
 me_status me_b200_synth(const me_synth_params* p, uint8_t* luma, uint8_t* alpha);
+/* The same generator on the device for a batch of n_seq sequences (one params
+ * entry per sequence, equal geometry; config 4 uses seed = base + i): luma and
+ * alpha (nullable) are DEVICE buffers [n_seq][frames][height][width], written
+ * on `stream` (NULL = default stream); byte-identical to me_b200_synth.
+ * Returns after the stream has finished the batch. */
+me_status me_b200_synth_dev(me_ctx* ctx, const me_synth_params* params, int n_seq, uint8_t* luma,
+                            uint8_t* alpha, void* stream);
 
 #ifdef __cplusplus
 }

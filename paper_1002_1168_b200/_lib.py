@@ -147,6 +147,7 @@ SIGNATURES = {
     "me_b200_sse": (I, [P, I, I, P, P, I64P]),
     "me_b200_synth_preset": (I, [I, C.c_uint64, C.POINTER(MeSynthParams)]),
     "me_b200_synth": (I, [C.POINTER(MeSynthParams), P, P]),
+    "me_b200_synth_dev": (I, [P, C.POINTER(MeSynthParams), I, P, P, P]),
 }
 
 _lib = None

@@ -80,17 +80,17 @@ void blur(std::vector<uint8_t>& img, int w, int h) {
     for (int y = 0; y < h; ++y) {
         const uint8_t* r = img.data() + size_t(y) * w;
         for (int x = 0; x < w; ++x) {
-            int acc = mes::kTaps[0] * r[x];
+            int acc = mes::blur_tap(0) * r[x];
             for (int k = 1; k <= 4; ++k)
-                acc += mes::kTaps[k] * (r[std::max(x - k, 0)] + r[std::min(x + k, w - 1)]);
+                acc += mes::blur_tap(k) * (r[std::max(x - k, 0)] + r[std::min(x + k, w - 1)]);
             tmp[size_t(y) * w + x] = uint8_t((acc + 2048) >> 12);
         }
     }
     for (int y = 0; y < h; ++y) {
         for (int x = 0; x < w; ++x) {
-            int acc = mes::kTaps[0] * tmp[size_t(y) * w + x];
+            int acc = mes::blur_tap(0) * tmp[size_t(y) * w + x];
             for (int k = 1; k <= 4; ++k)
-                acc += mes::kTaps[k] * (tmp[size_t(std::max(y - k, 0)) * w + x] +
+                acc += mes::blur_tap(k) * (tmp[size_t(std::max(y - k, 0)) * w + x] +
                                         tmp[size_t(std::min(y + k, h - 1)) * w + x]);
             img[size_t(y) * w + x] = uint8_t((acc + 2048) >> 12);
         }

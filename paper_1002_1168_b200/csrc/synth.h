@@ -15,14 +15,14 @@ namespace mes {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
 constexpr int kMaxObjects = 64;
-// sigma = 1.5, radius 4: round(4096 * g_k / sum g), centre adjusted to sum 4096.
-constexpr int kTaps[5] = {1092, 874, 449, 148, 31};
-
 #ifdef __CUDACC__
 #define MES_HD __host__ __device__
 #else
 #define MES_HD
 #endif
+
+// sigma = 1.5, radius 4: round(4096 * g_k / sum g), centre adjusted to sum 4096.
+MES_HD constexpr int blur_tap(int k) { return k == 0 ? 1092 : k == 1 ? 874 : k == 2 ? 449 : k == 3 ? 148 : 31; }
 
 MES_HD inline uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;

@@ -54,3 +54,25 @@ def config4_batch(n_seq: int, base_seed: int, frames: Optional[int] = None, luma
     with ThreadPoolExecutor(max(1, threads)) as ex:
         list(ex.map(one, range(n_seq)))
     return luma, alpha
+
+
+def config4_batch_dev(n_seq: int, base_seed: int, frames: Optional[int] = None, config_id: int = 4, device: int = 0, stream=None):
+    """The same batch generated on the GPU (me_b200_synth_dev): uint8 CUDA
+    tensors (luma, alpha) [n_seq, frames, H, W], byte-identical to
+    config4_batch."""
+    import torch
+
+    from ._lib import ctx
+
+    params = (MeSynthParams * n_seq)()
+    for i in range(n_seq):
+        params[i] = preset(config_id, base_seed + i, frames)
+    p0 = params[0]
+    shape = (n_seq, p0.frames, p0.height, p0.width)
+    dev = torch.device("cuda", device)
+    luma = torch.empty(shape, dtype=torch.uint8, device=dev)
+    alpha = torch.empty(shape, dtype=torch.uint8, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    check(lib().me_b200_synth_dev(ctx(device), params, n_seq, C.c_void_p(luma.data_ptr()), C.c_void_p(alpha.data_ptr()), C.c_void_p(stream)))
+    return luma, alpha

@@ -61,3 +61,21 @@ def test_bad_params():
         synth.generate(p)
     with pytest.raises(ValueError):
         synth.preset(9, 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid,frames", [(1, None), (2, 4), (3, 2), (5, 2)])
+def test_device_generator_matches_host(me_gpu, cid, frames):
+    """me_b200_synth_dev renders the same bytes as the host generator."""
+    luma_d, alpha_d = synth.config4_batch_dev(2, 33, frames=frames, config_id=cid)
+    for i in range(2):
+        l, a = synth.config_sequence(cid, 33 + i, frames)
+        assert np.array_equal(luma_d[i].cpu().numpy(), l), f"cfg{cid} seq {i} luma"
+        assert np.array_equal(alpha_d[i].cpu().numpy(), a), f"cfg{cid} seq {i} alpha"
+
+
+@pytest.mark.gpu
+def test_device_generator_config4_batch(me_gpu):
+    luma_d, alpha_d = synth.config4_batch_dev(7, 900, frames=3)
+    luma, alpha = synth.config4_batch(7, 900, frames=3, threads=4)
+    assert np.array_equal(luma_d.cpu().numpy(), luma) and np.array_equal(alpha_d.cpu().numpy(), alpha)
