@@ -244,8 +244,9 @@ def run_experiment_arrays(cfg: ExperimentConfig, luma: np.ndarray, alpha: Option
 def run_experiment(cfg: ExperimentConfig, device: int = 0) -> ExperimentResult:  # bench.cpp:120-227
     cfg.validate()
     n = cfg.frames_used()
-    luma = seqio.read_frames(cfg.source, n)
+    W, H = cfg.source.width, cfg.source.height
+    luma = seqio.stream_frames(cfg.source, n)  # straight into pinned memory
     alpha = None
     if cfg.masks.present():
-        alpha = seqio.read_masks(cfg.masks, n, cfg.source.width, cfg.source.height)
+        alpha = seqio.read_masks(cfg.masks, n, W, H, out=seqio.pinned_empty((n, H, W)))
     return run_experiment_arrays(cfg, luma, alpha, device)

@@ -132,6 +132,49 @@ def read_frames(src: SequenceSource, count: Optional[int] = None, chroma: bool =
     return luma, c
 
 
+def pinned_empty(shape) -> np.ndarray:
+    """A uint8 array in page-locked host memory (torch's pinned allocator) so
+    the host pipeline's H2D copies run asynchronously at full PCIe rate;
+    plain memory when torch / CUDA are unavailable."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.empty(tuple(shape), dtype=torch.uint8, pin_memory=True).numpy()
+    except ImportError:
+        pass
+    return np.empty(tuple(shape), np.uint8)
+
+
+def stream_frames(src: SequenceSource, count: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Luma of frames 0..count-1 read straight into ``out`` (default: pinned
+    memory), one ``readinto`` per frame, chroma skipped; Y4M markers checked."""
+    n = src.frame_count if count is None else count
+    if n < 0 or n > src.frame_count:
+        raise IndexError(f"frame index {n - 1} out of range [0,{src.frame_count})")
+    W, H = src.width, src.height
+    out = pinned_empty((n, H, W)) if out is None else out
+    if out.shape != (n, H, W) or out.dtype != np.uint8 or not out.flags.c_contiguous:
+        raise ValueError("out must be a contiguous uint8 array [frames, H, W]")
+    csize = W * H // 2
+    with open(src.path, "rb", buffering=0) as f:
+        f.seek(src.header_bytes)
+        for i in range(n):
+            if src.format == Y4M:
+                m = f.read(src.frame_marker_bytes)
+                if len(m) != src.frame_marker_bytes or not m.startswith(b"FRAME") or not m.endswith(b"\n"):
+                    raise RuntimeError(f"{src.path}: irregular FRAME marker at index {i}")
+            view = memoryview(out[i]).cast("B")
+            got = 0
+            while got < W * H:
+                k = f.readinto(view[got:])
+                if not k:
+                    raise RuntimeError(f"short read (frame payload) in {src.path}")
+                got += k
+            f.seek(csize, 1)
+    return out
+
+
 def read_pgm(path: str) -> np.ndarray:
     with open(path, "rb") as f:
         data = f.read()
@@ -172,11 +215,11 @@ def binarize(gray: np.ndarray, threshold: int = 128) -> np.ndarray:  # frame.cpp
     return np.where(gray >= threshold, 255, 0).astype(np.uint8)
 
 
-def read_masks(src: MaskSource, count: int, width: int, height: int) -> np.ndarray:
+def read_masks(src: MaskSource, count: int, width: int, height: int, out: Optional[np.ndarray] = None) -> np.ndarray:
     """``[count, H, W]`` binarised masks (read_mask, video_io.cpp:184-192)."""
     if not src.present():
         raise RuntimeError("read_mask called without a mask pattern")
-    out = np.empty((count, height, width), np.uint8)
+    out = np.empty((count, height, width), np.uint8) if out is None else out
     for i in range(count):
         gray = read_pgm(src.path_for(i))
         if gray.shape != (height, width):

@@ -61,6 +61,8 @@ def test_readers_roundtrip(tmp_path):
     seqio.write_i420(raw, luma)
     src2 = seqio.open_i420(raw, 176, 144)
     assert src2.frame_count == 5 and np.array_equal(seqio.read_frames(src2, 3), luma[:3])
+    assert np.array_equal(seqio.stream_frames(src2, 4), luma[:4])
+    assert np.array_equal(seqio.stream_frames(src), luma)
     with pytest.raises(ValueError):
         seqio.open_i420(raw, 100, 144)
     with pytest.raises(RuntimeError):
