@@ -650,6 +650,13 @@ constexpr int kFastWarpWords = 4 * kFastPatch + 16 + 4;  // patches, current blo
 __device__ __forceinline__ int off8x(int k) { const int i = k + (k >= 4); return i - 3 * (i / 3) - 1; }
 __device__ __forceinline__ int off8y(int k) { const int i = k + (k >= 4); return i / 3 - 1; }
 
+__device__ __forceinline__ void cp_async16(uint32_t* smem, const void* gmem, bool fill) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int n = fill ? 16 : 0;  // n = 0: zero-fill (patch columns outside the frame)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // 2 words of a staged patch row: bytes [t, t + 8) of the row's 32 raw bytes.
 __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, uint32_t& r1) {
     const int q = t >> 2;
@@ -666,7 +673,6 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     uint32_t* ws = s_pa + wid * kFastWarpWords;
     uint32_t* patch = ws;                    // [4][16][12]
     uint32_t* cw = ws + 4 * kFastPatch;      // [8][2] current block
-    uint32_t* vis = cw + 16;                 // [3] visited lattice bits
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     const int beg = a.range ? a.range[0] : 0, n = a.range ? a.range[1] : *a.nlist;
     const int W = a.b.W, H = a.b.H, S = a.P.S;
@@ -695,7 +701,18 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         uint2 crow = make_uint2(0u, 0u);
         if (lane < 8)
             crow = __ldg(reinterpret_cast<const uint2*>(a.b.luma + (ocur + uint32_t(y0 + lane) * W + uint32_t(x0))));
+        // a candidate's 16 x 32-byte reference patch into slot `slot` (cp.async:
+        // lane = patch row x 16-byte chunk; zero-fill outside the frame)
+        auto stage = [&](int slot, int cpx, int cpy) {
+            const int r = lane >> 1, ch = lane & 1;
+            const int cs = ((x0 + cpx - 4) & ~15) + 16 * ch;
+            const int y = clampi(y0 + cpy - 4 + r, 0, H - 1);
+            const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
+            const bool in = cs >= 0 && cs + 16 <= W;
+            cp_async16(patch + slot * kFastPatch + r * kFastPWW + 4 * ch, in ? rowp + cs : rowp, in);
+        };
         uint32_t mvw = 0;
+        bool b_early;
         {
             int back = -1;  // records back from g: A 1, B cols, C cols - 1, T rows * cols
             if (lane == 0 && h > 0) back = 1;
@@ -708,6 +725,11 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                 const int i = v * int(cols) + h;
                 mvw = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
             }
+            // B lies two wavefront steps back and is usually final already: its
+            // patch (slot 1) goes out before the wait for A, C and T
+            const uint32_t mb = __shfl_sync(0xFFFFFFFFu, mvw, 1);
+            b_early = mb != kSentinel;
+            if (b_early) stage(1, clip_comp(mv_dx(mb), lo_x, hi_x) >> 1, clip_comp(mv_dy(mb), lo_y, hi_y) >> 1);
             // warp-uniform wait (a vote per poll keeps the warp converged)
             while (__any_sync(0xFFFFFFFFu, back >= 0 && mvw == kSentinel)) {
                 __nanosleep(a.poll_ns);
@@ -722,16 +744,26 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         // my candidate (lanes 8c..8c+7 serve candidate c), clip_to_window (:275-276)
         const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
         const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
-        // duplicate candidates share a patch
+        // duplicate candidates share a patch: B's slot first (it may be staged
+        // already), else the first equal candidate's
         int md = c;
+        {
+            const int bx = __shfl_sync(0xFFFFFFFFu, myx, 8), by = __shfl_sync(0xFFFFFFFFu, myy, 8);
 #pragma unroll
-        for (int j = 2; j >= 0; --j) {
-            const int jx = __shfl_sync(0xFFFFFFFFu, myx, 8 * j), jy = __shfl_sync(0xFFFFFFFFu, myy, 8 * j);
-            if (j < c && jx == myx && jy == myy) md = j;
+            for (int j = 2; j >= 0; --j) {
+                const int jx = __shfl_sync(0xFFFFFFFFu, myx, 8 * j), jy = __shfl_sync(0xFFFFFFFFu, myy, 8 * j);
+                if (j < c && jx == myx && jy == myy) md = j;
+            }
+            if (bx == myx && by == myy) md = 1;
         }
-        // --- round B: all loads of the distinct candidates' patches (16-byte
-        // chunks, two lanes per patch row) and of the shape rows in flight
-        // together, then the shared-memory stores
+        // --- round B: the remaining distinct patches and the shape rows in flight
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
+            const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
+            const bool own = __shfl_sync(0xFFFFFFFFu, md, 8 * cc) == cc;  // warp-uniform
+            if (own && !(cc == 1 && b_early)) stage(cc, ccx, ccy);
+        }
         const bool shape = boundary && (c < 3 || a.P.bt_shape);
         uint2 cal = make_uint2(0u, 0u);
         uint32_t ral0 = 0, ral1 = 0;
@@ -740,29 +772,10 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             cal = __ldg(reinterpret_cast<const uint2*>(a.b.alpha + (ocur + ao)));
             ld8u(a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1))), ral0, ral1);
         }
-        {
-            const int r = lane >> 1, ch = lane & 1;
-            uint4 pv[4];
-            bool pd[4];
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
-                const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
-                pd[cc] = __shfl_sync(0xFFFFFFFFu, md, 8 * cc) == cc;  // warp-uniform
-                const int cs = ((x0 + ccx - 4) & ~15) + 16 * ch;
-                const int y = clampi(y0 + ccy - 4 + r, 0, H - 1);
-                pv[cc] = make_uint4(0u, 0u, 0u, 0u);
-                if (pd[cc] && cs >= 0 && cs + 16 <= W)
-                    pv[cc] = __ldg(reinterpret_cast<const uint4*>(a.b.luma + (oref + uint32_t(y) * W + uint32_t(cs))));
-            }
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-                if (pd[cc]) *reinterpret_cast<uint4*>(patch + cc * kFastPatch + r * kFastPWW + 4 * ch) = pv[cc];
-        }
+        cp_async_wait_all();
         // shape scores (boundary blocks): my candidate, my row
         uint32_t s = 0;
         if (shape) s = ((__popc(__vcmpne4(cal.x, ral0)) + __popc(__vcmpne4(cal.y, ral1))) >> 3) * (255u * 4u);
-        if (lane < 3) vis[lane] = lane == 1 ? (1u << (4 * 9 + 4 - 32)) : 0u;  // start = bit 40
         __syncwarp();
         // --- brs_select (estimators.cpp:257-301) --------------------------------
         const uint32_t c0 = cw[2 * sub], c1 = cw[2 * sub + 1];  // my BRS row of the block
@@ -800,7 +813,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
         }
         // --- prs_refine (estimators.cpp:311-382), lazily from the patch ---------
-        int ci = 0, cj = 0;
+        int ci = 0, cj = 0, pc0 = 0, pc1 = 0, pc2 = 0;  // earlier centres (see pa_duo_kernel)
         uint32_t dpd = 1, iters = 0;
         for (int it = 0; it < a.P.max_iter; ++it) {
             if (ccost == 0) break;  // already a global minimum (:341)
@@ -814,12 +827,13 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
             const uint32_t cost = 4u * part;
             const bool lead = adm && q == 0;
-            bool fresh = false;
-            if (lead) {  // unique aggregate evaluations (:321-332)
-                const int bit = (4 + py) * 9 + 4 + px;
-                const uint32_t m = 1u << (bit & 31);
-                fresh = (atomicOr(&vis[bit >> 5], m) & m) == 0;
-            }
+            // unique aggregate evaluations (:321-332): new iff at Chebyshev
+            // distance >= 2 from every earlier centre
+            auto far = [&](int pc) { return max(abs(px + 8 - (pc & 15)), abs(py + 8 - (pc >> 4))) >= 2; };
+            bool fresh = lead;
+            if (it >= 1) fresh = fresh && far(pc0);
+            if (it >= 2) fresh = fresh && far(pc1);
+            if (it >= 3) fresh = fresh && far(pc2);
             dpd += __popc(__ballot_sync(0xFFFFFFFFu, fresh));
             const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, lead ? cost : kInf);
             if (m >= ccost) break;  // centre kept (:376)
@@ -849,6 +863,10 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                     }
                 }
             }
+            const int pc = (ci + 8) | ((cj + 8) << 4);
+            if (it == 0) pc0 = pc;
+            if (it == 1) pc1 = pc;
+            if (it == 2) pc2 = pc;
             ci += off8x(w);
             cj += off8y(w);
             ccost = m;
@@ -889,12 +907,6 @@ constexpr int kDuoPatch = kFastPR * kDuoPWW;
 constexpr int kDuoTaskWords = 4 * kDuoPatch + 16 + 4;  // patches, current block, visited
 constexpr int kDuoWarpWords = 2 * kDuoTaskWords;
 
-__device__ __forceinline__ void cp_async16(uint32_t* smem, const void* gmem, bool fill) {
-    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    const int n = fill ? 16 : 0;  // n = 0: zero-fill (patch columns outside the frame)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int THREADS, int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
