@@ -262,3 +262,33 @@ def test_pa_kernel_modes(me_gpu, port, mode, monkeypatch):
         want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
         assert_recs(recs[i], want_r, f"{mode} seq {i}")
         assert np.array_equal(stats[i], want_s)
+
+
+def test_concurrent_host_threads(me_gpu, port):
+    """Each host thread gets its own context (stream + buffers): concurrent
+    calls on distinct data stay correct, as the reference's API promises."""
+    import threading
+
+    from paper_1002_1168_b200 import synth
+
+    jobs = [(algo, bs, seed) for seed in (41, 42) for algo, bs in ((4, 8), (0, 16), (2, 16))]
+    out, errs = {}, []
+
+    def work(algo, bs, seed):
+        try:
+            luma, alpha = synth.config_sequence(1, seed, 6)
+            cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=16, block_size=bs))
+            out[(algo, bs, seed)] = (luma, alpha, me_gpu.run_sequences(cfg, luma[None], alpha[None]))
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    threads = [threading.Thread(target=work, args=j) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for (algo, bs, seed), (luma, alpha, (recs, stats)) in out.items():
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=bs), luma, alpha)
+        assert_recs(recs[0], want_r, f"algo{algo} seed{seed}")
+        assert np.array_equal(stats[0], want_s)
