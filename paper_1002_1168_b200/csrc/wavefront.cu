@@ -184,23 +184,34 @@ __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int*
             my_hi = max(my_hi, i);
         }
     }
-    s_part[threadIdx.x] = sum;
     if (ranges && my_hi >= 0) {
         atomicMin(&s_lo, my_lo);
         atomicMax(&s_hi, my_hi);
     }
+    // exclusive block scan of the per-thread sums: warp scans, then a scan of
+    // the warp totals (no serial loop over the 1024 partials)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_part[wid] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int i = 0; i < T; ++i) {
-            const int v = s_part[i];
-            s_part[i] = acc;
-            acc += v;
+    if (wid == 0) {
+        const int nw = T >> 5;
+        int w = lane < nw ? s_part[lane] : 0, wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= o) wi += y;
         }
-        offs[nbins] = acc;
+        s_part[32 + lane] = wi - w;  // exclusive warp offsets
+        if (lane == 31) offs[nbins] = wi;
     }
     __syncthreads();
-    int acc = s_part[threadIdx.x];
+    int acc = s_part[32 + wid] + incl - sum;
     for (int i = lo; i < hi; ++i) {
         offs[i] = acc;
         cursor[i * kCursorStride] = acc;
@@ -221,9 +232,6 @@ __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int*
         }
     }
 }
-
-// Scatter estimated block ids into key order (per-CTA ranges per bin keep the
-// global atomics to one per (CTA, bin)).
 
 // Scatter estimated blocks into key order as decoded list entries
 // {h | v << 16 | boundary << 31, p | seq << 16} (per-CTA ranges per bin keep
