@@ -34,7 +34,7 @@ Scratch carve(const Batch& b, int nbins, void* base) {
     s.types = p;
     p += align_up(nb);
     s.list = reinterpret_cast<uint2*>(p);
-    p += align_up((nb + size_t(nbins)) * 8);
+    p += align_up((nb + 3 * size_t(nbins)) * 8);  // + padding of every step to a multiple of 4
     s.hist = reinterpret_cast<int*>(p);
     p += align_up(size_t(nbins) * 4);
     s.offs = reinterpret_cast<int*>(p);
@@ -71,16 +71,19 @@ int pa_bins(const Batch& b) {
 size_t scratch_bytes(const Batch& b, int algo) {
     const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
     const size_t nb = size_t(b.nblocks());
-    return align_up(nb) + align_up((nb + size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
+    return align_up(nb) + align_up((nb + 3 * size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
            align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4 * kCursorStride) + 256;
 }
 
-// 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel
+// 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel, 3: fast / duo /
+// fast over the list's narrow / wide / narrow step ranges, 4: the same with
+// pa_quad_kernel for the wide range (the default for wide batches).
 // Wide wavefront steps (many independent blocks per step) are throughput-
-// bound: two blocks per warp (duo) keep more blocks in flight.  Narrow ones
-// (single sequences, small batches) are latency-bound: a whole warp per block
-// (fast) finishes each block sooner.  Measured crossover (CIF, 148 SMs):
-// between 64 and 128 sequences, i.e. ~25 000 blocks per step.
+// bound: four blocks per warp (quad) keep more blocks in flight for fewer
+// instructions per block.  Narrow ones (single sequences, small batches) are
+// latency-bound: a whole warp per block (fast) finishes each block sooner.
+// Measured crossover (CIF, 148 SMs): between 64 and 128 sequences, i.e.
+// ~25 000 blocks per step.
 
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
@@ -129,12 +132,12 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     }
     if ((e = launch_classify(ca, num_sms, st))) return e;
     if (events) cudaEventRecord(events[1], st);
-    // PA kernel choice (pa.cu): the duo kernel takes list entries in pairs, so
-    // every wavefront step is padded to an even count; the hybrid splits the
-    // list into narrow / wide / narrow step ranges.
+    // PA kernel choice (pa.cu): the duo / quad kernels take list entries in
+    // pairs / fours, so every wavefront step is padded to a multiple of 2 / 4;
+    // the hybrids split the list into narrow / wide / narrow step ranges.
     const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, prev0_integer, num_sms) : 0;
-    int* ranges = pa_mode == 3 ? s.counter + 8 : nullptr;
-    if ((e = launch_scan(s.hist, nbins, pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
+    int* ranges = pa_mode >= 3 ? s.counter + 8 : nullptr;
+    if ((e = launch_scan(s.hist, nbins, pa_mode == 4 ? 4 : pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
                          pa_wide_threshold(num_sms), ranges, st)))
         return e;
     if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st))) return e;
@@ -152,7 +155,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     if (events) cudaEventRecord(events[3], st);
     if (pred && (e = launch_mc_pred(b, recs, pred, st))) return e;
     // classify, scan, fill, the search (three launches for the PA hybrid), MC
-    if (launches) *launches = 3 + (pa_mode == 3 ? 3 : 1) + (pred ? 1 : 0);
+    if (launches) *launches = 3 + (pa_mode >= 3 ? 3 : 1) + (pred ? 1 : 0);
     if (events) cudaEventRecord(events[4], st);
     return cudaGetLastError();
 }

@@ -1170,14 +1170,282 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
             if (TRACE) {  // {claimed, dependencies ready, published (globaltimer ns), phase cycles}
                 unsigned long long* tr = a.trace + size_t(item + hf) * 4;
+                const long long c_end = clock64();
+                auto c16 = [](long long d) { return (unsigned long long)min(max(d, 0ll), 65535ll); };
                 tr[0] = t_claim;
                 tr[1] = t_ready;
-                const long long c_end = clock64();
-                tr[1] = (unsigned long long)(c_patch - c_ready) | ((unsigned long long)(c_brs - c_patch) << 32);
                 tr[2] = gtimer();
-                // SM cycles: patches staged -> BRS done (tr[1] high), -> walk done, -> published
-                tr[3] = (unsigned long long)(c_walk - c_brs) | ((unsigned long long)(c_end - c_walk) << 32);
+                // SM cycles: ready -> patches staged, -> BRS done, -> walk done, -> published
+                tr[3] = c16(c_patch - c_ready) | (c16(c_brs - c_patch) << 16) | (c16(c_walk - c_brs) << 32) |
+                        (c16(c_end - c_walk) << 48);
             }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pa_quad_kernel: pa_duo_kernel's algorithm with FOUR blocks per warp, one per
+// 8-lane group.  The per-block bookkeeping is issued once for four blocks and
+// every lane of a group evaluates one PRS neighbour over all 8 block rows, so
+// the walk needs no cross-lane SAD reduction.  Patches are 16 rows x 24 bytes
+// (three 8-byte cp.async chunks): the block's 8 columns plus the walk's +-4.
+// Lanes of a group: BRS = candidate (gl >> 1) x rows 4 (gl & 1) .. +3; PRS =
+// neighbour gl x all rows.  The sort pads every wide step to a multiple of 4.
+// ---------------------------------------------------------------------------
+
+constexpr int kQuadPWW = 6;                               // patch row stride in words (24 bytes)
+constexpr int kQuadPatch = kFastPR * kQuadPWW;            // 96 words
+constexpr int kQuadTaskWords = 4 * kQuadPatch + 16 + 8;   // patches, current block, bank skew
+constexpr int kQuadWarpWords = 4 * kQuadTaskWords;
+
+__device__ __forceinline__ void cp_async8(uint32_t* smem, const void* gmem, bool fill) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int n = fill ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
+    extern __shared__ uint32_t s_pa[];
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int grp = lane >> 3, gl = lane & 7, gb = grp << 3;
+    const uint32_t gmask = 0xFFu << gb;
+    uint32_t* patch = s_pa + wid * kQuadWarpWords + grp * kQuadTaskWords;  // [4][16][6]
+    uint32_t* cw = patch + 4 * kQuadPatch;                                 // [8][2] current block
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int beg = a.range ? a.range[0] : 0, n = a.range ? a.range[1] : *a.nlist;  // multiples of 4
+    const int W = a.b.W, H = a.b.H, S = a.P.S;
+    const uint32_t cols = a.b.cols, rows = a.b.rows, pairs = a.b.pairs;
+    const uint32_t plane = uint32_t(W) * uint32_t(H);
+    const int c = gl >> 1, hh = gl & 1;      // BRS: candidate c, block rows 4 hh .. 4 hh + 3
+    const int kx = off8x(gl), ky = off8y(gl);  // PRS: neighbour gl
+    for (int item = beg + 4 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 4 * nwarps) {
+        const uint2 e = __ldg(a.list + item + grp);
+        const bool act = e.x != kInvalidEntry;  // uniform per group
+        if (!__any_sync(FULL, act)) continue;
+        const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
+        const uint32_t seq = e.y >> 16;
+        const bool boundary = (e.x & kBoundaryBit) != 0;
+        const uint32_t pair = seq * pairs + uint32_t(p);
+        const uint32_t g = (pair * rows + uint32_t(v)) * cols + uint32_t(h);
+        const uint32_t oref = (seq * uint32_t(a.b.F) + uint32_t(p)) * plane, ocur = oref + uint32_t(a.b.d) * plane;
+        const int x0 = h * 8, y0 = v * 8;
+        const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
+        const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
+        // --- round A: current row gl + MV words (gl 0..3) ---------------------
+        uint2 crow = make_uint2(0u, 0u);
+        if (act) crow = __ldg(reinterpret_cast<const uint2*>(a.b.luma + (ocur + uint32_t(y0 + gl) * W + uint32_t(x0))));
+        uint32_t mvw = 0;
+        {
+            int back = -1;  // records back from g: A 1, B cols, C cols - 1, T rows * cols
+            if (act && gl == 0 && h > 0) back = 1;
+            if (act && gl == 1 && v > 0) back = int(cols);
+            if (act && gl == 2 && v > 0 && uint32_t(h) + 1 < cols) back = int(cols) - 1;
+            if (act && gl == 3 && p > 0) back = int(rows * cols);
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(a.recs + (g - uint32_t(back)));
+            if (back >= 0) mvw = ld_relaxed(src);
+            while (__any_sync(FULL, back >= 0 && mvw == kSentinel)) {
+                __nanosleep(a.poll_ns);
+                if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
+            }
+        }
+        cw[2 * gl] = crow.x;
+        cw[2 * gl + 1] = crow.y;
+        // my candidate, clip_to_window (:275-276); duplicates share a patch
+        const uint32_t mine = __shfl_sync(FULL, mvw, gb + c);
+        const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
+        int md = c;
+        {
+            const int bx = __shfl_sync(FULL, myx, gb + 2), by = __shfl_sync(FULL, myy, gb + 2);
+#pragma unroll
+            for (int j = 2; j >= 0; --j) {
+                const int jx = __shfl_sync(FULL, myx, gb + 2 * j), jy = __shfl_sync(FULL, myy, gb + 2 * j);
+                if (j < c && jx == myx && jy == myy) md = j;
+            }
+            if (bx == myx && by == myy) md = 1;
+        }
+        // --- round B: the distinct candidates' patches + the shape rows --------
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const int ccx = __shfl_sync(FULL, myx, gb + 2 * cc) >> 1;
+            const int ccy = __shfl_sync(FULL, myy, gb + 2 * cc) >> 1;
+            const bool own = __shfl_sync(FULL, md, gb + 2 * cc) == cc;  // uniform per group
+            if (act && own) {
+                const int cs = (x0 + ccx - 4) & ~7;
+                uint32_t* dst = patch + cc * kQuadPatch;
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int r = gl + 8 * rr;
+                    const int y = clampi(y0 + ccy - 4 + r, 0, H - 1);
+                    const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const int col = cs + 8 * ch;
+                        const bool in = col >= 0 && col + 8 <= W;
+                        cp_async8(dst + r * kQuadPWW + 2 * ch, in ? rowp + col : rowp, in);
+                    }
+                }
+            }
+        }
+        const bool shape = act && boundary && (c < 3 || a.P.bt_shape);
+        uint32_t sh_cnt = 0;
+        if (shape) {
+            const uint32_t ao = uint32_t(y0 + 4 * hh) * W + uint32_t(x0);
+            const uint8_t* cap = a.b.alpha + (ocur + ao);
+            const uint8_t* rap = a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1)));
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint2 ca = __ldg(reinterpret_cast<const uint2*>(cap + r * W));
+                uint32_t r0, r1;
+                ld8u(rap + r * W, r0, r1);
+                sh_cnt += __popc(__vcmpne4(ca.x, r0)) + __popc(__vcmpne4(ca.y, r1));
+            }
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        // --- brs_select (estimators.cpp:257-301) ------------------------------
+        uint32_t s;
+        if (shape) {
+            s = (sh_cnt >> 3) * (255u * 4u);
+        } else {
+            const int po = (x0 + (myx >> 1) - 4) & 7;
+            const uint32_t* pr = patch + md * kQuadPatch + (4 + 4 * hh) * kQuadPWW;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint2 cr = *reinterpret_cast<const uint2*>(cw + 8 * hh + 2 * r);
+                uint32_t w0, w1;
+                prow8(pr + r * kQuadPWW, 4 + po, w0, w1);
+                acc = vad4(cr.y, w1, vad4(cr.x, w0, acc));
+            }
+            s = acc * 4u;
+        }
+        s += __shfl_xor_sync(FULL, s, 1);  // the candidate's 2 lanes
+        uint32_t best = __shfl_sync(FULL, s, gb);
+        int win = 0;
+#pragma unroll
+        for (int i = 1; i < 4; ++i) {
+            const uint32_t si = __shfl_sync(FULL, s, gb + 2 * i);
+            if (si < best) {  // strict <: A, B, C, T tie order (:295)
+                best = si;
+                win = i;
+            }
+        }
+        const bool win_shape = boundary && (win < 3 || a.P.bt_shape);
+        const int wx = __shfl_sync(FULL, myx, gb + 2 * win), wy = __shfl_sync(FULL, myy, gb + 2 * win);
+        const int wp = __shfl_sync(FULL, md, gb + 2 * win);
+        const uint32_t* pw = patch + wp * kQuadPatch;
+        const int wo = (x0 + (wx >> 1) - 4) & 7;  // the winner patch's byte offset
+        uint32_t ccost = best;
+        if (__any_sync(FULL, act && win_shape)) {  // the centre's texture cost was not computed by BRS
+            uint32_t t = 0;
+            if (c == 0) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint2 cr = *reinterpret_cast<const uint2*>(cw + 8 * hh + 2 * r);
+                    uint32_t w0, w1;
+                    prow8(pw + (4 + 4 * hh + r) * kQuadPWW, 4 + wo, w0, w1);
+                    t = vad4(cr.y, w1, vad4(cr.x, w0, t));
+                }
+            }
+            t += __shfl_xor_sync(FULL, t, 1);
+            t = __shfl_sync(FULL, t, gb);
+            if (win_shape) ccost = 4u * t;
+        }
+        // --- prs_refine (estimators.cpp:311-382), lazily from the patch -------
+        int ci = 0, cj = 0;
+        uint32_t dpd = 1, iters = 0;
+        bool alive = act;
+        int pc0 = 0, pc1 = 0, pc2 = 0;  // earlier centres, packed (x + 8) | (y + 8) << 4 (see pa_duo_kernel)
+        for (int it = 0; it < a.P.max_iter; ++it) {
+            alive = alive && ccost != 0;  // already a global minimum (:341)
+            if (!__any_sync(FULL, alive)) break;
+            const int px = ci + kx, py = cj + ky;
+            const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
+            const uint32_t* pr = pw + (4 + py) * kQuadPWW;
+            const int tt = 4 + px + wo;
+            uint32_t part = 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint2 cr = *reinterpret_cast<const uint2*>(cw + 2 * r);
+                uint32_t w0, w1;
+                prow8(pr + r * kQuadPWW, tt, w0, w1);
+                part = vad4(cr.y, w1, vad4(cr.x, w0, part));
+            }
+            const uint32_t cost = 4u * part;
+            const bool lead = alive && adm;
+            bool fresh = lead;
+            auto far = [&](int pc) { return max(abs(px + 8 - (pc & 15)), abs(py + 8 - (pc >> 4))) >= 2; };
+            if (it >= 1) fresh = fresh && far(pc0);
+            if (it >= 2) fresh = fresh && far(pc1);
+            if (it >= 3) fresh = fresh && far(pc2);
+            dpd += __popc(__ballot_sync(FULL, fresh) & gmask);
+            uint32_t m = lead ? cost : kInf;  // the group's minimum
+            m = min(m, __shfl_xor_sync(FULL, m, 1));
+            m = min(m, __shfl_xor_sync(FULL, m, 2));
+            m = min(m, __shfl_xor_sync(FULL, m, 4));
+            const bool move = alive && m < ccost;  // else the centre is kept (:376)
+            const uint32_t ties = (__ballot_sync(FULL, lead && cost == m) & gmask) >> gb;
+            int w = __ffs(ties) - 1;
+            const bool tie = move && __popc(ties) > 1;
+            if (__any_sync(FULL, tie)) {
+                // stable descending sort by off . dir (:357-362), the full warp
+                // for each group that needs it
+#pragma unroll 1
+                for (int t = 0; t < 4; ++t) {
+                    if (!__shfl_sync(FULL, tie, 8 * t)) continue;  // warp-uniform
+                    PaBlock B;
+                    B.cur = a.b.luma + __shfl_sync(FULL, ocur, 8 * t);
+                    B.ref = a.b.luma + __shfl_sync(FULL, oref, 8 * t);
+                    B.ca = B.ra = nullptr;
+                    B.x0 = __shfl_sync(FULL, x0, 8 * t);
+                    B.y0 = __shfl_sync(FULL, y0, 8 * t);
+                    const int cx = __shfl_sync(FULL, wx + 2 * ci, 8 * t), cy = __shfl_sync(FULL, wy + 2 * cj, 8 * t);
+                    double dir_x, dir_y;
+                    prs_direction(a.P, B, lane, cx, cy, dir_x, dir_y);
+                    if (grp == t) {
+                        int wb = -1;
+                        double bestkey = 0.0;
+                        for (int o = 0; o < 8; ++o) {
+                            if (!((ties >> o) & 1u)) continue;
+                            const double key = __dadd_rn(__dmul_rn(double(c_off8[o][0]), dir_x), __dmul_rn(double(c_off8[o][1]), dir_y));
+                            if (wb < 0 || key > bestkey) {
+                                wb = o;
+                                bestkey = key;
+                            }
+                        }
+                        w = wb;
+                    }
+                }
+            }
+            const int pc = (ci + 8) | ((cj + 8) << 4);
+            if (it == 0) pc0 = pc;
+            if (it == 1) pc1 = pc;
+            if (it == 2) pc2 = pc;
+            if (move) {
+                ci += off8x(w);
+                cj += off8y(w);
+                ccost = m;
+                ++iters;
+            }
+            alive = move;
+        }
+        // --- fused predict_frame + psnr SSE at the final vector ---------------
+        uint32_t se;
+        {
+            uint32_t w0, w1;
+            prow8(pw + (4 + cj + gl) * kQuadPWW, 4 + ci + wo, w0, w1);
+            se = sq4(cw[2 * gl + 1], w1, sq4(cw[2 * gl], w0, 0u));
+            se += __shfl_xor_sync(FULL, se, 1);
+            se += __shfl_xor_sync(FULL, se, 2);
+            se += __shfl_xor_sync(FULL, se, 4);
+        }
+        if (act && gl == 0) {
+            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
+            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
+            if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
         }
         __syncwarp();
     }
@@ -1612,9 +1880,10 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
     if (mode && std::string(mode) == "fast") return 1;
     if (prev0) return 1;  // the two-blocks-per-warp kernel takes no external prev field
     if (mode && std::string(mode) == "duo") return 2;
-    if (mode && std::string(mode) == "hybrid") return 3;
+    if (mode && std::string(mode) == "duo-hybrid") return 3;
+    if (mode && (std::string(mode) == "hybrid" || std::string(mode) == "quad")) return 4;
     const int64_t per_step = b.nblocks() / std::max(1, b.steps());
-    return per_step >= int64_t(num_sms) * 160 ? 3 : 1;
+    return per_step >= int64_t(num_sms) * 160 ? 4 : 1;
 }
 
 // One small pair in one CTA (pa_smem_kernel) when it fits in shared memory;
@@ -1710,6 +1979,14 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         e = launch(fast, 256, kFastWarpWords, nullptr);
     } else if (pa_mode == 2) {
         e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, nullptr);
+    } else if (pa_mode == 4) {  // narrow steps -> fast, the wide middle -> quad, narrow tail -> fast
+        // 3 CTAs (24 warps, 96 blocks in flight) per SM at 80 registers:
+        // measured 8 % faster than 4 at 64 (spills) and 1 % than 2 at 112
+        const char* qm = getenv("ME_PA_QMINB");
+        const int mb = qm ? atoi(qm) : 3;
+        PaKernel quad = mb == 4 ? pa_quad_kernel<4> : mb == 2 ? pa_quad_kernel<2> : pa_quad_kernel<3>;
+        if (!(e = launch(fast, 256, kFastWarpWords, ranges)) && !(e = launch(quad, 256, kQuadWarpWords, ranges + 2)))
+            e = launch(fast, 256, kFastWarpWords, ranges + 4);
     } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast
         if (!(e = launch(fast, 256, kFastWarpWords, ranges)) &&
             !(e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, ranges + 2)))

@@ -246,11 +246,12 @@ def test_estimate_field_random_prev(me_gpu, port, odd):
     assert_recs(recs, want)
 
 
-@pytest.mark.parametrize("mode", ["fast", "duo", "hybrid", "warp"])
+@pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid", "warp"])
 def test_pa_kernel_modes(me_gpu, port, mode, monkeypatch):
     """Every PA kernel schedule (one block per warp, two per warp, the hybrid
-    split of the sorted list, the generic kernel) on the same batch; the
-    hybrid's wide threshold is lowered so all three of its ranges are used."""
+    splits of the sorted list with two or four blocks per warp in the wide
+    range, the generic kernel) on the same batch; the hybrids' wide threshold
+    is lowered so all three of their ranges are used."""
     from paper_1002_1168_b200 import synth
 
     monkeypatch.setenv("ME_PA_MODE", mode)

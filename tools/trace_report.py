@@ -33,9 +33,9 @@ dT = dep(seq, p - 1, v, h, p > 0)
 dmax = np.maximum.reduce([dA, dB, dC, dT])
 has = dmax > -1e8
 print("tasks", len(tr), "span us %.1f" % done.max(), "steps", step.max() + 1)
-patch = (tr[:, 3] - t0) / 1e3
-print("ready->patches staged us: mean %.2f p50 %.2f p90 %.2f" % ((patch - ready).mean(), *np.percentile(patch - ready, [50, 90])))
-print("patches->done us:         mean %.2f p50 %.2f p90 %.2f" % ((done - patch).mean(), *np.percentile(done - patch, [50, 90])))
+cyc = np.stack([(tr[:, 3] >> (16 * i)) & 0xFFFF for i in range(4)], 1).astype(np.float64)
+for i, name in enumerate(["ready->staged", "staged->brs", "brs->walked", "walked->published"]):
+    print("cycles %-18s mean %7.0f p50 %7.0f p90 %7.0f" % (name, cyc[:, i].mean(), *np.percentile(cyc[:, i], [50, 90])))
 print("work (ready->done) us: mean %.2f p50 %.2f p90 %.2f p99 %.2f" % ((done - ready).mean(), *np.percentile(done - ready, [50, 90, 99])))
 print("claim->ready us:       mean %.2f p50 %.2f p90 %.2f" % ((ready - claim).mean(), *np.percentile(ready - claim, [50, 90])))
 late = ready[has] - dmax[has]
