@@ -1205,7 +1205,7 @@ __device__ __forceinline__ void cp_async8(uint32_t* smem, const void* gmem, bool
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
 }
 
-template <int MINB>
+template <int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
     extern __shared__ uint32_t s_pa[];
     constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -1224,6 +1224,9 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
     for (int item = beg + 4 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 4 * nwarps) {
         const uint2 e = __ldg(a.list + item + grp);
         const bool act = e.x != kInvalidEntry;  // uniform per group
+        unsigned long long t_claim = 0, t_ready = 0;
+        long long c_ready = 0, c_patch = 0, c_brs = 0, c_walk = 0;
+        if (TRACE) t_claim = gtimer();
         if (!__any_sync(FULL, act)) continue;
         const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
         const uint32_t seq = e.y >> 16;
@@ -1251,6 +1254,10 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
                 if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
             }
         }
+        if (TRACE) {
+            t_ready = gtimer();
+            c_ready = clock64();
+        }
         cw[2 * gl] = crow.x;
         cw[2 * gl + 1] = crow.y;
         // my candidate, clip_to_window (:275-276); duplicates share a patch
@@ -1273,19 +1280,17 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             const int ccy = __shfl_sync(FULL, myy, gb + 2 * cc) >> 1;
             const bool own = __shfl_sync(FULL, md, gb + 2 * cc) == cc;  // uniform per group
             if (act && own) {
+                // 16 rows x 3 chunks; consecutive lanes take consecutive chunks
                 const int cs = (x0 + ccx - 4) & ~7;
                 uint32_t* dst = patch + cc * kQuadPatch;
 #pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    const int r = gl + 8 * rr;
+                for (int k = 0; k < 6; ++k) {
+                    const int ci8 = gl + 8 * k, r = ci8 / 3, ch = ci8 - 3 * r;
                     const int y = clampi(y0 + ccy - 4 + r, 0, H - 1);
+                    const int col = cs + 8 * ch;
+                    const bool in = col >= 0 && col + 8 <= W;
                     const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) {
-                        const int col = cs + 8 * ch;
-                        const bool in = col >= 0 && col + 8 <= W;
-                        cp_async8(dst + r * kQuadPWW + 2 * ch, in ? rowp + col : rowp, in);
-                    }
+                    cp_async8(dst + r * kQuadPWW + 2 * ch, in ? rowp + col : rowp, in);
                 }
             }
         }
@@ -1305,6 +1310,7 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
         }
         cp_async_wait_all();
         __syncwarp();
+        if (TRACE) c_patch = clock64();
         // --- brs_select (estimators.cpp:257-301) ------------------------------
         uint32_t s;
         if (shape) {
@@ -1312,15 +1318,17 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
         } else {
             const int po = (x0 + (myx >> 1) - 4) & 7;
             const uint32_t* pr = patch + md * kQuadPatch + (4 + 4 * hh) * kQuadPWW;
-            uint32_t acc = 0;
+            uint32_t acc0 = 0, acc1 = 0;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const uint2 cr = *reinterpret_cast<const uint2*>(cw + 8 * hh + 2 * r);
-                uint32_t w0, w1;
+            for (int r = 0; r < 4; r += 2) {
+                const uint4 cr = *reinterpret_cast<const uint4*>(cw + 8 * hh + 2 * r);
+                uint32_t w0, w1, w2, w3;
                 prow8(pr + r * kQuadPWW, 4 + po, w0, w1);
-                acc = vad4(cr.y, w1, vad4(cr.x, w0, acc));
+                prow8(pr + (r + 1) * kQuadPWW, 4 + po, w2, w3);
+                acc0 = vad4(cr.y, w1, vad4(cr.x, w0, acc0));
+                acc1 = vad4(cr.w, w3, vad4(cr.z, w2, acc1));
             }
-            s = acc * 4u;
+            s = (acc0 + acc1) * 4u;
         }
         s += __shfl_xor_sync(FULL, s, 1);  // the candidate's 2 lanes
         uint32_t best = __shfl_sync(FULL, s, gb);
@@ -1354,6 +1362,7 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             t = __shfl_sync(FULL, t, gb);
             if (win_shape) ccost = 4u * t;
         }
+        if (TRACE) c_brs = clock64();
         // --- prs_refine (estimators.cpp:311-382), lazily from the patch -------
         int ci = 0, cj = 0;
         uint32_t dpd = 1, iters = 0;
@@ -1366,15 +1375,17 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
             const uint32_t* pr = pw + (4 + py) * kQuadPWW;
             const int tt = 4 + px + wo;
-            uint32_t part = 0;
+            uint32_t part0 = 0, part1 = 0;  // two accumulation chains
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint2 cr = *reinterpret_cast<const uint2*>(cw + 2 * r);
-                uint32_t w0, w1;
+            for (int r = 0; r < 8; r += 2) {
+                const uint4 cr = *reinterpret_cast<const uint4*>(cw + 2 * r);
+                uint32_t w0, w1, w2, w3;
                 prow8(pr + r * kQuadPWW, tt, w0, w1);
-                part = vad4(cr.y, w1, vad4(cr.x, w0, part));
+                prow8(pr + (r + 1) * kQuadPWW, tt, w2, w3);
+                part0 = vad4(cr.y, w1, vad4(cr.x, w0, part0));
+                part1 = vad4(cr.w, w3, vad4(cr.z, w2, part1));
             }
-            const uint32_t cost = 4u * part;
+            const uint32_t cost = 4u * (part0 + part1);
             const bool lead = alive && adm;
             bool fresh = lead;
             auto far = [&](int pc) { return max(abs(px + 8 - (pc & 15)), abs(py + 8 - (pc >> 4))) >= 2; };
@@ -1432,6 +1443,7 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             }
             alive = move;
         }
+        if (TRACE) c_walk = clock64();
         // --- fused predict_frame + psnr SSE at the final vector ---------------
         uint32_t se;
         {
@@ -1446,6 +1458,16 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
+            if (TRACE) {  // as pa_duo_kernel
+                unsigned long long* tr = a.trace + size_t(item + grp) * 4;
+                const long long c_end = clock64();
+                auto c16 = [](long long d) { return (unsigned long long)min(max(d, 0ll), 65535ll); };
+                tr[0] = t_claim;
+                tr[1] = t_ready;
+                tr[2] = gtimer();
+                tr[3] = c16(c_patch - c_ready) | (c16(c_brs - c_patch) << 16) | (c16(c_walk - c_brs) << 32) |
+                        (c16(c_end - c_walk) << 48);
+            }
         }
         __syncwarp();
     }
@@ -1985,6 +2007,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         const char* qm = getenv("ME_PA_QMINB");
         const int mb = qm ? atoi(qm) : 3;
         PaKernel quad = mb == 4 ? pa_quad_kernel<4> : mb == 2 ? pa_quad_kernel<2> : pa_quad_kernel<3>;
+        if (trace_path) quad = pa_quad_kernel<3, true>;
         if (!(e = launch(fast, 256, kFastWarpWords, ranges)) && !(e = launch(quad, 256, kQuadWarpWords, ranges + 2)))
             e = launch(fast, 256, kFastWarpWords, ranges + 4);
     } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast
