@@ -392,7 +392,7 @@ def main():
     if algo == "PA":
         ach = alg_bytes / (pipe_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": f"pipeline classify+scan+fill+PA wavefront search ({launches_per_step} launches/step)", "achieved": ach, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic, "traffic_by_kernel": traffic_src["dram_bytes"] if traffic_src else None, "algorithmic_bytes_per_step": alg_bytes, "pipeline_ms": pipe_ms,
-                "dominant": {"kernel": "pa_duo_kernel (wavefront search)", "ms": float(stage_ms[2]), "share": float(stage_ms[2]) / pipe_ms, "bound": "dependency latency + issue (see DESIGN.md)"}}
+                "dominant": {"kernel": "pa_fast + pa_quad + pa_fast (wavefront search)", "ms": float(stage_ms[2]), "share": float(stage_ms[2]) / pipe_ms, "bound": "dependency latency + issue (see DESIGN.md)"}}
     else:
         cmp_total = int(hstat["block_comparisons"].sum())
         ops = cmp_total * bs * bs  # SAD byte-ops of the search stage

@@ -8,7 +8,7 @@ timeout 300 python bench.py --workload cfg5-es --frames 4 --steps 3 --warmup 3 -
 CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
 $CMD > gpurun_out/ev/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/ev/launches.csv $CMD > gpurun_out/ev/ncu_launch.log 2>&1; echo launches rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"pa_duo_kernel" -s 1 -c 1 -o gpurun_out/ev/pa_duo $CMD > gpurun_out/ev/ncu_pa.log 2>&1; echo ncu_pa rc=$?
+ncu --set full --clock-control none --import-source on -k regex:"pa_quad_kernel" -s 1 -c 1 -o gpurun_out/ev/pa_quad $CMD > gpurun_out/ev/ncu_pa.log 2>&1; echo ncu_pa rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"classify_kernel" -s 3 -c 1 -o gpurun_out/ev/classify $CMD > gpurun_out/ev/ncu_cls.log 2>&1; echo ncu_cls rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"pa_fast_kernel" -s 2 -c 1 -o gpurun_out/ev/pa_fast $CMD > gpurun_out/ev/ncu_fast.log 2>&1; echo ncu_fast rc=$?
 for f in gpurun_out/ev/*.log; do tail -n 2 $f; done
