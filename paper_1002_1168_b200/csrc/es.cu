@@ -76,41 +76,44 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         CW += ((8 - (CW & 31)) + 32) & 31;  // copy stride = 8 (mod 32) words: conflict-free lanes
         const int row_g0 = y0 + lo_y + run0 * K;  // frame row of staged row 0
         const int rows_valid = min(srows, WY + BS - 1 - run0 * K);
-        const uint8_t* rb = ref + size_t(row_g0) * W + (x0 + lo_x);
+        // the frame's words (32-bit offsets: a frame is < 4 GB); ref is 4-byte
+        // aligned when W % 4 == 0 (checked by the launcher's caller)
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(ref) & ~uintptr_t(3));
+        const uint32_t ref_mis = uint32_t(reinterpret_cast<uintptr_t>(ref) & 3);
+        const uint32_t seg0 = ref_mis + uint32_t(row_g0) * uint32_t(W) + uint32_t(x0 + lo_x);  // byte offset from rw
         __syncthreads();  // previous band / block done with smem
         // staging from aligned words: copy s, word q = bytes [4q + s, 4q + s + 4)
         // of the row segment = a funnel shift of two aligned words.  Bytes past
         // the segment are never paired with the current block (only rows and
         // columns of admissible positions are summed), so the loads clamp to
         // the segment's last aligned word and rows past the window are skipped.
-        for (int row = tid / PW, q = tid - (tid / PW) * PW; row < srows;) {
-            if (row < rows_valid) {
-                const uint8_t* seg = rb + size_t(row) * W;
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(seg) & ~uintptr_t(3);
-                const uint32_t off = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3);
-                const uintptr_t last = (reinterpret_cast<uintptr_t>(seg) + rowbytes - 1) & ~uintptr_t(3);
-                uint32_t g[3];
-#pragma unroll
-                for (int m = 0; m < 3; ++m) {
-                    const uintptr_t ad = min(a0 + 4 * uintptr_t(q + m), last);
-                    g[m] = __ldg(reinterpret_cast<const uint32_t*>(ad));
-                }
-#pragma unroll
-                for (int sft = 0; sft < 4; ++sft) {
-                    const uint32_t t = off + sft;  // 0..6
-                    const uint32_t lo = t < 4 ? g[0] : g[1], hi = t < 4 ? g[1] : g[2];
-                    sm[sft * CW + row * PW + q] = __funnelshift_r(lo, hi, (t & 3) * 8);
-                }
-            }
-            q += blockDim.x;
-            while (q >= PW) {
-                q -= PW;
-                ++row;
+        // Flat index i = row * PW + q (row by a float reciprocal: exact, since
+        // (i + 0.5) / PW is never within 0.5 / PW of an integer).
+        {
+            const int total = rows_valid * PW;
+            const float inv_pw = 1.0f / float(PW);
+            uint32_t* const sm1 = sm + CW;
+            uint32_t* const sm2 = sm + 2 * CW;
+            uint32_t* const sm3 = sm + 3 * CW;
+            for (int i = tid; i < total; i += kEsThreads) {
+                const int row = __float2int_rz((float(i) + 0.5f) * inv_pw), q = i - row * PW;
+                const uint32_t b0 = seg0 + uint32_t(row) * uint32_t(W);
+                const uint32_t w0 = b0 >> 2, off = b0 & 3u, wl = (b0 + uint32_t(rowbytes) - 1) >> 2;
+                const uint32_t g0 = __ldg(rw + min(w0 + q, wl)), g1 = __ldg(rw + min(w0 + q + 1, wl)),
+                               g2 = __ldg(rw + min(w0 + q + 2, wl));
+                const uint32_t sh = off * 8;
+                // copies s = 0..3: byte offset off + s within (g0, g1, g2)
+                sm[i] = __funnelshift_r(g0, g1, sh);
+                sm1[i] = off + 1 < 4 ? __funnelshift_r(g0, g1, sh + 8) : g1;
+                sm2[i] = off + 2 < 4 ? __funnelshift_r(g0, g1, sh + 16) : __funnelshift_r(g1, g2, sh - 16);
+                sm3[i] = off == 0 ? __funnelshift_r(g0, g1, 24) : __funnelshift_r(g1, g2, sh - 8);
             }
         }
         __syncthreads();
-        // tasks (run, col) in raster order, walked incrementally (no division)
-        for (int run = tid / WX, col = tid - (tid / WX) * WX; run < bruns;) {
+        // tasks (run, col) in raster order: flat index, run by a float reciprocal
+        const float inv_wx = 1.0f / float(WX);
+        for (int ti = tid, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX; run < bruns;
+             ti += kEsThreads, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX) {
             const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
             uint32_t acc[K];
 #pragma unroll
@@ -148,11 +151,6 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
                                                (static_cast<unsigned long long>((m32 >> 3) & 0xFFu) << 24) |
                                                static_cast<unsigned long long>(wy * uint32_t(WX) + uint32_t(col));
                 best = key < best ? key : best;
-            }
-            col += blockDim.x;
-            while (col >= WX) {
-                col -= WX;
-                ++run;
             }
         }
     }
