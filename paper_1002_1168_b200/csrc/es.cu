@@ -38,7 +38,10 @@ struct EsArgs {
 
 constexpr int kEsThreads = 256;
 
-template <int BS, int K>
+// PWC: the staged row stride in words when known at compile time (the
+// launcher instantiates the common search ranges; every row offset in the SAD
+// loop is then an immediate), 0 = computed from the clipped window.
+template <int BS, int K, int PWC = 0>
 __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
                          int S, int band_runs_max, uint32_t* sm, unsigned long long* s_best,
                          int& out_dx, int& out_dy, uint32_t& out_sad, uint32_t& out_cmp) {
@@ -48,7 +51,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
     const int WX = hi_x - lo_x + 1, WY = hi_y - lo_y + 1;
     const int nruns = (WY + K - 1) / K;
     const int rowbytes = WX + BS - 1;
-    const int PW = ((WX - 1) >> 2) + (BS >> 2) + 1;  // words per staged row
+    const int PW = PWC ? PWC : ((WX - 1) >> 2) + (BS >> 2) + 1;  // words per staged row (>= the window's)
     constexpr int NW = BS / 4;
 
     uint32_t c[BS][NW];
@@ -172,7 +175,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
     }
 }
 
-template <int BS, int K>
+template <int BS, int K, int PWC>
 __global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ unsigned long long s_best[kEsThreads / 32];
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
         const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
         int dx, dy;
         uint32_t sad, cmp;
-        es_block<BS, K>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, s_best, dx, dy,
+        es_block<BS, K, PWC>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, s_best, dx, dy,
                         sad, cmp);
         if (threadIdx.x == 0) {
             s_res[0] = dx;
@@ -271,7 +274,15 @@ cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist
     ea.band_rows_max = es_band_rows(b.bs, S, b.W, b.H);
     ea.stats = stats;
     const size_t smem = es_smem_bytes(b.bs, S, b.W, b.H);
-    auto kern = b.bs == 16 ? es_kernel<16, 8> : es_kernel<8, 8>;
+    // the row stride of the widest (unclipped) window, fixed for every block
+    const int PW = ((min(2 * S + 1, b.W - b.bs + 1) - 1) >> 2) + (b.bs >> 2) + 1;
+    void (*kern)(EsArgs);
+    if (b.bs == 16)
+        kern = PW == 37 ? es_kernel<16, 8, 37> : PW == 21 ? es_kernel<16, 8, 21> : PW == 13 ? es_kernel<16, 8, 13>
+                                                                                            : es_kernel<16, 8, 0>;
+    else
+        kern = PW == 35 ? es_kernel<8, 8, 35> : PW == 19 ? es_kernel<8, 8, 19> : PW == 11 ? es_kernel<8, 8, 11>
+                                                                                         : es_kernel<8, 8, 0>;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
     int occ = 0;
