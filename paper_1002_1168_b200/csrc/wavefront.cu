@@ -305,9 +305,10 @@ cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cur
 
 cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st) {
     const Batch& b = ca.b;
-    // <= 128 rows per CTA (fewer global atomics), >= 2 CTAs per SM
+    // <= 64 rows per CTA, >= 2 CTAs per SM
     const int64_t nrows = int64_t(b.n_seq) * b.pairs * b.rows;
-    const int64_t rpc = std::max<int64_t>(4, std::min<int64_t>(128, nrows / (2 * num_sms)));
+    const int64_t rmax = getenv("ME_FILL_RPC") ? atoi(getenv("ME_FILL_RPC")) : 64;  // measured: 64 <= 32, 128 < 256
+    const int64_t rpc = std::max<int64_t>(4, std::min<int64_t>(rmax, nrows / (2 * num_sms)));
     const int grid = int((nrows + rpc - 1) / rpc);
     const size_t smem = 2 * size_t(ca.nbins) * 4;
     cudaError_t e;
