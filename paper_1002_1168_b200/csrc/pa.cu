@@ -1,6 +1,8 @@
 // pa.cu — the proposed algorithm (estimators.cpp:238-382): gather_candidates
 // + brs_select + prs_refine as a dataflow wavefront over the sorted work list
 // (pa_fast_kernel: a warp per block; pa_duo_kernel: two blocks per warp;
+// pa_quad_kernel: four blocks per warp, the wide middle of large batches;
+// pa_smem_kernel: one small pair resident in one CTA's shared memory;
 // pa_kernel: the generic path for 16x16, half-pel and external prev fields),
 // and the single-block BRS / PRS / prs_update kernels.
 #include <cuda_runtime.h>
