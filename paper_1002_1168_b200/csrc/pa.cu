@@ -668,7 +668,7 @@ __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, 
     r1 = __funnelshift_r(w1, w2, sh);
 }
 
-template <int MINB>
+template <int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     extern __shared__ uint32_t s_pa[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -686,6 +686,9 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     for (int item = beg + blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
         const uint2 e = __ldg(a.list + item);
         if (e.x == kInvalidEntry) continue;
+        unsigned long long t_claim = 0, t_ready = 0;
+        long long c_ready = 0, c_patch = 0, c_brs = 0, c_walk = 0;
+        if (TRACE) t_claim = gtimer();
         const int h = int(e.x & 0xFFFF), v = int((e.x >> 16) & 0x7FFF), p = int(e.y & 0xFFFF);
         const uint32_t seq = e.y >> 16;
         const bool boundary = (e.x & kBoundaryBit) != 0;
@@ -738,6 +741,10 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                 if (back >= 0 && mvw == kSentinel) mvw = ld_relaxed(src);
             }
         }
+        if (TRACE) {
+            t_ready = gtimer();
+            c_ready = clock64();
+        }
         if (lane < 8) {
             cw[2 * lane] = crow.x;
             cw[2 * lane + 1] = crow.y;
@@ -779,6 +786,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         uint32_t s = 0;
         if (shape) s = ((__popc(__vcmpne4(cal.x, ral0)) + __popc(__vcmpne4(cal.y, ral1))) >> 3) * (255u * 4u);
         __syncwarp();
+        if (TRACE) c_patch = clock64();
         // --- brs_select (estimators.cpp:257-301) --------------------------------
         const uint32_t c0 = cw[2 * sub], c1 = cw[2 * sub + 1];  // my BRS row of the block
         if (!shape) {
@@ -814,6 +822,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             uint32_t t = c == 0 ? vad4(c1, w1, vad4(c0, w0, 0u)) : 0u;
             ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
         }
+        if (TRACE) c_brs = clock64();
         // --- prs_refine (estimators.cpp:311-382), lazily from the patch ---------
         int ci = 0, cj = 0, pc0 = 0, pc1 = 0, pc2 = 0;  // earlier centres (see pa_duo_kernel)
         uint32_t dpd = 1, iters = 0;
@@ -874,6 +883,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             ccost = m;
             ++iters;
         }
+        if (TRACE) c_walk = clock64();
         // --- fused predict_frame + psnr SSE at the final vector -----------------
         uint32_t se = 0;
         if (lane < 8) {
@@ -886,6 +896,16 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
             write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
+            if (TRACE) {  // as pa_duo_kernel
+                unsigned long long* tr = a.trace + size_t(item) * 4;
+                const long long c_end = clock64();
+                auto c16 = [](long long d) { return (unsigned long long)min(max(d, 0ll), 65535ll); };
+                tr[0] = t_claim;
+                tr[1] = t_ready;
+                tr[2] = gtimer();
+                tr[3] = c16(c_patch - c_ready) | (c16(c_brs - c_patch) << 16) | (c16(c_walk - c_brs) << 32) |
+                        (c16(c_end - c_walk) << 48);
+            }
         }
         __syncwarp();
     }
@@ -1984,6 +2004,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     {
         const int mb = minb ? atoi(minb) : 4;
         fast = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
+        if (trace_path) fast = pa_fast_kernel<4, true>;
     }
     const int duo_threads = cta ? atoi(cta) : 256;
     PaKernel duo = pa_duo_kernel<256, 4>;
