@@ -2002,8 +2002,14 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     };
     PaKernel fast = pa_fast_kernel<4>;
     {
-        const int mb = minb ? atoi(minb) : 4;
-        fast = mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
+        // narrow wavefronts (< 100 blocks per step per SM, e.g. single
+        // sequences and batches up to ~32 CIF sequences) are latency-bound:
+        // one CTA per SM with 128 registers per thread runs each block sooner
+        // (measured 3-6 % on configs 2, 3, 5 and 4-32 sequences); wider ones
+        // need the blocks in flight of 4 CTAs per SM
+        const int64_t per_step = b.nblocks() / std::max(1, b.steps());
+        const int mb = minb ? atoi(minb) : (pa_mode == 1 && per_step < int64_t(num_sms) * 100 ? 1 : 4);
+        fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         if (trace_path) fast = pa_fast_kernel<4, true>;
     }
     const int duo_threads = cta ? atoi(cta) : 256;
