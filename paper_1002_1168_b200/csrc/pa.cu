@@ -884,6 +884,8 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             ++iters;
         }
         if (TRACE) c_walk = clock64();
+        // publish first (the dependents wait on the record, not on the SSE)
+        if (lane == 0) write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, boundary ? ME_BOUNDARY : ME_OPAQUE);
         // --- fused predict_frame + psnr SSE at the final vector -----------------
         uint32_t se = 0;
         if (lane < 8) {
@@ -893,8 +895,6 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         }
         se = __reduce_add_sync(0xFFFFFFFFu, se);
         if (lane == 0) {
-            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
-            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
             if (TRACE) {  // as pa_duo_kernel
                 unsigned long long* tr = a.trace + size_t(item) * 4;
@@ -1175,6 +1175,9 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
         }
         long long c_walk = 0;
         if (TRACE) c_walk = clock64();
+        // publish first (the dependents wait on the record, not on the SSE)
+        if (act && hl == 0)
+            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, boundary ? ME_BOUNDARY : ME_OPAQUE);
         // --- fused predict_frame + psnr SSE at the final vector ---------------
         uint32_t se = 0;
         if (hl < 8) {
@@ -1187,8 +1190,6 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
             se = hf ? s1 : s0;
         }
         if (act && hl == 0) {
-            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
-            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
             if (TRACE) {  // {claimed, dependencies ready, published (globaltimer ns), phase cycles}
                 unsigned long long* tr = a.trace + size_t(item + hf) * 4;
@@ -1466,6 +1467,9 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             alive = move;
         }
         if (TRACE) c_walk = clock64();
+        // publish first (the dependents wait on the record, not on the SSE)
+        if (act && gl == 0)
+            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, boundary ? ME_BOUNDARY : ME_OPAQUE);
         // --- fused predict_frame + psnr SSE at the final vector ---------------
         uint32_t se;
         {
@@ -1477,8 +1481,6 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             se += __shfl_xor_sync(FULL, se, 4);
         }
         if (act && gl == 0) {
-            const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
-            write_rec_v4(a.recs + g, wx + 2 * ci, wy + 2 * cj, ccost, 4, dpd, iters, ty);
             if (a.stats) add_stats_pa(a.stats + pair, se, dpd);
             if (TRACE) {  // as pa_duo_kernel
                 unsigned long long* tr = a.trace + size_t(item + grp) * 4;
