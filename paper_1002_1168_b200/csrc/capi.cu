@@ -155,6 +155,51 @@ bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst) {
     return !bad;
 }
 
+// The sparse form (kernels.h: unpack_mask_sparse) of a binary mask, n % 64 ==
+// 0: packs 64 pixels per AVX-512 step (or 8 per scalar step) into tmp, then
+// keeps only the nonzero 64-pixel words.  Returns the encoded size in bytes,
+// or 0 when the mask is not binary.
+size_t pack_sparse_mask(const uint8_t* src, size_t n, uint8_t* dst, uint64_t* tmp) {
+    static const bool avx512 = __builtin_cpu_supports("avx512bw");
+    const int64_t nwords = int64_t(n / 64), ngroups = (nwords + 31) / 32;
+    uint32_t* pres = reinterpret_cast<uint32_t*>(dst);
+    uint32_t* base = pres + ngroups;
+    uint64_t* lit = reinterpret_cast<uint64_t*>(dst + mek::sparse_mask_header_bytes(n));
+    int bad = 0;
+    std::vector<int64_t> tcount(size_t(omp_get_max_threads()) + 1, 0);
+    int nthreads = 1;
+#pragma omp parallel reduction(| : bad)
+    {
+        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+#pragma omp single
+        nthreads = nt;
+        const int64_t g0 = ngroups * t / nt, g1 = ngroups * (t + 1) / nt;
+        const int64_t w0 = g0 * 32, w1 = std::min(nwords, g1 * 32);
+        if (avx512)
+            bad |= pack_range_avx512(src, w0, w1, reinterpret_cast<uint8_t*>(tmp));
+        else
+            bad |= pack_range_scalar(src, 8 * w0, 8 * w1, reinterpret_cast<uint8_t*>(tmp));
+        int64_t cnt = 0;
+        for (int64_t g = g0; g < g1; ++g) {
+            uint32_t m = 0;
+            for (int64_t i = 0; i < 32 && g * 32 + i < nwords; ++i) m |= uint32_t(tmp[g * 32 + i] != 0) << i;
+            pres[g] = m;
+            cnt += __builtin_popcount(m);
+        }
+        tcount[size_t(t) + 1] = cnt;
+#pragma omp barrier
+#pragma omp single
+        for (int i = 0; i < nt; ++i) tcount[size_t(i) + 1] += tcount[size_t(i)];
+        int64_t at = tcount[size_t(t)];
+        for (int64_t g = g0; g < g1; ++g) {
+            base[g] = uint32_t(at);
+            for (uint32_t m = pres[g]; m; m &= m - 1) lit[at++] = tmp[g * 32 + __builtin_ctz(m)];
+        }
+    }
+    if (bad) return 0;
+    return mek::sparse_mask_header_bytes(n) + size_t(tcount[size_t(nthreads)]) * 8;
+}
+
 me_status sync(me_ctx* ctx) {
     ME_CUDA(cudaStreamSynchronize(ctx->stream));
     ME_CUDA(cudaGetLastError());
@@ -387,11 +432,12 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     // Binary alpha masks cross PCIe bit-packed (packed on the host cores while
     // the previous chunk's copies are in flight, expanded on the device).
     const bool pack = alpha && !getenv("ME_B200_NO_MASK_PACK");
+    const bool sparse = !getenv("ME_B200_DENSE_MASK_PACK");
     const size_t max_chunk = seq_bytes * size_t((n_seq + nchunks - 1) / nchunks);
     if (pack)
         for (int i = 0; i < 2; ++i) {
-            ME_CUDA(ctx->pack_host[i].reserve(max_chunk / 8 + 64));
-            ME_CUDA(ctx->pack_dev[i].reserve(max_chunk / 8 + 64));
+            ME_CUDA(ctx->pack_host[i].reserve(mek::sparse_mask_header_bytes(max_chunk) + max_chunk / 8 + 64));
+            ME_CUDA(ctx->pack_dev[i].reserve(mek::sparse_mask_header_bytes(max_chunk) + max_chunk / 8 + 64));
         }
     ctx->h2d_bytes = ctx->d2h_bytes = 0;
     ctx->launches = 0;
@@ -409,15 +455,24 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
                 // the copy out of this staging slot (chunk k - 2) must be done
                 if (k >= 2) ME_CUDA(cudaEventSynchronize(ctx->ev_pack[slot]));
                 uint8_t* hb = static_cast<uint8_t*>(ctx->pack_host[slot].p);
-                packed = pack_binary_mask(alpha + o, n, hb);
-                if (packed) {
-                    uint8_t* db = static_cast<uint8_t*>(ctx->pack_dev[slot].p);
+                uint8_t* db = static_cast<uint8_t*>(ctx->pack_dev[slot].p);
+                if (n % 64 == 0 && sparse) {
+                    // zero 64-pixel words elided (object masks are mostly background)
+                    if (ctx->pack_tmp.size() < n / 64) ctx->pack_tmp.resize(max_chunk / 64 + 1);
+                    const size_t bytes = pack_sparse_mask(alpha + o, n, hb, ctx->pack_tmp.data());
+                    if ((packed = bytes > 0)) {
+                        ME_CUDA(cudaMemcpyAsync(db, hb, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+                        ctx->h2d_bytes += int64_t(bytes);
+                        ME_CUDA(cudaEventRecord(ctx->ev_pack[slot], ctx->copy_stream));
+                        ME_CUDA(mek::unpack_mask_sparse(db, da + o, n, ctx->copy_stream));
+                    }
+                } else if ((packed = pack_binary_mask(alpha + o, n, hb))) {
                     ME_CUDA(cudaMemcpyAsync(db, hb, n / 8, cudaMemcpyHostToDevice, ctx->copy_stream));
                     ctx->h2d_bytes += int64_t(n / 8);
                     ME_CUDA(cudaEventRecord(ctx->ev_pack[slot], ctx->copy_stream));
                     ME_CUDA(mek::unpack_mask(db, da + o, n, ctx->copy_stream));
-                    packed_chunk = true;
                 }
+                packed_chunk = packed;
             }
             if (!packed) {
                 ME_CUDA(cudaMemcpyAsync(da + o, alpha + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));

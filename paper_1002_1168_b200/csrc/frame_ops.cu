@@ -34,6 +34,34 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ bits, uint4* __restri
     }
 }
 
+// unpack_sparse_kernel: the same masks with the all-zero 64-pixel words elided
+// (object masks are mostly background): per group of 32 words a presence mask
+// and the group's first literal; one warp per group, one lane per word.
+__global__ void unpack_sparse_kernel(const uint32_t* __restrict__ pres, const uint32_t* __restrict__ base,
+                                     const unsigned long long* __restrict__ lit, uint4* __restrict__ out,
+                                     size_t nwords) {
+    const int lane = threadIdx.x & 31;
+    const size_t ngroups = (nwords + 31) / 32;
+    for (size_t gi = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; gi < ngroups;
+         gi += (size_t(gridDim.x) * blockDim.x) >> 5) {
+        const size_t w = gi * 32 + lane;
+        if (w >= nwords) continue;
+        const uint32_t m = __ldg(pres + gi);
+        unsigned long long x = 0;
+        if ((m >> lane) & 1u) x = __ldg(lit + __ldg(base + gi) + __popc(m & ((1u << lane) - 1u)));
+        uint4 v[4];
+        uint32_t* o = reinterpret_cast<uint32_t*>(v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {  // 4 pixels per output word
+            const uint32_t nib = uint32_t(x >> (4 * q)) & 0xFu;
+            o[q] = ((nib & 1u) ? 0xFFu : 0u) | ((nib & 2u) ? 0xFF00u : 0u) | ((nib & 4u) ? 0xFF0000u : 0u) |
+                   ((nib & 8u) ? 0xFF000000u : 0u);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[4 * w + q] = v[q];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // mc_kernel: predict_frame (compensation.cpp:30-71) fused with the psnr SSE
 // (metrics.cpp:108-124) and the per-pair SearchStats reduction.  One thread
@@ -229,6 +257,17 @@ cudaError_t unpack_mask(const uint8_t* bits, uint8_t* out, size_t n, cudaStream_
         unpack_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(bits), reinterpret_cast<uint4*>(out), nw);
     }
     if (n % 32) return cudaErrorInvalidValue;  // callers pass whole 32-pixel groups
+    return cudaGetLastError();
+}
+
+cudaError_t unpack_mask_sparse(const uint8_t* packed, uint8_t* out, size_t n, cudaStream_t st) {
+    if (n % 64) return cudaErrorInvalidValue;
+    const size_t nwords = n / 64, ngroups = (nwords + 31) / 32;
+    const uint32_t* pres = reinterpret_cast<const uint32_t*>(packed);
+    const uint32_t* base = pres + ngroups;
+    const auto* lit = reinterpret_cast<const unsigned long long*>(packed + sparse_mask_header_bytes(n));
+    const int grid = int(std::min<size_t>((ngroups * 32 + 255) / 256, 148 * 16));
+    unpack_sparse_kernel<<<grid, 256, 0, st>>>(pres, base, lit, reinterpret_cast<uint4*>(out), nwords);
     return cudaGetLastError();
 }
 

@@ -60,6 +60,12 @@ cudaError_t binarize(const uint8_t* gray, int n, int threshold, uint8_t* out, cu
 // Expands a bit-packed binary mask (bit i of byte j = pixel 8j + i) to bytes
 // 0 / 255; n (pixels) is a multiple of 8.
 cudaError_t unpack_mask(const uint8_t* bits, uint8_t* out, size_t n, cudaStream_t st);
+// Sparse form of the same mask (n % 64 == 0): uint32 presence[G] (bit i of
+// group g: 64-pixel word 32g + i is nonzero), uint32 base[G] (index of the
+// group's first literal), then at sparse_mask_header_bytes(n) the nonzero
+// words (uint64, bit i = pixel i); G = ceil(n / 64 / 32).
+inline size_t sparse_mask_header_bytes(size_t n) { return ((n / 64 + 31) / 32 * 8 + 15) & ~size_t(15); }
+cudaError_t unpack_mask_sparse(const uint8_t* packed, uint8_t* out, size_t n, cudaStream_t st);
 cudaError_t predict(const uint8_t* ref, const uint8_t* cur, const int32_t* mv, const uint8_t* types,
                     int W, int H, int bs, uint8_t* pred, me_pair_stats* stats,
                     cudaStream_t st);

@@ -4,6 +4,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "me_b200.h"
 
@@ -80,6 +81,7 @@ struct me_ctx {
     // bit-packed alpha staging (binary masks cross PCIe at 1 bit per pixel)
     HostBuf pack_host[2];
     DevBuf pack_dev[2];
+    std::vector<uint64_t> pack_tmp;  // dense 64-pixel words before the zero words are elided
     cudaEvent_t ev_pack[2] = {};
     int64_t h2d_bytes = 0, d2h_bytes = 0;  // of the last host-pointer batch
     int64_t launches = 0;                  // kernels launched by the last batched call
