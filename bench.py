@@ -428,7 +428,7 @@ def main():
             raise SystemExit("e2e records differ from the device-resident run")
         h2d, d2h = B.last_transfer_bytes(local)  # counted by the library: alpha masks cross bit-packed
         e2e = {"value": total_units / e2e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e, "s_per_step": e2e_s,
-               "input_bytes_per_step": int(2 * n_seq * F * W * H), "note": "pinned host buffers; luma as bytes, binary alpha bit-packed on the host cores and expanded on the GPU"}
+               "input_bytes_per_step": int(2 * n_seq * F * W * H), "note": "pinned host buffers; luma as bytes, binary alpha bit-packed on the host cores (AVX-512) with all-zero 64-pixel words elided, expanded on the GPU"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
