@@ -130,6 +130,16 @@ me_status me_b200_ctx_transfer_bytes(me_ctx* ctx, int64_t* h2d, int64_t* d2h);
  * the mask expansions of the host path. */
 me_status me_b200_ctx_launches(me_ctx* ctx, int64_t* out);
 
+/* The host path's transfer form of a binary alpha mask (n pixels, n % 64 ==
+ * 0, every byte 0 or 255): G = ceil(n / 2048) groups of 32 64-pixel words;
+ * uint32 presence[G] (bit i of group g: word 32g + i has a set pixel),
+ * uint32 base[G] (index of the group's first stored word), zero padding to a
+ * 16-byte boundary, then the stored (nonzero) words as uint64, bit i = pixel
+ * i of the word.  *out_bytes receives the encoded size (<= 16 + n/256 + n/8);
+ * ME_ERR_INVALID_ARGUMENT for a non-binary mask, n % 64 != 0 or a short
+ * buffer.  Runs on the host cores (AVX-512BW when available). */
+me_status me_b200_pack_mask(const uint8_t* mask, size_t n, uint8_t* out, size_t out_cap, size_t* out_bytes);
+
 /* SearchConfig::validate + PrsConfig::validate (estimators.cpp:139-150). */
 me_status me_b200_validate_config(const me_config* cfg);
 

@@ -132,6 +132,7 @@ SIGNATURES = {
     "me_b200_ctx_stage_ms": (I, [P, C.POINTER(C.c_float), I]),
     "me_b200_ctx_transfer_bytes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "me_b200_ctx_launches": (I, [P, C.POINTER(C.c_int64)]),
+    "me_b200_pack_mask": (I, [P, C.c_size_t, P, C.c_size_t, C.POINTER(C.c_size_t)]),
     "me_b200_run_sequences_dev": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P, P]),
     "me_b200_run_sequences": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P]),
     "me_b200_estimate_field": (I, [P, C.POINTER(MeConfig), I, I, P, P, P, P, P, I, I, P, P]),

@@ -309,6 +309,18 @@ me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable) {
     return ok();
 }
 
+me_status me_b200_pack_mask(const uint8_t* mask, size_t n, uint8_t* out, size_t out_cap, size_t* out_bytes) {
+    if (!mask || !out || !out_bytes) return me_fail(ME_ERR_INVALID_ARGUMENT, "null argument");
+    if (n % 64) return me_fail(ME_ERR_INVALID_ARGUMENT, "mask size must be a multiple of 64 pixels");
+    if (out_cap < mek::sparse_mask_header_bytes(n) + n / 8)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "output buffer too small");
+    std::vector<uint64_t> tmp(n / 64 + 1);
+    const size_t bytes = pack_sparse_mask(mask, n, out, tmp.data());
+    if (!bytes) return me_fail(ME_ERR_INVALID_ARGUMENT, "mask is not binary (bytes other than 0 and 255)");
+    *out_bytes = bytes;
+    return ok();
+}
+
 me_status me_b200_ctx_launches(me_ctx* ctx, int64_t* out) {
     me_status s = check_ctx(ctx);
     if (s) return s;

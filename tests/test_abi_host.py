@@ -114,3 +114,47 @@ def test_psnr_tail_and_figure_of_merit():
     a, b = np.full((4, 4), 10, np.uint8), np.full((4, 4), 250, np.uint8)
     assert (me.residual(a, b) == -240).all()
     assert (me.residual_to_gray(me.residual(a, b)) == 0).all()
+
+
+def _decode_sparse_mask(buf: np.ndarray, n: int) -> np.ndarray:
+    """numpy restatement of the transfer form documented at me_b200_pack_mask."""
+    nwords = n // 64
+    groups = (nwords + 31) // 32
+    pres = buf[: 4 * groups].view(np.uint32)
+    base = buf[4 * groups: 8 * groups].view(np.uint32)
+    head = (8 * groups + 15) & ~15
+    words = np.zeros(nwords, np.uint64)
+    lit = buf[head:].view(np.uint64)
+    for g in range(groups):
+        m = int(pres[g])
+        k = int(base[g])
+        for i in range(32):
+            if (m >> i) & 1:
+                words[32 * g + i] = lit[k]
+                k += 1
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")
+    return (bits * 255).astype(np.uint8)
+
+
+@pytest.mark.parametrize("n", [64, 2048, 4096 + 64, 352 * 288 * 3])
+def test_pack_mask_roundtrip(n):
+    """The host path's sparse bit-packed mask (zero 64-pixel words elided)
+    decodes back to the mask; non-binary masks and bad sizes are refused."""
+    L = me.lib()
+    rng = np.random.default_rng(n)
+    mask = np.zeros(n, np.uint8)
+    for _ in range(max(1, n // 5000)):  # a few runs of foreground, like object masks
+        a = int(rng.integers(0, n))
+        mask[a: a + int(rng.integers(1, 700))] = 255
+    mask[rng.integers(0, n, size=max(1, n // 1000))] = 255  # and isolated pixels
+    cap = 16 + n // 256 + n // 8 + 64
+    out = np.zeros(cap, np.uint8)
+    nb = C.c_size_t(0)
+    assert L.me_b200_pack_mask(mask.ctypes.data, n, out.ctypes.data, cap, C.byref(nb)) == 0
+    assert nb.value <= cap
+    assert np.array_equal(_decode_sparse_mask(out[: nb.value], n), mask)
+    gray = mask.copy()
+    gray[n // 2] = 7
+    assert L.me_b200_pack_mask(gray.ctypes.data, n, out.ctypes.data, cap, C.byref(nb)) == _lib.ME_ERR_INVALID_ARGUMENT
+    assert "binary" in L.me_b200_last_error().decode()
+    assert L.me_b200_pack_mask(mask.ctypes.data, n - 8, out.ctypes.data, cap, C.byref(nb)) == _lib.ME_ERR_INVALID_ARGUMENT
