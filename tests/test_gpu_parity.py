@@ -293,3 +293,31 @@ def test_concurrent_host_threads(me_gpu, port):
         want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=bs), luma, alpha)
         assert_recs(recs[0], want_r, f"algo{algo} seed{seed}")
         assert np.array_equal(stats[0], want_s)
+
+
+@pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid"])
+@pytest.mark.parametrize("shape", [(16, 16), (48, 32), (64, 80)])
+def test_pa_kernel_modes_small_frames(me_gpu, port, mode, shape, monkeypatch):
+    """Every PA schedule on frames a few blocks wide (patches clipped by every
+    frame edge, windows smaller than the search range), with masks mixing
+    transparent, opaque and boundary blocks and strong motion."""
+    H, W = shape
+    monkeypatch.setenv("ME_PA_MODE", mode)
+    monkeypatch.setenv("ME_PA_WIDE", "1")
+    monkeypatch.setenv("ME_PA_NO_SMEM", "1")  # the batched kernels, not the one-CTA pair kernel
+    rng = np.random.default_rng(H * 1000 + W)
+    n_seq, F = 6, 5
+    base = noise(rng, H + 40, W + 40)
+    luma = np.stack([np.stack([shift_clamped(base, int(rng.integers(-6, 7)), int(rng.integers(-6, 7)))[20:20 + H, 20:20 + W]
+                               for _ in range(F)]) for _ in range(n_seq)])
+    alpha = np.zeros_like(luma)
+    alpha[0] = 255  # all opaque
+    alpha[2, :, H // 4: 3 * H // 4, W // 3:] = 255  # boundary blocks
+    alpha[3] = (rng.integers(0, 4, size=alpha[3].shape) == 0) * 255  # speckle: mostly boundary
+    alpha[4, :, :, : W // 2] = 255
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha.astype(np.uint8))
+    for i in range(n_seq):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i].astype(np.uint8))
+        assert_recs(recs[i], want_r, f"{mode} {shape} seq {i}")
+        assert np.array_equal(stats[i], want_s)
