@@ -1304,16 +1304,26 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             const bool own = __shfl_sync(FULL, md, gb + 2 * cc) == cc;  // uniform per group
             if (act && own) {
                 // 16 rows x 3 chunks; consecutive lanes take consecutive chunks
-                const int cs = (x0 + ccx - 4) & ~7;
+                const int cs = (x0 + ccx - 4) & ~7, ry0 = y0 + ccy - 4;
                 uint32_t* dst = patch + cc * kQuadPatch;
+                if (ry0 >= 0 && ry0 + kFastPR <= H && cs >= 0 && cs + 24 <= W) {
+                    // the whole patch inside the frame (the common case): one base
+                    const uint8_t* base = a.b.luma + (oref + uint32_t(ry0) * W + uint32_t(cs));
 #pragma unroll
-                for (int k = 0; k < 6; ++k) {
-                    const int ci8 = gl + 8 * k, r = ci8 / 3, ch = ci8 - 3 * r;
-                    const int y = clampi(y0 + ccy - 4 + r, 0, H - 1);
-                    const int col = cs + 8 * ch;
-                    const bool in = col >= 0 && col + 8 <= W;
-                    const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
-                    cp_async8(dst + r * kQuadPWW + 2 * ch, in ? rowp + col : rowp, in);
+                    for (int k = 0; k < 6; ++k) {
+                        const int ci8 = gl + 8 * k, r = ci8 / 3, ch = ci8 - 3 * r;
+                        cp_async8(dst + r * kQuadPWW + 2 * ch, base + (r * W + 8 * ch), true);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) {
+                        const int ci8 = gl + 8 * k, r = ci8 / 3, ch = ci8 - 3 * r;
+                        const int y = clampi(ry0 + r, 0, H - 1);
+                        const int col = cs + 8 * ch;
+                        const bool in = col >= 0 && col + 8 <= W;
+                        const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
+                        cp_async8(dst + r * kQuadPWW + 2 * ch, in ? rowp + col : rowp, in);
+                    }
                 }
             }
         }
