@@ -402,14 +402,26 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
     if ((reinterpret_cast<uintptr_t>(luma) | reinterpret_cast<uintptr_t>(alpha) |
          reinterpret_cast<uintptr_t>(recs)) & 15)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "device buffers must be 16-byte aligned");
-    const mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H, luma, alpha);
-    const size_t need = mek::scratch_bytes(b, cfg->algo);
-    ME_CUDA(ctx->tasks.reserve(need));
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: the CUDA default stream
-    int nl = 0;
-    ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, pred, ctx->tasks.p, ctx->tasks.cap,
-                           ctx->num_sms, st, ctx->events(), false, &nl));
-    ctx->launches = nl;
+    // Sequences are independent: a batch whose frames span 4 GiB or more runs
+    // as consecutive sub-batches below 4 GiB each, so every one takes the
+    // kernels with 32-bit plane offsets.
+    const size_t seq_bytes = size_t(n_frames) * size_t(W) * size_t(H);
+    const int per = int(std::max<size_t>(1, std::min<size_t>(size_t(n_seq), ((size_t(1) << 32) - 1) / seq_bytes)));
+    const int pairs = n_frames - cfg->ref_distance;
+    const size_t seq_recs = size_t(pairs) * (W / cfg->block_size) * (H / cfg->block_size);
+    ctx->launches = 0;
+    for (int s0 = 0; s0 < n_seq; s0 += per) {
+        const int ns = std::min(per, n_seq - s0);
+        const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, luma + seq_bytes * s0,
+                                        alpha ? alpha + seq_bytes * s0 : nullptr);
+        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+        int nl = 0;
+        ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs + seq_recs * s0, stats + size_t(pairs) * s0,
+                               pred ? pred + size_t(W) * H * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
+                               ctx->num_sms, st, ctx->events(), false, &nl));
+        ctx->launches += nl;
+    }
     ctx->ev_valid = ctx->profiling;
     return ok();
 }

@@ -321,3 +321,44 @@ def test_pa_kernel_modes_small_frames(me_gpu, port, mode, shape, monkeypatch):
         want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i].astype(np.uint8))
         assert_recs(recs[i], want_r, f"{mode} {shape} seq {i}")
         assert np.array_equal(stats[i], want_s)
+
+
+def test_batch_beyond_4gib(me_gpu, port):
+    """A batch whose frames span more than 4 GiB of device memory (the PA
+    kernels use 32-bit plane offsets; the library runs it as consecutive
+    sub-batches below 4 GiB): the last sequences, whose pixels lie past
+    4 GiB, match the oracle, and so does the first."""
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import synth
+
+    free, _ = torch.cuda.mem_get_info()
+    n_seq, F = 1440, 30  # 1440 x 30 x 352 x 288 = 4.38 GB of luma (and as much alpha)
+    if free < 14 * 2**30:
+        pytest.skip("needs ~14 GB of free device memory")
+    luma, alpha = synth.config4_batch_dev(n_seq, 4100, frames=F)
+    assert luma.numel() > 2**32
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = B.run_sequences_dev(cfg, luma, alpha)
+    torch.cuda.synchronize()
+    for i in (0, n_seq - 2, n_seq - 1):
+        got_r = recs[i].cpu().numpy().view(_lib_rec_dtype()).reshape(recs.shape[1:4])
+        got_s = stats[i].cpu().numpy().view(_lib_stats_dtype()).reshape(-1)
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i].cpu().numpy(), alpha[i].cpu().numpy())
+        assert_recs(got_r, want_r, f"seq {i}")
+        assert np.array_equal(got_s, want_s)
+    del luma, alpha, recs, stats
+    torch.cuda.empty_cache()
+
+
+def _lib_rec_dtype():
+    from paper_1002_1168_b200 import _lib
+
+    return _lib.rec_dtype()
+
+
+def _lib_stats_dtype():
+    from paper_1002_1168_b200 import _lib
+
+    return _lib.stats_dtype()
