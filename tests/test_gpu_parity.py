@@ -362,3 +362,43 @@ def _lib_stats_dtype():
     from paper_1002_1168_b200 import _lib
 
     return _lib.stats_dtype()
+
+
+@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("bs", [8, 16])
+@pytest.mark.parametrize("shape", [(96, 144), (64, 96)])
+def test_ring_searches_batched(me_gpu, port, algo, bs, shape):
+    """TSS / FSS / DS through the batched ring kernel at both block sizes
+    (every displaced reference row is unaligned for odd vectors: the kernel's
+    aligned-load path), an odd number of 16-pixel columns, and a smooth moving
+    texture (long descents, revisited positions)."""
+    h, w = shape
+    rng = np.random.default_rng(algo * 100 + bs + h)
+    base = noise(rng, h + 40, w + 40)
+    base = np.convolve(base.ravel(), np.ones(5) / 5, "same").reshape(base.shape).astype(np.uint8)
+    frames = np.stack([shift_clamped(base, 3 * t, -2 * t)[20:20 + h, 20:20 + w] for t in range(5)])
+    for rng_s in (7, 16):
+        cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=rng_s, block_size=bs, ref_distance=1))
+        recs, stats = me_gpu.run_sequences(cfg, frames[None], None)
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=rng_s, block_size=bs, ref_distance=1), frames, None)
+        assert_recs(recs[0], want_r, f"algo{algo} bs{bs} {shape} S{rng_s}")
+        assert np.array_equal(stats[0], want_s)
+
+
+@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("bs", [8, 16])
+def test_ring_single_block_odd_width(me_gpu, port, algo, bs):
+    """The per-block entry points on a frame whose width is not a multiple of
+    4 (no row of either plane is word-aligned)."""
+    rng = np.random.default_rng(31 * algo + bs)
+    base = noise(rng, 90, 110)
+    base = np.convolve(base.ravel(), np.ones(7) / 7, "same").reshape(base.shape).astype(np.uint8)
+    cur, ref = base[10:60, 10:80].copy(), base[13:63, 8:78].copy()  # 50 x 70
+    fn = [None, me_gpu.tss_search, me_gpu.fss_search, me_gpu.ds_search][algo]
+    rects = [me_gpu.BlockRect(x0, y0, bs, x0 // bs, y0 // bs) for y0 in range(0, 50 - bs + 1, bs) for x0 in range(0, 70 - bs + 1, bs)]
+    for r in rects:
+        for rng_s in (7, 16):
+            st = me_gpu.SearchStats()
+            mv = fn(cur, ref, r, me_gpu.SearchConfig(search_range=rng_s, block_size=bs), st)
+            want_mv, want_cmp, _ = port.block_search(algo, cur, ref, r.x0, r.y0, bs, rng_s)
+            assert mv == tuple(want_mv) and st.block_comparisons == want_cmp, (r, rng_s)
