@@ -427,8 +427,21 @@ def main():
         if not np.array_equal(hrecs.numpy()[0].view(_lib.rec_dtype()).reshape(pairs, rows, cols), hrec):
             raise SystemExit("e2e records differ from the device-resident run")
         h2d, d2h = B.last_transfer_bytes(local)  # counted by the library: alpha masks cross bit-packed
+        # this box's pinned H2D bandwidth (256 MiB copies): the e2e step's copy floor is h2d / it
+        probe_h = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        probe_d = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        probe_d.copy_(probe_h, non_blocking=True)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(4):
+            probe_d.copy_(probe_h, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        h2d_gbs = 4 * (256 << 20) / (ev0.elapsed_time(ev1) * 1e-3) / 1e9
+        del probe_h, probe_d
         e2e = {"value": total_units / e2e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e, "s_per_step": e2e_s,
-               "input_bytes_per_step": int(2 * n_seq * F * W * H), "note": "pinned host buffers; luma as bytes, binary alpha bit-packed on the host cores (AVX-512) with all-zero 64-pixel words elided, expanded on the GPU"}
+               "input_bytes_per_step": int(2 * n_seq * F * W * H), "h2d_gbs_measured": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6, "note": "pinned host buffers; luma as bytes, binary alpha bit-packed on the host cores (AVX-512) with all-zero 64-pixel words elided, expanded on the GPU"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
