@@ -54,6 +54,72 @@ def gather_fields(mv, dst: int = 0, group=None):
     return out
 
 
+def pack_mv(recs, search_range: int):
+    """The MV field of a uint8 record tensor [..., 16] in its smallest exact
+    form: (dx, dy) as int8 pairs [..., 2] when every vector fits (half-pel
+    components lie in [-2S, 2S], so S <= 63), else the int32 words of
+    `mv_words`.  One elementwise pass over the records."""
+    import torch
+
+    if 2 * search_range <= 127:
+        return recs.view(torch.int16)[..., 0:2].to(torch.int8)
+    return mv_words(recs)
+
+
+def unpack_mv(packed):
+    """(dx, dy) int32 [..., 2] from either `pack_mv` form."""
+    import torch
+
+    if packed.dtype == torch.int8:
+        return packed.to(torch.int32)
+    return torch.stack([(packed << 16) >> 16, packed >> 16], dim=-1)
+
+
+class FieldGatherer:
+    """Per-step gather of the MV fields into rank `dst`, overlapped with the
+    next step: step k's packed field is gathered asynchronously (NCCL runs it
+    on its own stream after step k's kernels) while step k+1 computes; two
+    send buffers alternate, and a buffer is refilled only after its previous
+    gather completed (`Work.wait`, a stream dependency under NCCL).  `finish`
+    waits for the last gather; the received fields of the latest completed
+    step are in `fields` on rank `dst`."""
+
+    def __init__(self, search_range: int, dst: int = 0, group=None):
+        self.S, self.dst, self.group = search_range, dst, group
+        self.bufs = [None, None]
+        self.outs = [None, None]
+        self.work = [None, None]
+        self.k = 0
+        self.fields = None
+
+    def submit(self, recs):
+        import torch
+        import torch.distributed as dist
+
+        i = self.k & 1
+        if self.work[i] is not None:
+            self.work[i].wait()
+            self.fields = self.outs[i]
+        packed = pack_mv(recs, self.S)
+        if self.bufs[i] is None or self.bufs[i].shape != packed.shape or self.bufs[i].dtype != packed.dtype:
+            self.bufs[i] = torch.empty_like(packed)
+            rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+            self.outs[i] = [torch.empty_like(packed) for _ in range(world)] if rank == self.dst else None
+        self.bufs[i].copy_(packed)
+        self.work[i] = dist.gather(self.bufs[i], self.outs[i], dst=self.dst, group=self.group, async_op=True)
+        self.k += 1
+
+    def finish(self):
+        """Waits for every outstanding gather; returns rank dst's fields of
+        the last step (None on the other ranks)."""
+        for j in (self.k & 1, (self.k + 1) & 1):  # older first
+            if self.work[j] is not None:
+                self.work[j].wait()
+                self.fields = self.outs[j]
+                self.work[j] = None
+        return self.fields
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a scalar over all ranks (timings: the slowest rank defines the job)."""
     import torch

@@ -25,6 +25,20 @@ def test_shard_covers_everything():
         mdist.shard(4, 2, 2)
 
 
+def test_pack_mv_both_forms():
+    recs = torch.zeros((3, 7, 16), dtype=torch.uint8)
+    r16 = recs.view(torch.int16)
+    r16[..., 0] = torch.arange(-10, 11, dtype=torch.int16).view(3, 7) * 6  # up to +-60
+    r16[..., 1] = -torch.arange(-10, 11, dtype=torch.int16).view(3, 7) * 3
+    want = r16[..., 0:2].to(torch.int32)
+    small = mdist.pack_mv(recs, 31)
+    assert small.dtype == torch.int8 and torch.equal(mdist.unpack_mv(small), want)
+    r16[..., 0] *= 2  # up to +-120 half-pel: S = 64 needs the int32 words
+    want = r16[..., 0:2].to(torch.int32)
+    wide = mdist.pack_mv(recs, 64)
+    assert wide.dtype == torch.int32 and torch.equal(mdist.unpack_mv(wide), want)
+
+
 def test_seeds_weak_and_strong():
     weak = [mdist.sequence_seeds(100, 4, r, 2) for r in range(2)]
     assert weak == [[100, 101, 102, 103], [104, 105, 106, 107]]
@@ -48,6 +62,22 @@ def _worker(rank, world, port, q):
         w = recs.view(torch.int32)
         w[..., 0] = torch.arange(2 * 3 * 4 * 5, dtype=torch.int32).view(2, 3, 4, 5) + 1000 * rank
         got = mdist.gather_fields(mdist.mv_words(recs))
+        # the pipelined compact gather: 3 steps, each with its own field
+        g = mdist.FieldGatherer(search_range=16)
+        for step in range(3):
+            r16 = recs.view(torch.int16)
+            r16[..., 0] = (torch.arange(120, dtype=torch.int16).view(2, 3, 4, 5) % 65) - 32 + step
+            r16[..., 1] = -(torch.arange(120, dtype=torch.int16).view(2, 3, 4, 5) % 61) + 30 + rank
+            want_step = mdist.unpack_mv(mdist.pack_mv(recs, 16)).clone()
+            g.submit(recs)
+        last = g.finish()
+        if rank == 0:
+            assert len(last) == 2
+            assert torch.equal(mdist.unpack_mv(last[0]), want_step)
+            assert torch.equal(mdist.unpack_mv(last[1])[..., 0], want_step[..., 0])
+            assert torch.equal(mdist.unpack_mv(last[1])[..., 1], want_step[..., 1] + 1)
+        else:
+            assert last is None
         t = mdist.max_over_ranks(float(rank + 1))
         if rank == 0:
             q.put(([g.tolist() for g in got], t))
