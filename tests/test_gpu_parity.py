@@ -246,22 +246,25 @@ def test_estimate_field_random_prev(me_gpu, port, odd):
     assert_recs(recs, want)
 
 
+@pytest.mark.parametrize("bt,it", [(0, 4), (1, 4), (0, 7)])
 @pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid", "warp"])
-def test_pa_kernel_modes(me_gpu, port, mode, monkeypatch):
+def test_pa_kernel_modes(me_gpu, port, mode, bt, it, monkeypatch):
     """Every PA kernel schedule (one block per warp, two per warp, the hybrid
     splits of the sorted list with two or four blocks per warp in the wide
     range, the generic kernel) on the same batch; the hybrids' wide threshold
-    is lowered so all three of their ranges are used."""
+    is lowered so all three of their ranges are used.  Also with
+    BoundaryTemporal::Shape and a longer PRS iteration limit."""
     from paper_1002_1168_b200 import synth
 
     monkeypatch.setenv("ME_PA_MODE", mode)
     monkeypatch.setenv("ME_PA_WIDE", "4")
     luma, alpha = synth.config4_batch(5, 700, frames=6)
-    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8),
+                             prs=me_gpu.PrsConfig(max_iterations=it), boundary_temporal=me_gpu.BoundaryTemporal(bt))
     recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
     for i in range(5):
-        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
-        assert_recs(recs[i], want_r, f"{mode} seq {i}")
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8, boundary_temporal=bt, max_iterations=it), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"{mode} bt{bt} it{it} seq {i}")
         assert np.array_equal(stats[i], want_s)
 
 
@@ -402,3 +405,40 @@ def test_ring_single_block_odd_width(me_gpu, port, algo, bs):
             mv = fn(cur, ref, r, me_gpu.SearchConfig(search_range=rng_s, block_size=bs), st)
             want_mv, want_cmp, _ = port.block_search(algo, cur, ref, r.x0, r.y0, bs, rng_s)
             assert mv == tuple(want_mv) and st.block_comparisons == want_cmp, (r, rng_s)
+
+
+PA_VARIANTS = [
+    # (bs, halfpel, boundary_temporal, max_iter, step, eps, theta)
+    (8, 0, 1, 4, 2, 0.5, 2.0),    # BoundaryTemporal::Shape: T scored by sad_shape on boundary blocks
+    (16, 0, 1, 4, 2, 0.5, 2.0),
+    (8, 1, 1, 4, 1, 0.5, 2.0),    # half-pel + Shape
+    (16, 1, 0, 4, 1, 0.5, 2.0),
+    (8, 0, 0, 1, 2, 0.5, 2.0),    # one PRS iteration
+    (8, 0, 0, 9, 2, 0.5, 2.0),    # long descents (more centres than the register-tracked three)
+    (16, 1, 0, 6, 1, 0.25, 1.0),  # other epsilon / theta: the FP64 probing direction changes tie breaks
+    (8, 0, 0, 4, 2, 1.0, 0.5),
+]
+
+
+@pytest.mark.parametrize("bs,hp,bt,it,step,eps,theta", PA_VARIANTS)
+def test_pa_config_variants(me_gpu, port, bs, hp, bt, it, step, eps, theta):
+    """The PA variants the API exposes but the benchmark configs do not
+    exercise (SURVEY §8f rank 2): BoundaryTemporal::Shape, half-pel mode,
+    PRS iteration limits, epsilon and theta — bit-exact records and stats on
+    config 1 and config 2 sequences (every kernel schedule the variant takes)."""
+    from paper_1002_1168_b200 import synth
+
+    for cfg_id, seed in ((1, 4100 + bs), (2, 4200 + bs)):
+        luma, alpha = synth.config_sequence(cfg_id, seed, 6)
+        cfg = me_gpu.BatchConfig(
+            algo=me_gpu.Algo.PA,
+            search=me_gpu.SearchConfig(search_range=16, block_size=bs, halfpel=bool(hp)),
+            prs=me_gpu.PrsConfig(epsilon=eps, theta=theta, max_iterations=it, step=step),
+            boundary_temporal=me_gpu.BoundaryTemporal(bt),
+        )
+        recs, stats = me_gpu.run_sequences(cfg, luma[None], alpha[None])
+        want_r, want_s = port.run_sequence(
+            oracle.make_cfg(algo=4, search_range=16, block_size=bs, halfpel=hp, boundary_temporal=bt,
+                            max_iterations=it, step=step, epsilon=eps, theta=theta), luma, alpha)
+        assert_recs(recs[0], want_r, f"cfg{cfg_id} bs{bs} hp{hp} bt{bt} it{it} step{step} eps{eps} theta{theta}")
+        assert np.array_equal(stats[0], want_s)
