@@ -300,17 +300,35 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(ClassArgs a, int* cursor
     }
     const uint8_t* types = a.types + size_t(r) * cols;
     const int key0 = a.pa ? a.key_a * int(2 * v + p) + a.key_s * int(seq) : 0, kstep = a.pa ? a.key_a : 0;
+    // rows of a multiple of 4 blocks (cfg4: 44) are read as words, and a word
+    // of four transparent blocks (ME_TRANSPARENT = 0: most of them) is skipped whole
+    const bool words = (cols & 3u) == 0;
     for (int pass = 0; pass < 2; ++pass) {
         if (live) {
-            int key = key0;
-            for (uint32_t h = 0; h < cols; ++h, key += kstep) {
-                const int ty = types[h];
-                if (ty == ME_TRANSPARENT) continue;
+            auto visit = [&](uint32_t h, int ty) {
+                const int key = key0 + int(h) * kstep;
                 if (pass == 0) {
                     atomicAdd(&s_cnt[key], 1);
                 } else {
                     const int pos = s_base[key] + atomicAdd(&s_cnt[key], 1);
                     list[pos] = make_uint2(h | (v << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u), p | (seq << 16));
+                }
+            };
+            if (words) {
+                const uint32_t* t32 = reinterpret_cast<const uint32_t*>(types);
+                for (uint32_t w = 0; w < (cols >> 2); ++w) {
+                    const uint32_t t4 = t32[w];
+                    if (t4 == 0u) continue;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int ty = int((t4 >> (8 * j)) & 0xFFu);
+                        if (ty != ME_TRANSPARENT) visit(4 * w + j, ty);
+                    }
+                }
+            } else {
+                for (uint32_t h = 0; h < cols; ++h) {
+                    const int ty = types[h];
+                    if (ty != ME_TRANSPARENT) visit(h, ty);
                 }
             }
         }
