@@ -316,6 +316,7 @@ struct PaArgs {
     int fast;              // patch fast path allowed (step 2, max_iter <= 4)
     int warp_words;        // shared words per warp
     int poll_ns;           // dependency poll interval
+    int pdl;               // hybrid launches chained by programmatic dependent launch (see PdlScope)
     const int* range;      // [begin, end) of the list for this launch (device) or null: [0, *nlist)
     unsigned long long* trace;  // debug: per entry {claimed, deps ready, done, smid} (ns)
 };
@@ -668,8 +669,26 @@ __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, 
     r1 = __funnelshift_r(w1, w2, sh);
 }
 
+// Programmatic dependent launch between the hybrid's three persistent grids
+// (head -> middle -> tail).  Their items already synchronise through the
+// record polls, so a dependent grid may start as soon as every CTA of its
+// predecessor is resident: each CTA allows it on entry
+// (griddepcontrol.launch_dependents) and, on exit, waits for the predecessor
+// grid to complete (griddepcontrol.wait), so a grid never completes before
+// the one it was chained to (stream order after the tail stays intact).
+struct PdlScope {
+    bool on;
+    __device__ explicit PdlScope(bool o) : on(o) {
+        if (on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
+    __device__ ~PdlScope() {
+        if (on) asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+};
+
 template <int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
+    const PdlScope pdl_scope(a.pdl != 0);
     extern __shared__ uint32_t s_pa[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t* ws = s_pa + wid * kFastWarpWords;
@@ -1230,6 +1249,7 @@ __device__ __forceinline__ void cp_async8(uint32_t* smem, const void* gmem, bool
 
 template <int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
+    const PdlScope pdl_scope(a.pdl != 0);
     extern __shared__ uint32_t s_pa[];
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1987,6 +2007,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     pa_args.stats = stats;
     pa_args.fast = (pa_args.P.step == 2 && cfg.max_iterations <= 4) ? 1 : 0;
     pa_args.poll_ns = getenv("ME_PA_POLL_NS") ? atoi(getenv("ME_PA_POLL_NS")) : 64;
+    pa_args.pdl = 0;
     pa_args.trace = nullptr;
     const char* trace_path = getenv("ME_PA_TRACE");
     int n_host = 0;
@@ -1999,16 +2020,32 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     const char* cta = getenv("ME_PA_CTA");
     const char* minb = getenv("ME_PA_MINB");
     using PaKernel = void (*)(const PaArgs);
+    // ME_PA_PDL=0 launches the hybrid's grids in plain stream order
+    const bool pdl = pa_mode == 4 && !trace_path && !(getenv("ME_PA_PDL") && atoi(getenv("ME_PA_PDL")) == 0);
     // persistent grids: every warp of a launch must be co-resident (dependency spinning)
-    auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range) -> cudaError_t {
+    auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range, bool chained = false) -> cudaError_t {
         PaArgs la = pa_args;
         la.range = range;
+        la.pdl = pdl ? 1 : 0;
         la.warp_words = std::max(la.P.bm_words, warp_words);
         const size_t smem = size_t(threads / 32) * la.warp_words * 4;
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e2) return e2;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (pdl && chained) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(num_sms * (occ > 0 ? occ : 1));
+            lc.blockDim = dim3(threads);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            return cudaLaunchKernelEx(&lc, kern, la);
+        }
         kern<<<num_sms * (occ > 0 ? occ : 1), threads, smem, st>>>(la);
         return cudaGetLastError();
     };
@@ -2049,8 +2086,8 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         const int mb = qm ? atoi(qm) : 3;
         PaKernel quad = mb == 4 ? pa_quad_kernel<4> : mb == 2 ? pa_quad_kernel<2> : pa_quad_kernel<3>;
         if (trace_path) quad = pa_quad_kernel<3, true>;
-        if (!(e = launch(fast, 256, kFastWarpWords, ranges)) && !(e = launch(quad, 256, kQuadWarpWords, ranges + 2)))
-            e = launch(fast, 256, kFastWarpWords, ranges + 4);
+        if (!(e = launch(fast, 256, kFastWarpWords, ranges)) && !(e = launch(quad, 256, kQuadWarpWords, ranges + 2, true)))
+            e = launch(fast, 256, kFastWarpWords, ranges + 4, true);
     } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast
         if (!(e = launch(fast, 256, kFastWarpWords, ranges)) &&
             !(e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, ranges + 2)))
