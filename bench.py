@@ -323,7 +323,9 @@ def main():
     stream = torch.cuda.current_stream(dev)
     lib = me.lib()
     ctxh = _lib.ctx(local)
-    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
+    # stage events only in the untimed breakdown pass: an event between two
+    # launches would also break their programmatic-dependent-launch chain
+    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))
     import ctypes as C
 
     stage = (C.c_float * 4)()
@@ -364,6 +366,7 @@ def main():
     launches_per_step = B.last_launches(local)
     # per-stage breakdown (CUDA events on the launching stream), untimed
     n_stage = min(args.steps, 20)
+    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
     for _ in range(n_stage):
         step(True)
     if gatherer is not None:

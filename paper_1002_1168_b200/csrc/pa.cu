@@ -678,7 +678,9 @@ __device__ __forceinline__ void prow8(const uint32_t* row, int t, uint32_t& r0, 
 // the one it was chained to (stream order after the tail stays intact).
 struct PdlScope {
     bool on;
-    __device__ explicit PdlScope(bool o) : on(o) {
+    __device__ explicit PdlScope(int mode) : on(mode != 0) {
+        // mode 2: also chained to the sort (reads its list): wait for it first
+        if (mode == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
         if (on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
     __device__ ~PdlScope() {
@@ -688,7 +690,7 @@ struct PdlScope {
 
 template <int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
-    const PdlScope pdl_scope(a.pdl != 0);
+    const PdlScope pdl_scope(a.pdl);
     extern __shared__ uint32_t s_pa[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t* ws = s_pa + wid * kFastWarpWords;
@@ -1249,7 +1251,7 @@ __device__ __forceinline__ void cp_async8(uint32_t* smem, const void* gmem, bool
 
 template <int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
-    const PdlScope pdl_scope(a.pdl != 0);
+    const PdlScope pdl_scope(a.pdl);
     extern __shared__ uint32_t s_pa[];
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2023,10 +2025,11 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     // ME_PA_PDL=0 launches the hybrid's grids in plain stream order
     const bool pdl = pa_mode == 4 && !trace_path && !(getenv("ME_PA_PDL") && atoi(getenv("ME_PA_PDL")) == 0);
     // persistent grids: every warp of a launch must be co-resident (dependency spinning)
-    auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range, bool chained = false) -> cudaError_t {
+    auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range, bool chained = false,
+                      bool after_sort = false) -> cudaError_t {
         PaArgs la = pa_args;
         la.range = range;
-        la.pdl = pdl ? 1 : 0;
+        la.pdl = pdl ? (after_sort ? 2 : 1) : 0;
         la.warp_words = std::max(la.P.bm_words, warp_words);
         const size_t smem = size_t(threads / 32) * la.warp_words * 4;
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -2086,7 +2089,8 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         const int mb = qm ? atoi(qm) : 3;
         PaKernel quad = mb == 4 ? pa_quad_kernel<4> : mb == 2 ? pa_quad_kernel<2> : pa_quad_kernel<3>;
         if (trace_path) quad = pa_quad_kernel<3, true>;
-        if (!(e = launch(fast, 256, kFastWarpWords, ranges)) && !(e = launch(quad, 256, kQuadWarpWords, ranges + 2, true)))
+        if (!(e = launch(fast, 256, kFastWarpWords, ranges, pdl_sort(), pdl_sort())) &&
+            !(e = launch(quad, 256, kQuadWarpWords, ranges + 2, true)))
             e = launch(fast, 256, kFastWarpWords, ranges + 4, true);
     } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast
         if (!(e = launch(fast, 256, kFastWarpWords, ranges)) &&

@@ -32,6 +32,7 @@ struct ClassArgs {
 
 // wavefront.cu: classify -> per-step histogram -> scan -> fill (the sorted list)
 cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st);
+bool pdl_sort();  // scan, fill and the PA head chained by programmatic dependent launch
 cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
                         int wide, int* ranges, cudaStream_t st);
 cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st);

@@ -22,6 +22,13 @@ namespace mek {
 // t = h + 2v + p; baselines: a single bin).
 // ---------------------------------------------------------------------------
 
+// Programmatic dependent launch along classify -> scan -> fill -> PA head:
+// every kernel allows its successor to launch on entry; a successor waits for
+// its predecessor's completion (and memory) before reading anything.  Both
+// instructions are no-ops for kernels launched in plain stream order.
+__device__ __forceinline__ void pdl_allow_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // SSE of a block predicted with the zero vector (transparent blocks,
 // compensation.cpp:45): cur block vs the co-located ref block.
 __device__ __forceinline__ uint32_t block_sse0(const uint8_t* cur, const uint8_t* ref, int W,
@@ -47,6 +54,7 @@ __device__ __forceinline__ uint32_t block_sse0(const uint8_t* cur, const uint8_t
 template <int BS>
 __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
     extern __shared__ int s_hist[];
+    pdl_allow_next();
     constexpr int NB = 16 / BS;  // blocks per strip
     const Batch& b = a.b;
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
@@ -165,6 +173,8 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
 // holding >= wide blocks: {0, b1}, {b1, b2}, {b2, total} (narrow, wide, narrow).
 __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
                             uint2* list, int wide, int* ranges) {
+    pdl_wait_prev();
+    pdl_allow_next();
     __shared__ int s_part[1024];
     __shared__ int s_lo, s_hi;  // first / last wide step
     const int T = blockDim.x;
@@ -241,6 +251,8 @@ __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int*
 // then scatter.
 
 __global__ void __launch_bounds__(256) fill_kernel(ClassArgs a, int* cursor, uint2* list, uint32_t rows_per_cta) {
+    pdl_wait_prev();
+    pdl_allow_next();
     extern __shared__ int s_cnt[];  // [nbins] counts, then [nbins] bases
     int* s_base = s_cnt + a.nbins;
     const Batch& b = a.b;
@@ -282,6 +294,8 @@ __global__ void __launch_bounds__(256) fill_kernel(ClassArgs a, int* cursor, uin
 // pair, row decoded once per row instead of per block; a row's blocks go to
 // consecutive bins, so the shared-memory counters see fewer collisions).
 __global__ void __launch_bounds__(256) fill_rows_kernel(ClassArgs a, int* cursor, uint2* list) {
+    pdl_wait_prev();
+    pdl_allow_next();
     extern __shared__ int s_cnt[];  // [nbins] counts, then [nbins] bases
     int* s_base = s_cnt + a.nbins;
     const Batch& b = a.b;
@@ -347,6 +361,28 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(ClassArgs a, int* cursor
 // Launchers
 // ---------------------------------------------------------------------------
 
+// ME_PDL_SORT=0 launches scan and fill in plain stream order
+bool pdl_sort() {
+    static const bool on = !(getenv("ME_PDL_SORT") && atoi(getenv("ME_PDL_SORT")) == 0);
+    return on;
+}
+
+static cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    return lc;
+}
+
+static void pdl_attr(cudaLaunchConfig_t& lc, cudaLaunchAttribute* at) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+}
+
 cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
     const Batch& b = ca.b;
     const int threads = 256;
@@ -364,6 +400,12 @@ cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
 
 cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
                         int wide, int* ranges, cudaStream_t st) {
+    if (pdl_sort()) {
+        cudaLaunchConfig_t lc = pdl_config(dim3(1), dim3(1024), 0, st);
+        cudaLaunchAttribute at[1];
+        pdl_attr(lc, at);
+        return cudaLaunchKernelEx(&lc, scan_kernel, hist, nbins, pad, offs, cursor, list, wide, ranges);
+    }
     scan_kernel<<<1, 1024, 0, st>>>(hist, nbins, pad, offs, cursor, list, wide, ranges);
     return cudaGetLastError();
 }
@@ -387,6 +429,12 @@ cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_s
         if (smem > 48 * 1024 &&
             (e = cudaFuncSetAttribute(fill_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
             return e;
+        if (pdl_sort()) {
+            cudaLaunchConfig_t lc = pdl_config(dim3(unsigned((nrows + 255) / 256)), dim3(256), smem, st);
+            cudaLaunchAttribute at[1];
+            pdl_attr(lc, at);
+            return cudaLaunchKernelEx(&lc, fill_rows_kernel, ca, cursor, list);
+        }
         fill_rows_kernel<<<int((nrows + 255) / 256), 256, smem, st>>>(ca, cursor, list);
         return cudaGetLastError();
     }
