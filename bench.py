@@ -369,6 +369,7 @@ def main():
     _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
     for _ in range(n_stage):
         step(True)
+    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))  # the e2e leg runs without stage events
     if gatherer is not None:
         gatherer.finish()
     stage_sum *= args.steps / n_stage
