@@ -1,25 +1,29 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 shape-adaptive motion-estimation hot path.
 
-Default workload (BASELINE.json config 4, the throughput batch): per GPU, 256
+Default workload (BASELINE.json config 4, the throughput batch): 256
 independent CIF 352x288 sequences x 30 frames from the config-2 generator
 (seed = base + i), proposed algorithm (PA: BRS + PRS) at +/-16, 8x8 blocks,
-ref_distance 2, plus motion compensation and PSNR for every pair.  One "step"
-= one pass of the whole pipeline (classify -> wavefront sort -> PA -> MC+PSNR)
-over the batch.  Metric: macroblocks/s = (W/16)(H/16) x pairs x sequences / s,
-every 16x16 macroblock counted (transparent ones included).
+ref_distance 2, with motion compensation + PSNR (SSE) of every pair.  One
+"step" = one pass of the whole pipeline (classify -> wavefront sort -> PA
+search with the fused SSE) over the batch.  Metric: macroblocks/s =
+(W/16)(H/16) x pairs x sequences / s, every 16x16 macroblock counted
+(transparent ones included).
+
+The same run also measures BASELINE's second headline, exhaustive search on
+config 5 (4K, 30 frames = 28 pairs, S = 64, 16x16) on the INT pipe: the
+`es_cfg5` object of the JSON line (its own clocks, roofline against the
+VABSDIFF4 peak measured live, a reference CPU sample, sampled parity).
 
   python bench.py [--gpus N --steps K --warmup W] [--workload cfg4-pa|cfg5-es|...]
   python bench.py --impl reference ...   # the reference's own CPU code path
 
-N > 1 (torchrun): every rank runs its own 256-sequence batch (weak scaling; seeds
-base + 256 * rank + i), no data-path collective; the motion-vector fields of
-each step are gathered into rank 0 over NCCL inside the timed region (the
-north star's "final gather of MV fields over NVLink"): packed as int8 (dx, dy)
-pairs when S <= 63 and gathered asynchronously while the next step computes
-(paper_1002_1168_b200/dist.py FieldGatherer); the last gather completes before
-the closing event.  --strong shards one
-256-sequence batch across ranks instead.
+Multi-GPU (one process per GPU; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run): config 4 is STRONG-scaled by default — the 256
+sequences are sharded over the ranks (`--weak`: 256 per rank) — and each
+step's MV fields + per-pair stats/SSE are gathered into rank 0 over NCCL,
+overlapped with the next step.  ES config 5 shards (pair, block-row band)
+units over the ranks, balanced by estimated-block count.
 """
 from __future__ import annotations
 
@@ -36,7 +40,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# workload -> (config id, algo, block size, search range, default sequences per GPU)
+# workload -> (config id, algo, block size, search range, default sequences)
 WORKLOADS = {
     "cfg4-pa": (4, "PA", 8, 16, 256),
     "cfg2-pa": (2, "PA", 8, 16, 1),
@@ -54,6 +58,7 @@ WORKLOADS = {
 }
 ALGO_ID = {"ES": 0, "TSS": 1, "FSS": 2, "DS": 3, "PA": 4}
 BASE_SEED = 20260000
+GEOMETRY = {1: "QCIF 176x144", 2: "CIF 352x288", 3: "1920x1088", 4: "CIF 352x288", 5: "3840x2160"}
 
 
 def log(*a):
@@ -69,74 +74,79 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def int_peak_path():
-    return os.path.join(ROOT, "profiles", "int_peak.json")
-
-
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled through NVML every
+    `interval` seconds by a background thread DURING the timed region."""
 
-    Q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    SLOW = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown", "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+            "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown", "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+            "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, device):
-        self.device = device
-        self.proc = None
-        self.lines = []
+    def __init__(self, device_index, interval=0.001):
+        self.device, self.interval = device_index, interval
+        self.samples, self.thread, self.err = [], None, None
+
+    def _handle(self, nv):
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            return nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.device)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml as nv
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            nv.nvmlInit()
+            self.nv, self.h = nv, self._handle(nv)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: the line says so
+            self.err = f"nvml unavailable: {e}"
+            return self
+        self.stop_flag = False
+
+        def run():
+            nv, h = self.nv, self.h
+            bits = {k: getattr(nv, v, 0) for k, v in self.SLOW.items()}
+            while not self.stop_flag:
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, [k for k, b in bits.items() if b and (r & b)]))
+                except Exception as e:
+                    self.err = str(e)
+                    return
+                time.sleep(self.interval)
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+        return self
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() in ("active", "1"):
-                    reasons.add(n)
-        return {
-            "sm_mhz": float(np.median(sm)) if sm else None,
-            "sm_max_mhz": max(mx) if mx else None,
-            "reasons": sorted(reasons),
-            "samples": len(sm),
-        }
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"], "samples": 0, "source": "nvml"}
+        self.stop_flag = True
+        self.thread.join(timeout=2)
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({r for _, rs in self.samples for r in rs})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.max_mhz), "reasons": reasons,
+                "samples": len(sm), "source": f"NVML every {self.interval * 1e3:.0f} ms during the timed region"}
 
 
-def gen_inputs(cfg_id, n_seq, first_seed, frames=None, out_luma=None, out_alpha=None):
-    from paper_1002_1168_b200 import synth
+def respawn_torchrun(args_list, n):
+    """`--gpus N` without a torchrun environment: re-launch this script as N
+    ranks (one process per GPU) and return their exit code."""
+    import socket
 
-    if cfg_id == 4:
-        return synth.config4_batch(n_seq, first_seed, frames, out_luma, out_alpha, threads=min(32, os.cpu_count() or 8))
-    l, a = synth.config_sequence(cfg_id, first_seed, frames)
-    if out_luma is not None:
-        out_luma[0] = l
-        out_alpha[0] = a
-        return out_luma, out_alpha
-    return l[None], a[None]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + args_list
+    log("[bench] launching", " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 def me_config(algo, bs, S):
@@ -145,63 +155,70 @@ def me_config(algo, bs, S):
     return me.BatchConfig(algo=me.Algo[algo], search=me.SearchConfig(search_range=S, block_size=bs, ref_distance=2), prs=me.PrsConfig())
 
 
+def workload_config(wl, args, world, n_total, F):
+    cfg_id, algo, bs, S, _ = WORKLOADS[wl]
+    strong = cfg_id == 4 and not args.weak
+    c = {
+        "workload": f"{wl}: BASELINE config {cfg_id} ({GEOMETRY[cfg_id]} x {F}f, {F - 2} pairs), {algo} S={S} bs={bs}, ref_distance 2"
+        + (f", {n_total} sequences in total ({'sharded over' if strong else 'per rank,'} {world} GPU(s))" if cfg_id == 4 else ""),
+        "config_id": cfg_id,
+        "algo": algo,
+        "search_range": S,
+        "block_size": bs,
+        "frames": F,
+        "sequences": n_total,
+        "l2": "inputs larger than L2 (126 MB)" if cfg_id in (3, 4, 5) else "L2 flushed between steps (256 MB write)",
+        "parallelism": (f"dp{world}: sequences sharded (strong), per-step gather of MV fields + pair stats/SSE to rank 0 over NCCL, overlapped with the next step"
+                        if strong else f"dp{world}: {'independent batches per rank (weak)' if cfg_id == 4 else 'replicas'}"),
+    }
+    return c
+
+
 # ---------------------------------------------------------------------------
-# CPU legs (reference arm and cpu_baseline): the reference's own code path
-# (oracle/_ref/libme_ref.so, compiled from the unmodified sources) when built,
-# else the oracle port.
+# Reference arm: the reference's own CPU code path (oracle/_ref/libme_ref.so,
+# the unmodified reference sources), inputs from the same generator compiled
+# into that library (oracle/ref_synth_glue.cpp) — libme_b200.so is never loaded.
 
 
-def cpu_oracle():
-    import oracle
-
-    if oracle.available("reference"):
-        return oracle.Oracle("reference"), "reference"
-    if not oracle.available("port"):
-        oracle.build(ref=False)
-    return oracle.Oracle("port"), "port"
-
-
-def cpu_measure(wl, luma, alpha, threads, max_seq=0):
-    """Times the CPU implementation on a bounded sample; returns (MB/s, sample, seconds)."""
+def cpu_sample(wl, luma, alpha, threads, kind_pref="reference"):
+    """Times the reference on a bounded sample of the workload with `threads`
+    host threads.  Returns (MB/s, sample text, seconds, kind)."""
     import oracle as O
 
     cfg_id, algo, bs, S, _ = WORKLOADS[wl]
-    orc, kind = cpu_oracle()
+    kind = "reference" if O.available("reference") else "port"
+    orc = O.Oracle(kind)
     cfg = O.make_cfg(algo=ALGO_ID[algo], search_range=S, block_size=bs, ref_distance=2)
     n_seq, F, H, W = luma.shape
-    mb_per_pair = (W // 16) * (H // 16)
-    if algo == "PA" or algo in ("TSS", "FSS", "DS"):
-        if algo == "PA":
-            # one sequence per thread at a time (pairs chain through the temporal candidate)
-            n = min(n_seq, max_seq or max(threads, 1) * 2)
-            t = time.perf_counter()
-            orc.time_sequences(cfg, np.ascontiguousarray(luma[:n]), np.ascontiguousarray(alpha[:n]), threads)
-            dt = time.perf_counter() - t
-            return n * (F - 2) * mb_per_pair / dt, f"{n} sequences x {F - 2} pairs ({kind}, {threads} threads)", dt, kind
+    mbpp = (W // 16) * (H // 16)
+    if algo == "PA":  # one sequence per thread (pairs chain through the temporal candidate)
+        t = time.perf_counter()
+        orc.time_sequences(cfg, np.ascontiguousarray(luma), np.ascontiguousarray(alpha), threads)
+        dt = time.perf_counter() - t
+        return n_seq * (F - 2) * mbpp / dt, f"{n_seq} sequences x {F - 2} pairs ({kind}, {threads} threads)", dt, kind
+    if algo in ("TSS", "FSS", "DS"):
         n_pairs = F - 2
         t = time.perf_counter()
         orc.time_pairs(cfg, luma[0], alpha[0], 0, n_pairs, threads)
         dt = time.perf_counter() - t
-        return n_pairs * mb_per_pair / dt, f"1 sequence x {n_pairs} pairs ({kind}, {threads} threads)", dt, kind
-    # ES: bounded sample of estimated blocks of the first pair(s); rate in
-    # macroblocks/s of the full workload = sample blocks/s scaled by the
-    # all-block / estimated-block ratio of that pair
+        return n_pairs * mbpp / dt, f"1 sequence x {n_pairs} pairs ({kind}, {threads} threads)", dt, kind
+    # ES: a bounded sample of pair 0's estimated blocks, scaled to whole pairs
     types = orc.classify(alpha[0, 2], bs)
     cols = W // bs
     est = np.flatnonzero(types != 0)
-    if est.size == 0:
-        return None, "no estimated blocks", 0.0, kind
-    # sample ~ (threads * 4) blocks, spread over the frame
     k = min(est.size, max(threads * 4, 16))
     pick = est[np.linspace(0, est.size - 1, k).astype(int)]
     xy = np.stack([(pick % cols) * bs, (pick // cols) * bs], 1).astype(np.int32)
     t = time.perf_counter()
     orc.time_blocks(cfg, np.ascontiguousarray(luma[0, 2]), np.ascontiguousarray(luma[0, 0]), xy, threads)
     dt = time.perf_counter() - t
-    blocks_per_s = k / dt
-    # a pair's macroblocks are done when its estimated blocks are
-    mbs = blocks_per_s * mb_per_pair / est.size
-    return mbs, f"{k} of {est.size} estimated blocks of pair 0 ({kind}, {threads} threads), scaled to whole pairs", dt, kind
+    return k / dt * mbpp / est.size, f"{k} of {est.size} estimated blocks of pair 0 ({kind}, {threads} threads), scaled to whole pairs", dt, kind
+
+
+def ref_inputs(cfg_id, n, first_seed, F, threads):
+    import oracle as O
+
+    return O.synth_batch(cfg_id, n, first_seed, F, threads=threads)
 
 
 def run_reference_arm(args, wl):
@@ -210,121 +227,112 @@ def run_reference_arm(args, wl):
         return 0
     cfg_id, algo, bs, S, nseq = WORKLOADS[wl]
     threads = os.cpu_count() or 1
-    n = nseq if cfg_id == 4 else 1
-    n_gen = min(n, max(64, 4 * threads)) if cfg_id == 4 else 1
-    luma, alpha = gen_inputs(cfg_id, n_gen, BASE_SEED)
-    vals = []
+    F = args.frames or {1: 10, 2: 30, 3: 60, 4: 30, 5: 30}[cfg_id]
+    n_total = (args.n_seq or nseq) if cfg_id == 4 else 1
+    # bounded sample: up to 4 sequences per host thread (a few CPU-seconds)
+    n = min(n_total, max(16, 4 * threads)) if cfg_id == 4 else 1
+    luma, alpha = ref_inputs(cfg_id, n, BASE_SEED, F, threads)
+    vals, sample, kind = [], "", "reference"
     for i in range(args.warmup + args.steps):
-        v, sample, dt, kind = cpu_measure(wl, luma, alpha, threads, max_seq=max(64, 4 * threads))
+        v, sample, dt, kind = cpu_sample(wl, luma, alpha, threads)
         if i >= args.warmup:
             vals.append(v)
     value = float(np.mean(vals))
+    one = one_core(wl, luma, alpha)
+    gpus = int(os.environ.get("WORLD_SIZE", args.gpus))
     line = {
         "impl": "reference",
         "metric": "macroblocks/sec",
         "value": value,
         "unit": "MB/s",
-        "n_gpus": args.gpus,
+        "n_gpus": gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if cfg_id == 4 and not args.weak else "weak",
         "vs_baseline": None,
         "dtype": "u8",
-        "data": "synthetic (seeded config generator, SURVEY §8d)",
-        "config": workload_config(wl, args),
-        "cpu_baseline": {"value": value, "unit": "MB/s", "cores": threads, "kind": kind, "sample": sample},
+        "data": "synthetic (seeded integer config generator, SURVEY §8d), generated by oracle/_ref (no libme_b200.so in this arm)",
+        "config": workload_config(wl, args, gpus, n_total, F),
+        "cpu_baseline": {"value": value, "unit": "MB/s", "cores": threads, "kind": kind, "sample": sample, **one},
         "e2e": {"value": value, "unit": "MB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(wl, args):
-    cfg_id, algo, bs, S, nseq = WORKLOADS[wl]
-    geo = {1: "QCIF 176x144 x 10f", 2: "CIF 352x288 x 30f", 3: "1920x1088 x 60f", 4: "CIF 352x288 x 30f", 5: "3840x2160 x 30f"}[cfg_id]
-    return {
-        "workload": f"{wl}: BASELINE config {cfg_id} ({geo}), {algo} S={S} bs={bs}, ref_distance 2" + (f", {args.n_seq or nseq} sequences/GPU" if cfg_id == 4 else ""),
-        "config_id": cfg_id,
-        "algo": algo,
-        "search_range": S,
-        "block_size": bs,
-        "sequences_per_gpu": (args.n_seq or nseq),
-        "l2": "inputs larger than L2 (126 MB)" if cfg_id in (3, 4, 5) else "L2 flushed between steps (256 MB write)",
-        "parallelism": f"sequences sharded, {args.gpus} GPU(s), MV-field gather to rank 0 (int8 pairs for S <= 63, overlapped with the next step)",
-    }
+def one_core(wl, luma, alpha):
+    """The same reference code on ONE host thread over a small sample."""
+    cfg_id = WORKLOADS[wl][0]
+    n1 = min(luma.shape[0], 4) if cfg_id == 4 else 1
+    v1, s1, dt1, _ = cpu_sample(wl, luma[:n1], alpha[:n1], 1)
+    return {"value_1core": v1, "seconds_1core": dt1, "sample_1core": s1}
 
 
 # ---------------------------------------------------------------------------
+# b200 arm
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg4-pa", choices=sorted(WORKLOADS))
-    ap.add_argument("--n-seq", type=int, default=0, help="sequences per GPU (config 4)")
-    ap.add_argument("--frames", type=int, default=0)
-    ap.add_argument("--strong", action="store_true", help="shard one batch across ranks")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=0)
-    args = ap.parse_args()
-    wl = args.workload
-    if args.impl == "reference":
-        return run_reference_arm(args, wl)
+def digest_parity(recs_np, stats_np, luma_h, alpha_h, cfg_id, algo, bs, S, threads):
+    """Checks the CUDA path's MV fields + stats of a batch against the
+    reference's own results on the same inputs (per-sequence digests,
+    oracle/ref_driver.cpp Digest).  Returns (parity dict, reference seconds)."""
+    import oracle as O
 
+    n_seq, F, H, W = luma_h.shape
+    cfg = O.make_cfg(algo=ALGO_ID[algo], search_range=S, block_size=bs, ref_distance=2)
+    t = time.perf_counter()
+    want = O.time_sequences_digest(cfg, luma_h, alpha_h, threads)
+    dt = time.perf_counter() - t
+    got = O.digest_records(recs_np, stats_np, W, H)
+    bad = np.flatnonzero(got != want)
+    return {"sequences": int(n_seq), "mismatches": int(bad.size), "first_bad": [int(i) for i in bad[:8]],
+            "how": "per-sequence digest of every MV, the SearchStats counters and the exact SSE vs the reference (oracle/_ref) on the same inputs"}, dt
+
+
+def bench_pa_batch(args, wl, world, rank, local, dev):
+    """Config 4 (or any PA/baseline batch workload): returns the JSON line (rank 0) or None."""
     import torch
     import torch.distributed as dist
 
     import paper_1002_1168_b200 as me
     from paper_1002_1168_b200 import _lib
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    cfg_id, algo, bs, S, nseq_default = WORKLOADS[wl]
-    n_seq = args.n_seq or nseq_default
-    if args.strong and cfg_id == 4:
-        n_seq = (n_seq + world - 1) // world
-    warmup = max(args.warmup, 3)
-    frames = args.frames or None
-
-    # inputs: generated on the host into pinned memory, then made resident
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import dist as mdist
     from paper_1002_1168_b200 import synth
 
-    p0 = synth.preset(cfg_id, BASE_SEED, frames)
-    F, H, W = p0.frames, p0.height, p0.width
-    # generated on the GPU (me_b200_synth_dev, byte-identical to the host
-    # generator), then copied to pinned host memory for the e2e and CPU legs
+    cfg_id, algo, bs, S, nseq_default = WORKLOADS[wl]
+    n_arg = args.n_seq or nseq_default
+    strong = cfg_id == 4 and not args.weak
+    if cfg_id == 4:
+        if strong:
+            counts = [mdist.shard(n_arg, r, world)[1] for r in range(world)]
+            first = mdist.shard(n_arg, rank, world)[0]
+            n_total = n_arg
+        else:
+            counts = [n_arg] * world
+            first = rank * n_arg
+            n_total = n_arg * world
+    else:
+        counts, first, n_total = [1] * world, 0, world
+    n_seq = counts[rank]
+    F = args.frames or {1: 10, 2: 30, 3: 60, 4: 30, 5: 30}[cfg_id]
+    warmup = max(args.warmup, 3)
     t0 = time.perf_counter()
-    luma, alpha = synth.config4_batch_dev(n_seq, BASE_SEED + 256 * rank, frames, config_id=cfg_id, device=local)
+    luma, alpha = synth.config4_batch_dev(n_seq, BASE_SEED + first, F, config_id=cfg_id, device=local)
     torch.cuda.synchronize(dev)
-    pin = torch.empty((2, n_seq, F, H, W), dtype=torch.uint8, pin_memory=True)
-    pin[0].copy_(luma)
-    pin[1].copy_(alpha)
-    hl, ha = pin[0].numpy(), pin[1].numpy()
+    H, W = luma.shape[2], luma.shape[3]
     log(f"[rank {rank}] generated {n_seq} x {F} x {H}x{W} on the device in {time.perf_counter() - t0:.2f}s")
     cfg = me_config(algo, bs, S)
     pairs = F - 2
     rows, cols = H // bs, W // bs
     recs = torch.empty((n_seq, pairs, rows, cols, 16), dtype=torch.uint8, device=dev)
     stats = torch.empty((n_seq, pairs, 48), dtype=torch.uint8, device=dev)
-    from paper_1002_1168_b200 import dist as mdist
-
-    gatherer = mdist.FieldGatherer(S) if world > 1 else None
+    gatherer = mdist.ResultGatherer(S, counts) if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if cfg_id in (1, 2) else None
     stream = torch.cuda.current_stream(dev)
     lib = me.lib()
     ctxh = _lib.ctx(local)
-    # stage events only in the untimed breakdown pass: an event between two
-    # launches would also break their programmatic-dependent-launch chain
     _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))
     import ctypes as C
 
@@ -332,12 +340,12 @@ def main():
     stage_sum = np.zeros(4)
 
     def step(stages):
-        me.run_sequences_dev(cfg, luma, alpha, recs, stats, device=local, stream=stream.cuda_stream)
+        B.run_sequences_dev(cfg, luma, alpha, recs, stats, device=local, stream=stream.cuda_stream)
         if stages:  # waits for the step: only in the untimed breakdown pass below
             _lib.check(lib.me_b200_ctx_stage_ms(ctxh, stage, 4))
             stage_sum[:] += np.array(stage[:])
-        if gatherer is not None:  # step k's packed MV field -> rank 0, overlapping step k+1
-            gatherer.submit(recs)
+        if gatherer is not None:  # step k's MV fields + stats -> rank 0, overlapping step k+1
+            gatherer.submit(recs, stats)
         if flush is not None:
             flush.fill_(1)
 
@@ -349,82 +357,77 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks = ClockSampler(local).start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
         step(False)
-    if gatherer is not None:
-        gatherer.finish()  # the last step's gather completes inside the timed region
+    gathered = gatherer.finish() if gatherer is not None else None  # the last gather completes inside the timed region
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
-    from paper_1002_1168_b200 import batch as B
-
     launches_per_step = B.last_launches(local)
+    ms = mdist.max_over_ranks(ev0.elapsed_time(ev1), dev)
+    ms_per_step = ms / args.steps
+    total_units = n_total * pairs * (W // 16) * (H // 16)
+    value = total_units / (ms_per_step / 1e3)
     # per-stage breakdown (CUDA events on the launching stream), untimed
     n_stage = min(args.steps, 20)
     _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
     for _ in range(n_stage):
         step(True)
-    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))  # the e2e leg runs without stage events
+    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))
     if gatherer is not None:
         gatherer.finish()
-    stage_sum *= args.steps / n_stage
+    stage_ms = stage_sum / n_stage
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+
+    # results of the whole batch on rank 0 (the gather's payload at N > 1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
-    total_units = n_seq * pairs * (W // 16) * (H // 16) * world
-    value = total_units / (ms_per_step / 1e3)
+        if rank == 0:
+            mv_all, st_all = gathered
+            recs_np = np.zeros((n_total, pairs, rows, cols), _lib.rec_dtype())
+            mv_np = mv_all.cpu().numpy()
+            recs_np["dx"], recs_np["dy"] = mv_np[..., 0], mv_np[..., 1]
+            stats_np = st_all.cpu().numpy().view(_lib.stats_dtype()).reshape(n_total, pairs)
+    else:
+        recs_np = recs.cpu().numpy().view(_lib.rec_dtype()).reshape(n_seq, pairs, rows, cols)
+        stats_np = stats.cpu().numpy().view(_lib.stats_dtype()).reshape(n_seq, pairs)
 
-    # correctness guard: the bench result of sequence 0 equals a host-API run
-    hrec = recs[0].cpu().numpy().view(_lib.rec_dtype()).reshape(pairs, rows, cols)
-    hstat = stats.cpu().numpy().view(_lib.stats_dtype()).reshape(n_seq, pairs)
-
-    # roofline of the step (HBM): every luma + alpha byte read once, records written once
     hbm_peak, peak_src = peaks()
-    stage_ms = stage_sum / args.steps
     alg_bytes = n_seq * F * W * H * 2 + n_seq * pairs * rows * cols * 16
     pipe_ms = float(stage_ms.sum())
     roof = None
-    # dram bytes per step from the committed ncu --set full captures (profiles/ncu_traffic.json)
-    traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tr = json.load(f).get(args.workload)
-        if tr and tr.get("n_seq") == n_seq:
-            traffic, traffic_src = float(sum(tr["dram_bytes"].values())), tr
     if algo == "PA":
+        traffic, traffic_src = None, None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                tr = json.load(f).get(wl)
+            if tr and tr.get("n_seq") == n_seq:
+                traffic, traffic_src = float(sum(tr["dram_bytes"].values())), tr
         ach = alg_bytes / (pipe_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"pipeline classify+scan+fill+PA wavefront search ({launches_per_step} launches/step)", "achieved": ach, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic, "traffic_by_kernel": traffic_src["dram_bytes"] if traffic_src else None, "algorithmic_bytes_per_step": alg_bytes, "pipeline_ms": pipe_ms,
-                "dominant": {"kernel": "pa_fast + pa_quad + pa_fast (wavefront search)", "ms": float(stage_ms[2]), "share": float(stage_ms[2]) / pipe_ms, "bound": "dependency latency + issue (see DESIGN.md)"}}
-    else:
-        cmp_total = int(hstat["block_comparisons"].sum())
-        ops = cmp_total * bs * bs  # SAD byte-ops of the search stage
-        search_s = stage_ms[2] / 1e3
-        ip = None
-        if os.path.exists(int_peak_path()):
-            with open(int_peak_path()) as f:
-                ip = json.load(f)
-        peak_t = ip["byte_ops_per_s"] / 1e12 if ip else None
-        ach = ops / search_s / 1e12
-        roof = {"bound": "int", "kernel": f"{algo.lower()}_kernel (search stage)", "achieved": ach, "peak": peak_t, "peak_source": "profiles/int_peak.json (VABSDIFF4 microbenchmark)" if ip else "not measured", "unit": "T byte-ops/s", "frac": (ach / peak_t) if peak_t else None, "traffic": None, "sad_byte_ops_per_step": ops, "search_ms": float(stage_ms[2])}
+        roof = {"bound": "hbm", "kernel": f"pipeline classify+scan+fill+PA wavefront search ({launches_per_step} launches/step; this rank's shard)",
+                "achieved": ach, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
+                "traffic_by_kernel": traffic_src["dram_bytes"] if traffic_src else None, "algorithmic_bytes_per_step": alg_bytes,
+                "pipeline_ms": pipe_ms, "timing": "stage times from CUDA events on the launching stream in an untimed pass right after the timed loop",
+                "dominant": {"kernel": "pa_fast + pa_quad + pa_fast (wavefront search)", "ms": float(stage_ms[2]), "share": float(stage_ms[2]) / pipe_ms,
+                             "bound": "dependency latency + issue (see DESIGN.md)"}}
 
     # end to end through the public host-pointer C ABI: pinned H2D + pipeline + D2H
     e2e = None
+    hl = ha = None
+    need_host = (not args.no_e2e) or (world == 1 and rank == 0)
+    if need_host:
+        pin = torch.empty((2, n_seq, F, H, W), dtype=torch.uint8, pin_memory=True)
+        pin[0].copy_(luma)
+        pin[1].copy_(alpha)
+        hl, ha = pin[0].numpy(), pin[1].numpy()
     if not args.no_e2e:
         hrecs = torch.empty((n_seq, pairs, rows, cols, 16), dtype=torch.uint8, pin_memory=True)
         hstats = torch.empty((n_seq, pairs, 48), dtype=torch.uint8, pin_memory=True)
-        from paper_1002_1168_b200 import batch as B
-
         n_e2e = args.e2e_steps or max(1, min(args.steps, 10))
         B.run_sequences_ptr(cfg, n_seq, F, W, H, hl.ctypes.data, ha.ctypes.data, hrecs.data_ptr(), hstats.data_ptr(), local)  # warm
         if world > 1:
@@ -432,39 +435,55 @@ def main():
         t = time.perf_counter()
         for _ in range(n_e2e):
             B.run_sequences_ptr(cfg, n_seq, F, W, H, hl.ctypes.data, ha.ctypes.data, hrecs.data_ptr(), hstats.data_ptr(), local)
-        e2e_s = (time.perf_counter() - t) / n_e2e
-        if world > 1:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
-        if not np.array_equal(hrecs.numpy()[0].view(_lib.rec_dtype()).reshape(pairs, rows, cols), hrec):
+        e2e_s = mdist.max_over_ranks((time.perf_counter() - t) / n_e2e, dev)
+        got = hrecs.numpy().view(_lib.rec_dtype()).reshape(n_seq, pairs, rows, cols)
+        if not np.array_equal(got, recs.cpu().numpy().view(_lib.rec_dtype()).reshape(n_seq, pairs, rows, cols)):
             raise SystemExit("e2e records differ from the device-resident run")
-        h2d, d2h = B.last_transfer_bytes(local)  # counted by the library: alpha masks cross bit-packed
-        # this box's pinned H2D bandwidth (256 MiB copies): the e2e step's copy floor is h2d / it
+        h2d, d2h = B.last_transfer_bytes(local)
         probe_h = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
         probe_d = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         probe_d.copy_(probe_h, non_blocking=True)
         torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         for _ in range(4):
             probe_d.copy_(probe_h, non_blocking=True)
-        ev1.record()
+        e1.record()
         torch.cuda.synchronize()
-        h2d_gbs = 4 * (256 << 20) / (ev0.elapsed_time(ev1) * 1e-3) / 1e9
+        h2d_gbs = 4 * (256 << 20) / (e0.elapsed_time(e1) * 1e-3) / 1e9
         del probe_h, probe_d
-        e2e = {"value": total_units / e2e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e, "s_per_step": e2e_s,
-               "input_bytes_per_step": int(2 * n_seq * F * W * H), "h2d_gbs_measured": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6, "note": "pinned host buffers; luma as bytes, binary alpha bit-packed on the host cores (AVX-512) with all-zero 64-pixel words elided, expanded on the GPU"}
+        e2e = {"value": total_units / e2e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e,
+               "s_per_step": e2e_s, "input_bytes_per_step": int(2 * n_seq * F * W * H), "h2d_gbs_measured": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6,
+               "note": "pinned host buffers through me_b200_run_sequences (per rank: its shard); luma as bytes, binary alpha bit-packed on the host cores with all-zero 64-pixel words elided, expanded on the GPU"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        # the whole batch (~10 CPU-seconds at 256 sequences)
-        v, sample, dt, kind = cpu_measure(wl, hl, ha, threads, max_seq=n_seq)
-        cpu = {"value": v, "unit": "MB/s", "cores": threads, "kind": kind, "sample": sample, "seconds": dt}
-
+    line = None
     if rank == 0:
-        est = int(hstat["blocks_opaque"].sum() + hstat["blocks_boundary"].sum())
+        threads = os.cpu_count() or 1
+        # the whole batch's inputs on this host: the device-generated bytes at
+        # N = 1, the same generator on the host cores otherwise
+        if world == 1:
+            lh, ah = hl, ha
+        else:
+            import oracle
+
+            lh, ah = oracle.synth_batch(cfg_id, n_total, BASE_SEED, F, threads=threads) if cfg_id == 4 else oracle.synth_batch(cfg_id, 1, BASE_SEED, F, threads=1)
+        parity, ref_s = None, None
+        if not args.no_parity and algo == "PA":
+            parity, ref_s = digest_parity(recs_np, stats_np, lh, ah, cfg_id, algo, bs, S, threads)
+            log(f"[bench] parity vs reference: {parity['mismatches']} of {parity['sequences']} sequences differ")
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            if ref_s is not None:  # the parity run IS the reference on the whole batch, all host threads
+                import oracle
+
+                cpu = {"value": n_total * pairs * (W // 16) * (H // 16) / ref_s, "unit": "MB/s", "cores": threads,
+                       "kind": "reference" if oracle.available("reference") else "port",
+                       "sample": f"the whole batch: {n_total} sequences x {pairs} pairs, {threads} threads (the parity run)", "seconds": ref_s}
+            else:
+                v, sample, dt, kind = cpu_sample(wl, lh, ah, threads)
+                cpu = {"value": v, "unit": "MB/s", "cores": threads, "kind": kind, "sample": sample, "seconds": dt}
+            cpu.update(one_core(wl, lh, ah))
+        est = int(stats_np["blocks_opaque"].sum() + stats_np["blocks_boundary"].sum())
         line = {
             "metric": "macroblocks/sec",
             "value": value,
@@ -474,20 +493,258 @@ def main():
             "warmup": warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak",
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
             "dtype": "u8",
             "data": "synthetic (seeded integer config generator, SURVEY §8d; no public sequences in this container)",
-            "config": workload_config(wl, args),
+            "config": workload_config(wl, args, world, n_total, F),
             "roofline": roof,
             "stages_ms": {"classify": stage_ms[0], "sort": stage_ms[1], "search": stage_ms[2], "mc_psnr": stage_ms[3]},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
-            "estimated_blocks_per_gpu": int(est * 1),
+            "parity": parity,
+            "estimated_blocks": est,
             "macroblocks_per_step": int(total_units),
         }
+        if parity is not None and parity["mismatches"]:
+            print(json.dumps(line), flush=True)
+            raise SystemExit(f"parity FAILED: {parity['mismatches']} sequences differ from the reference")
+    del luma, alpha, recs, stats
+    torch.cuda.empty_cache()
+    return line
+
+
+# ---------------------------------------------------------------------------
+# ES on config 5 (the INT-pipe headline), sharded by (pair, row band) units
+
+
+def es_units(alpha_dev, bs, pairs, d, n_bands):
+    """Estimated-block count of every (band, pair) unit, band-major."""
+    import torch
+
+    F, H, W = alpha_dev.shape
+    rows, cols = H // bs, W // bs
+    cur = alpha_dev[d:d + pairs].view(pairs, rows, bs, cols, bs)
+    est = (cur.amax(dim=(2, 4)) > 0).to(torch.int64)  # classify_block: any sample set -> not transparent
+    per_row = est.sum(dim=2).cpu().numpy()  # [pairs, rows]
+    edges = np.linspace(0, rows, n_bands + 1).round().astype(int)
+    units = []
+    for b in range(n_bands):
+        for p in range(pairs):
+            units.append((b, p, int(edges[b]), int(edges[b + 1]), int(per_row[p, edges[b]:edges[b + 1]].sum())))
+    return units
+
+
+def split_units(units, world):
+    """Contiguous (band-major) split balanced by estimated-block count."""
+    cost = np.array([u[4] + 1 for u in units], dtype=np.float64)
+    cum = np.concatenate([[0], np.cumsum(cost)])
+    cuts = [0] + [int(np.searchsorted(cum, cum[-1] * r / world)) for r in range(1, world)] + [len(units)]
+    return [units[cuts[r]:cuts[r + 1]] for r in range(world)]
+
+
+def runs_of(my_units):
+    """Groups a rank's units into calls: same band, consecutive pairs."""
+    runs = []
+    for b, p, r0, r1, _ in my_units:
+        if runs and runs[-1][0] == b and runs[-1][2] == p:
+            runs[-1][2] = p + 1
+        else:
+            runs.append([b, p, p + 1, r0, r1])
+    return runs
+
+
+def bench_es_cfg5(args, world, rank, local, dev):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1002_1168_b200 as me
+    from paper_1002_1168_b200 import _lib
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import dist as mdist
+    from paper_1002_1168_b200 import synth
+    import ctypes as C
+
+    cfg_id, algo, bs, S = 5, "ES", 16, 64
+    F = args.es_frames or 30
+    pairs, d = F - 2, 2
+    luma, alpha = synth.config4_batch_dev(1, BASE_SEED, F, config_id=5, device=local)
+    torch.cuda.synchronize(dev)
+    _, _, H, W = luma.shape
+    rows, cols = H // bs, W // bs
+    cfg = me_config(algo, bs, S)
+    n_bands = 1 if world == 1 else 4
+    units = es_units(alpha[0], bs, pairs, d, n_bands)
+    mine = split_units(units, world)[rank]
+    runs = runs_of(mine)
+    recs = torch.zeros((1, pairs, rows, cols, 16), dtype=torch.uint8, device=dev)
+    stats_acc = torch.zeros((pairs, 6), dtype=torch.int64, device=dev)
+    tmp_stats = torch.empty((1, pairs, 48), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    lib = me.lib()
+    ctxh = _lib.ctx(local)
+
+    def step():
+        stats_acc.zero_()
+        for b, p0, p1, r0, r1 in runs:
+            n = p1 - p0
+            lv, av = luma[:, p0:p1 + d], alpha[:, p0:p1 + d]
+            rv, sv = recs[:, p0:p1], tmp_stats[:, :n]
+            if world == 1:
+                B.run_sequences_dev(cfg, lv, av, rv, sv, device=local, stream=stream.cuda_stream)
+            else:
+                B.run_band_dev(cfg, lv, av, r0, r1, rv, sv, device=local, stream=stream.cuda_stream)
+            stats_acc[p0:p1] += sv[0].view(torch.int64).view(n, 6)
+        if world > 1:  # MV words of my units + my partial stats -> rank 0
+            mvw = mdist.mv_words(recs[0])
+            outs = [torch.empty_like(mvw) for _ in range(world)] if rank == 0 else None
+            sts = [torch.empty_like(stats_acc) for _ in range(world)] if rank == 0 else None
+            dist.gather(mvw, outs, dst=0)
+            dist.gather(stats_acc, sts, dst=0)
+            return outs, sts
+        return None, None
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local).start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.es_steps):
+        outs, sts = step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = mdist.max_over_ranks(ev0.elapsed_time(ev1), dev) / args.es_steps
+    # search-stage time of this rank's calls (stage events, untimed pass)
+    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
+    stage = (C.c_float * 4)()
+    search_ms = 0.0
+    for b, p0, p1, r0, r1 in runs:
+        n = p1 - p0
+        lv, av = luma[:, p0:p1 + d], alpha[:, p0:p1 + d]
+        if world == 1:
+            B.run_sequences_dev(cfg, lv, av, recs[:, p0:p1], tmp_stats[:, :n], device=local, stream=stream.cuda_stream)
+        else:
+            B.run_band_dev(cfg, lv, av, r0, r1, recs[:, p0:p1], tmp_stats[:, :n], device=local, stream=stream.cuda_stream)
+        _lib.check(lib.me_b200_ctx_stage_ms(ctxh, stage, 4))
+        search_ms += stage[2]
+    _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))
+    search_ms = mdist.max_over_ranks(search_ms, dev)
+    ipk = C.c_double()
+    _lib.check(lib.me_b200_probe_int_peak(ctxh, C.byref(ipk)))
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        return None
+    # whole-sequence results on rank 0
+    if world > 1:
+        owner = {}
+        for r, us in enumerate(split_units(units, world)):
+            for b, p, r0, r1, _ in us:
+                owner[(p, b)] = (r, r0, r1)
+        mv = torch.zeros((pairs, rows, cols), dtype=torch.int32, device=dev)
+        for (p, b), (r, r0, r1) in owner.items():
+            mv[p, r0:r1] = outs[r][p, r0:r1]
+        st = torch.stack(sts).sum(0).cpu().numpy()
+        mvn = mv.cpu().numpy()
+        dx, dy = (mvn << 16) >> 16, mvn >> 16
+        cmp_total = int(st[:, 0].sum())
+    else:
+        rn = recs[0].cpu().numpy().view(_lib.rec_dtype()).reshape(pairs, rows, cols)
+        dx, dy = rn["dx"].astype(np.int32), rn["dy"].astype(np.int32)
+        st = stats_acc.cpu().numpy()
+        cmp_total = int(st[:, 0].sum())
+    ops = cmp_total * bs * bs
+    units_mb = pairs * (W // 16) * (H // 16)
+    # sampled parity: estimated blocks spread over the pairs vs the reference's full_search
+    import oracle as O
+
+    lh, ah = luma[0].cpu().numpy(), alpha[0].cpu().numpy()
+    parity = None
+    if not args.no_parity:
+        orc = O.Oracle("reference" if O.available("reference") else "port")
+        rng = np.random.default_rng(5)
+        bad, n_chk = 0, 0
+        for p in rng.choice(pairs, size=min(8, pairs), replace=False):
+            types = orc.classify(ah[p + d], bs)
+            est = np.flatnonzero(types != 0)
+            for gi in rng.choice(est, size=min(6, est.size), replace=False):
+                v, h = divmod(int(gi), cols)
+                (rdx, rdy), rcmp, rcost = orc.block_search(0, lh[p + d], lh[p], h * bs, v * bs, bs, S)
+                n_chk += 1
+                bad += (int(dx[p, v, h]), int(dy[p, v, h])) != (rdx, rdy)
+        parity = {"blocks_checked": n_chk, "mismatches": bad, "how": f"ES MVs of randomly sampled estimated blocks vs the reference's full_search ({orc.kind})"}
+    threads = os.cpu_count() or 1
+    wl = "cfg5-es"
+    v_cpu, sample, dt, kind = cpu_sample(wl, lh[None], ah[None], threads)
+    peak = ipk.value / 1e12
+    ach = ops / (search_ms / 1e3) / 1e12
+    return {
+        "workload": f"cfg5-es: BASELINE config 5 (3840x2160 x {F}f, {pairs} pairs), ES S=64 bs=16" + (f", (pair, row-band) units over {world} GPUs" if world > 1 else ""),
+        "metric": "macroblocks/sec", "value": units_mb / (ms / 1e3), "unit": "MB/s", "ms_per_step": ms, "steps": args.es_steps,
+        "sad_byte_ops_per_step": ops, "search_ms": search_ms,
+        "roofline": {"bound": "int", "kernel": "es_kernel (search stage)", "achieved": ach, "peak": peak, "unit": "T byte-ops/s", "frac": ach / peak,
+                     "peak_source": "VABSDIFF4.U8.ACC microbenchmark measured in this run on this GPU (me_b200_probe_int_peak)",
+                     "note": "achieved = oracle-exact comparisons x 256 byte-ops / search-stage time (CUDA events)"},
+        "clocks": clk, "parity": parity,
+        "cpu_baseline": {"value": v_cpu, "unit": "MB/s", "cores": threads, "kind": kind, "sample": sample, "seconds": dt},
+        "units": {"n": len(units), "bands": n_bands, "per_rank": [len(u) for u in split_units(units, world)]},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg4-pa", choices=sorted(WORKLOADS))
+    ap.add_argument("--n-seq", type=int, default=0, help="config 4: sequences in total (strong) or per rank (--weak)")
+    ap.add_argument("--weak", action="store_true", help="config 4: every rank runs its own batch")
+    ap.add_argument("--frames", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-es", action="store_true", help="skip the es_cfg5 leg of the default run")
+    ap.add_argument("--es-steps", type=int, default=5)
+    ap.add_argument("--es-frames", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args()
+    wl = args.workload
+    if args.impl == "reference":
+        return run_reference_arm(args, wl)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return respawn_torchrun(sys.argv[1:], args.gpus)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    line = bench_pa_batch(args, wl, world, rank, local, dev) if wl != "cfg5-es" else None
+    es = None
+    if wl == "cfg5-es" or (wl == "cfg4-pa" and not args.no_es):
+        es = bench_es_cfg5(args, world, rank, local, dev)
+    if rank == 0:
+        if line is None:  # --workload cfg5-es: the ES leg is the line
+            line = {"metric": "macroblocks/sec", "value": es["value"], "unit": "MB/s", "n_gpus": world, "steps": es["steps"], "warmup": max(args.warmup, 3),
+                    "ms_per_step": es["ms_per_step"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+                    "data": "synthetic (seeded integer config generator, SURVEY §8d)", "config": {"workload": es["workload"]}, "roofline": es["roofline"],
+                    "cpu_baseline": es["cpu_baseline"], "e2e": None, "clocks": es["clocks"], "parity": es["parity"]}
+        else:
+            line["es_cfg5"] = es
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -167,6 +167,27 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
                                     const uint8_t* alpha, me_block_rec* recs,
                                     me_pair_stats* stats, uint8_t* pred, void* stream);
 
+/* A block-row band [row0, row1) of the same batch (baselines ES/TSS/FSS/DS
+ * only; PA blocks depend on the rows above -> ME_ERR_INVALID_ARGUMENT): the
+ * unit of the row sharding across GPUs.  Records of the band's
+ * blocks are written (the others are left untouched); stats are the band's
+ * share of each pair's SearchStats + SSE, so the bands' stats of a pair sum
+ * to the whole pair's.  Device pointers, enqueued on `stream`. */
+me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames,
+                               int width, int height, const uint8_t* luma, const uint8_t* alpha,
+                               int row0, int row1, me_block_rec* recs, me_pair_stats* stats,
+                               void* stream);
+
+/* The batch of me_b200_run_sequences over devices 0..n_gpus-1 of this
+ * process (the reference's run_experiment pair loop, bench.cpp:155-205,
+ * sharded): sequences split contiguously over the devices (a single
+ * baseline sequence: its frame pairs), each shard end to end on its own host
+ * thread and context, results written straight into the host arrays.  HOST
+ * buffers; synchronous. */
+me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_frames, int width,
+                                      int height, const uint8_t* luma, const uint8_t* alpha,
+                                      me_block_rec* recs, me_pair_stats* stats, int n_gpus);
+
 /* Same, end to end from HOST buffers: H2D of the inputs, the device pipeline,
  * D2H of the records and stats (and pred when non-NULL), synchronous. */
 me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames,
@@ -255,6 +276,11 @@ me_status me_b200_predict_frame(me_ctx* ctx, int width, int height, const uint8_
 /* psnr numerator (metrics.cpp:108-124): int64 sum of squared luma differences. */
 me_status me_b200_sse(me_ctx* ctx, int width, int height, const uint8_t* a, const uint8_t* b,
                       int64_t* out_sse);
+
+/* The INT-pipe roofline denominator of the SAD kernels, measured on ctx's
+ * device now: VABSDIFF4.U8.ACC byte-ops per second of independent chains at
+ * full occupancy (best of 10 launches, CUDA events). */
+me_status me_b200_probe_int_peak(me_ctx* ctx, double* byte_ops_per_s);
 
 /* ---------------------------------------------------------------------------
  * Deterministic synthetic sequences (host code, integer-only so

@@ -253,3 +253,100 @@ class Oracle:
         self._chk(self._f("run_experiment")(enc(path), fmt, W, H, enc(mask_pattern), a, len(algos), C.byref(cfg),
                                             int(block_size_auto), frame_limit, enc(csv_path), enc(dump_dir), _vp(out)))
         return out
+
+
+# ---------------------------------------------------------------------------
+# Input generation for the reference arm (oracle/ref_synth_glue.cpp): the
+# product's host generator compiled into oracle/_ref/libme_ref.so, so the
+# reference arm never loads libme_b200.so.  Same bytes as
+# paper_1002_1168_b200.synth (checked by tests/test_synth.py).
+
+
+class SynthParams(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32), ("height", C.c_int32), ("frames", C.c_int32), ("seed", C.c_uint64),
+        ("blur_sigma_q8", C.c_int32), ("bg_jitter", C.c_int32), ("bg_drift_q8", C.c_int32 * 2),
+        ("n_objects", C.c_int32), ("obj_min", C.c_int32), ("obj_max", C.c_int32),
+        ("obj_w", C.c_int32 * 4), ("obj_h", C.c_int32 * 4), ("obj_v", (C.c_int32 * 2) * 4),
+        ("vel_fixed", C.c_int32), ("vmax", C.c_int32), ("shapes", C.c_int32), ("noise_sigma_q8", C.c_int32),
+    ]
+
+
+_REF_HANDLE = None
+
+
+def _ref_lib():
+    global _REF_HANDLE
+    if _REF_HANDLE is None:
+        _REF_HANDLE = C.CDLL(REF_LIB)
+        _REF_HANDLE.ref_synth_last_error.restype = C.c_char_p
+    return _REF_HANDLE
+
+
+def synth_preset(config_id: int, seed: int, frames=None) -> SynthParams:
+    L = _ref_lib()
+    p = SynthParams()
+    if L.ref_synth_preset(int(config_id), C.c_uint64(seed), C.byref(p)) != ME_OK:
+        raise OracleError(1, L.ref_synth_last_error().decode())
+    if frames:
+        p.frames = int(frames)
+    return p
+
+
+def synth_generate(p: SynthParams, luma=None, alpha=None):
+    shape = (p.frames, p.height, p.width)
+    luma = np.empty(shape, np.uint8) if luma is None else luma
+    alpha = np.empty(shape, np.uint8) if alpha is None else alpha
+    L = _ref_lib()
+    if L.ref_synth(C.byref(p), _vp(luma), _vp(alpha)) != ME_OK:
+        raise OracleError(1, L.ref_synth_last_error().decode())
+    return luma, alpha
+
+
+def synth_batch(config_id: int, n_seq: int, base_seed: int, frames=None, threads: int = 8):
+    """n_seq sequences with seed = base + i ([n_seq, F, H, W] luma, alpha)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    p0 = synth_preset(config_id, base_seed, frames)
+    shape = (n_seq, p0.frames, p0.height, p0.width)
+    luma, alpha = np.empty(shape, np.uint8), np.empty(shape, np.uint8)
+
+    def one(i):
+        synth_generate(synth_preset(config_id, base_seed + i, frames), luma[i], alpha[i])
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        list(ex.map(one, range(n_seq)))
+    return luma, alpha
+
+
+def time_sequences_digest(cfg: _Cfg, luma, alpha, threads: int):
+    """The reference's own estimate_field + predict_frame + psnr loop over
+    n_seq sequences on `threads` host threads; returns the per-sequence result
+    digests (uint64, see ref_driver.cpp Digest)."""
+    n_seq, F, H, W = luma.shape
+    dig = np.zeros(n_seq, np.uint64)
+    cs = C.c_int64()
+    L = _ref_lib()
+    L.ref_last_error.restype = C.c_char_p
+    rc = L.ref_time_sequences_digest(C.byref(cfg), n_seq, F, W, H, _vp(luma), _vp(alpha), threads, C.byref(cs), _vp(dig))
+    if rc != ME_OK:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return dig
+
+
+def digest_records(recs, stats, W: int, H: int) -> np.ndarray:
+    """The same digest from record/stat arrays ([n_seq, pairs, rows, cols] of
+    the record dtype, [n_seq, pairs] of the stats dtype), e.g. the CUDA path's."""
+    n_seq, pairs, rows, cols = recs.shape
+    nb = rows * cols
+    dx = recs["dx"].astype(np.int64).astype(np.uint64).reshape(n_seq, pairs * nb)
+    dy = recs["dy"].astype(np.int64).astype(np.uint64).reshape(n_seq, pairs * nb)
+    w = (2 * np.arange(pairs * nb, dtype=np.uint64) + np.uint64(1))
+    with np.errstate(over="ignore"):
+        v = ((dx * np.uint64(0x9E37) + dy * np.uint64(0x7F4B) + np.uint64(1)) * w[None, :]).sum(axis=1, dtype=np.uint64)
+        st = stats
+        s = (st["block_comparisons"].astype(np.uint64) * np.uint64(1000003) + st["dpd_refinement_steps"].astype(np.uint64) * np.uint64(7919)
+             + st["blocks_opaque"].astype(np.uint64) * np.uint64(131) + st["blocks_boundary"].astype(np.uint64) * np.uint64(137)
+             + st["blocks_transparent"].astype(np.uint64) * np.uint64(139) + st["sse"].astype(np.uint64) * np.uint64(17))
+        v = v + s.sum(axis=1, dtype=np.uint64)
+    return v

@@ -198,10 +198,32 @@ int run_sequence_impl(const me_config* c, int n_frames, int w, int h, const uint
     return 0;
 }
 
+// Result digest of one sequence (order-dependent, uint64 wrap-around):
+// sum over pairs p and blocks i (raster) of (dx * 0x9E37 + dy * 0x7F4B + 1) *
+// (2 * (p * blocks + i) + 1), plus sum over pairs of the SearchStats counters
+// and the exact SSE (psnr's mse * W * H, rounded) with fixed weights.  The same
+// digest computed from the CUDA path's records and stats (bench.py) checks
+// the benchmarked batch against the reference without shipping every record.
+struct Digest {
+    uint64_t v = 0;
+    void field(const MotionField& f, uint64_t pair) {
+        const uint64_t n = f.vectors.size();
+        for (uint64_t i = 0; i < n; ++i) {
+            const MotionVector& m = f.vectors[i];
+            v += (uint64_t(int64_t(m.dx)) * 0x9E37u + uint64_t(int64_t(m.dy)) * 0x7F4Bu + 1u) * (2u * (pair * n + i) + 1u);
+        }
+    }
+    void stats(const SearchStats& s, int64_t sse) {
+        v += uint64_t(s.block_comparisons) * 1000003u + uint64_t(s.dpd_refinement_steps) * 7919u +
+             uint64_t(s.blocks_opaque) * 131u + uint64_t(s.blocks_boundary) * 137u +
+             uint64_t(s.blocks_transparent) * 139u + uint64_t(sse) * 17u;
+    }
+};
+
 // Plain timing path: estimate_field + predict_frame + psnr exactly as
 // run_experiment calls them (no replay), for the CPU baseline.
 int time_sequence_impl(const me_config* c, int n_frames, int w, int h, const uint8_t* luma,
-                       const uint8_t* alpha, int64_t* mvsum) {
+                       const uint8_t* alpha, int64_t* mvsum, uint64_t* digest = nullptr) {
     const size_t plane = size_t(w) * h;
     std::vector<Frame> frames;
     std::vector<AlphaPlane> masks;
@@ -218,6 +240,7 @@ int time_sequence_impl(const me_config* c, int n_frames, int w, int h, const uin
     const Algo algo = static_cast<Algo>(c->algo);
     std::optional<MotionField> prev;
     int64_t acc = 0;
+    Digest dg;
     for (int tau = c->ref_distance; tau < n_frames; ++tau) {
         const Frame& cur = frames[tau];
         const Frame& ref = frames[tau - c->ref_distance];
@@ -226,11 +249,16 @@ int time_sequence_impl(const me_config* c, int n_frames, int w, int h, const uin
                                              prev ? &*prev : nullptr, scfg, prs, opts);
         const Frame pred = predict_frame(ref, field, scfg);
         const PsnrResult pr = psnr(cur, pred);
+        if (digest) {
+            dg.field(field, uint64_t(tau - c->ref_distance));
+            dg.stats(stats, int64_t(std::llround(pr.mse * double(plane))));
+        }
         acc += stats.block_comparisons + int64_t(pr.mse);
         for (const MotionVector& v : field.vectors) acc += v.dx + 3 * v.dy;
         if (algo == Algo::PA) prev = std::move(field);
     }
     if (mvsum) *mvsum = acc;
+    if (digest) *digest = dg.v;
     return 0;
 }
 
@@ -253,8 +281,19 @@ int ref_run_sequence(const me_config* c, int n_frames, int w, int h, const uint8
 // Times `n_seq` independent sequences of the same shape on `threads` host
 // threads (one sequence per thread at a time), the reference's own code path.
 // Returns 0; *checksum is an order-independent digest of the results.
+int ref_time_sequences_digest(const me_config* c, int n_seq, int n_frames, int w, int h,
+                              const uint8_t* luma, const uint8_t* alpha, int threads, int64_t* checksum,
+                              uint64_t* digests);
 int ref_time_sequences(const me_config* c, int n_seq, int n_frames, int w, int h,
                        const uint8_t* luma, const uint8_t* alpha, int threads, int64_t* checksum) {
+    return ref_time_sequences_digest(c, n_seq, n_frames, w, h, luma, alpha, threads, checksum, nullptr);
+}
+
+// As ref_time_sequences, plus the per-sequence result digest (Digest above)
+// into digests[n_seq] when non-null.
+int ref_time_sequences_digest(const me_config* c, int n_seq, int n_frames, int w, int h,
+                              const uint8_t* luma, const uint8_t* alpha, int threads, int64_t* checksum,
+                              uint64_t* digests) {
     std::atomic<int> next{0};
     std::atomic<int64_t> sum{0};
     std::atomic<int> rc{0};
@@ -266,7 +305,7 @@ int ref_time_sequences(const me_config* c, int n_seq, int n_frames, int w, int h
             int64_t cs = 0;
             try {
                 time_sequence_impl(c, n_frames, w, h, luma + seq * s,
-                                   alpha ? alpha + seq * s : nullptr, &cs);
+                                   alpha ? alpha + seq * s : nullptr, &cs, digests ? digests + s : nullptr);
             } catch (const std::exception& e) {
                 rc = fail(e);
             }

@@ -135,6 +135,8 @@ SIGNATURES = {
     "me_b200_pack_mask": (I, [P, C.c_size_t, P, C.c_size_t, C.POINTER(C.c_size_t)]),
     "me_b200_run_sequences_dev": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P, P]),
     "me_b200_run_sequences": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P]),
+    "me_b200_run_band_dev": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, I, I, P, P, P]),
+    "me_b200_run_sequences_multi": (I, [C.POINTER(MeConfig), I, I, I, I, P, P, P, P, I]),
     "me_b200_estimate_field": (I, [P, C.POINTER(MeConfig), I, I, P, P, P, P, P, I, I, P, P]),
     "me_b200_block_search": (I, [P, I, I, I, P, P, I, I, I, I, I32P, I64P, U32P]),
     "me_b200_brs_select": (I, [P, I, I, P, P, P, P, I, I, I, I, I32P, I, I, I32P, U8P, U32P]),
@@ -146,6 +148,7 @@ SIGNATURES = {
     "me_b200_binarize": (I, [P, I, I, P, I, P]),
     "me_b200_predict_frame": (I, [P, I, I, P, P, P, I, P, P, I64P]),
     "me_b200_sse": (I, [P, I, I, P, P, I64P]),
+    "me_b200_probe_int_peak": (I, [P, C.POINTER(C.c_double)]),
     "me_b200_synth_preset": (I, [I, C.c_uint64, C.POINTER(MeSynthParams)]),
     "me_b200_synth": (I, [C.POINTER(MeSynthParams), P, P]),
     "me_b200_synth_dev": (I, [P, C.POINTER(MeSynthParams), I, P, P, P]),

@@ -57,6 +57,7 @@ def run_sequences_dev(cfg: BatchConfig, luma, alpha=None, recs=None, stats=None,
         recs = torch.empty((n_seq, pairs, rows, cols, 16), dtype=torch.uint8, device=luma.device)
     if stats is None:
         stats = torch.empty((n_seq, pairs, 48), dtype=torch.uint8, device=luma.device)
+    _check_dev_buffers(luma, alpha, recs, stats, pred, device, (n_seq, pairs, rows, cols, 16), (n_seq, pairs, 48), (n_seq, pairs, H, W))
     if stream is None:
         stream = torch.cuda.current_stream(luma.device).cuda_stream
     c = cfg.c()
@@ -70,6 +71,64 @@ def run_sequences_dev(cfg: BatchConfig, luma, alpha=None, recs=None, stats=None,
             C.c_void_p(stream),
         )
     )
+    return recs, stats
+
+
+def _check_dev_buffers(luma, alpha, recs, stats, pred, device, recs_shape, stats_shape, pred_shape):
+    """The C ABI takes raw device pointers: wrong dtype, strides, device or
+    sizes would be silently misread (or written out of bounds), so check here."""
+    import torch
+
+    def chk(name, t, shape):
+        if t is None:
+            return
+        if t.dtype != torch.uint8 or not t.is_contiguous() or t.device.type != "cuda" or t.device.index != device:
+            raise ValueError(f"{name}: need a contiguous uint8 tensor on cuda:{device}")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+
+    chk("luma", luma, luma.shape)
+    chk("alpha", alpha, luma.shape)
+    chk("recs", recs, recs_shape)
+    chk("stats", stats, stats_shape)
+    chk("pred", pred, pred_shape)
+
+
+def run_band_dev(cfg: BatchConfig, luma, alpha, row0: int, row1: int, recs, stats, device: int = 0, stream=None):
+    """The block-row band [row0, row1) of a device-resident batch
+    (me_b200_run_band_dev; baselines only): writes the band's records, and its
+    share of each pair's stats into `stats` (zeroed first by the library)."""
+    import torch
+
+    n_seq, F, H, W = luma.shape
+    bs = cfg.search.block_size
+    pairs = F - cfg.search.ref_distance
+    _check_dev_buffers(luma, alpha, recs, stats, None, device, (n_seq, pairs, H // bs, W // bs, 16), (n_seq, pairs, 48), None)
+    if stream is None:
+        stream = torch.cuda.current_stream(luma.device).cuda_stream
+    c = cfg.c()
+    check(lib().me_b200_run_band_dev(ctx(device), C.byref(c), n_seq, F, W, H, C.c_void_p(luma.data_ptr()),
+                                     C.c_void_p(alpha.data_ptr()) if alpha is not None else None, int(row0), int(row1),
+                                     C.c_void_p(recs.data_ptr()), C.c_void_p(stats.data_ptr()), C.c_void_p(stream)))
+    return recs, stats
+
+
+def run_sequences_multi(cfg: BatchConfig, luma: np.ndarray, alpha: Optional[np.ndarray] = None, n_gpus: int = 1):
+    """me_b200_run_sequences_multi: the host batch sharded over n_gpus devices
+    of this process (sequences, or a single baseline sequence's frame pairs)."""
+    luma = np.ascontiguousarray(luma, np.uint8)
+    if luma.ndim == 3:
+        luma = luma[None]
+    n_seq, F, H, W = luma.shape
+    if alpha is not None:
+        alpha = np.ascontiguousarray(alpha, np.uint8).reshape(luma.shape)
+    bs = cfg.search.block_size
+    pairs = F - cfg.search.ref_distance
+    recs = np.zeros((n_seq, pairs, H // bs, W // bs), _lib.rec_dtype())
+    stats = np.zeros((n_seq, pairs), _lib.stats_dtype())
+    c = cfg.c()
+    vp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+    check(lib().me_b200_run_sequences_multi(C.byref(c), n_seq, F, W, H, vp(luma), vp(alpha), vp(recs), vp(stats), int(n_gpus)))
     return recs, stats
 
 

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.h"
@@ -40,10 +41,16 @@ bool device_ok(int dev) {
     return p.major == 10;  // sm_100 family (the fatbin carries sm_100a code only)
 }
 
+constexpr int kMaxSearchRange = 255;
+
 // SearchConfig::validate + PrsConfig::validate (estimators.cpp:139-150)
 me_status validate(const me_config* c) {
     if (!c) return me_fail(ME_ERR_INVALID_ARGUMENT, "null config");
     if (c->search_range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    // implementation limit of the B200 path (the reference takes any S >= 1):
+    // the ES tie-break key holds |dx| + |dy| <= 2S in 9 bits
+    if (c->search_range > kMaxSearchRange)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range above 255 is not supported by the B200 path");
     if (c->block_size != 8 && c->block_size != 16)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
     if (c->ref_distance < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "ref_distance must be >= 1");
@@ -426,6 +433,85 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
     return ok();
 }
 
+me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
+                               int H, const uint8_t* luma, const uint8_t* alpha, int row0, int row1,
+                               me_block_rec* recs, me_pair_stats* stats, void* stream) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
+    if (cfg->algo == ME_ALGO_PA)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "PA blocks depend on the rows above: no row bands");
+    const int rows = H / cfg->block_size;
+    if (row0 < 0 || row1 > rows || row0 >= row1) return me_fail(ME_ERR_INVALID_ARGUMENT, "bad row band");
+    if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    if ((reinterpret_cast<uintptr_t>(luma) | reinterpret_cast<uintptr_t>(alpha) |
+         reinterpret_cast<uintptr_t>(recs)) & 15)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "device buffers must be 16-byte aligned");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H, luma, alpha);
+    b.v0 = row0;
+    b.v1 = row1;
+    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+    int nl = 0;
+    ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
+                           st, ctx->events(), false, &nl));
+    ctx->launches = nl;
+    ctx->ev_valid = ctx->profiling;
+    return ok();
+}
+
+// Several devices from one process: units (sequences, or for a single
+// sequence of a baseline, frame pairs) sharded contiguously over devices
+// 0..n_gpus-1, each shard run end to end by its own host thread and context;
+// the results land in the caller's host arrays, so rank 0's gather is the
+// D2H itself.
+me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_frames, int W, int H,
+                                      const uint8_t* luma, const uint8_t* alpha, me_block_rec* recs,
+                                      me_pair_stats* stats, int n_gpus) {
+    me_status s = check_batch(cfg, n_seq, n_frames, W, H);
+    if (s) return s;
+    if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+    if (n_gpus < 1 || n_gpus > ndev)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "n_gpus must be between 1 and the visible device count");
+    const size_t plane = size_t(W) * H, seq_bytes = plane * n_frames;
+    const int pairs = n_frames - cfg->ref_distance;
+    const size_t pair_recs = size_t(W / cfg->block_size) * (H / cfg->block_size);
+    // a lone baseline sequence shards by frame pairs (pairs are independent
+    // for ES/TSS/FSS/DS; PA pairs chain through the temporal candidate)
+    const bool by_pair = n_seq == 1 && cfg->algo != ME_ALGO_PA && pairs > 1;
+    const int units = by_pair ? pairs : n_seq;
+    const int ng = std::min(n_gpus, units);
+    std::vector<me_status> rc(ng, ME_OK);
+    std::vector<std::string> msg(ng);
+    auto work = [&](int g) {
+        const int u0 = int(int64_t(units) * g / ng), u1 = int(int64_t(units) * (g + 1) / ng);
+        me_ctx* c = nullptr;
+        me_status r = me_b200_ctx_create(g, &c);
+        if (!r) {
+            if (by_pair)  // pairs [u0, u1) = frames [u0, u1 + d)
+                r = me_b200_run_sequences(c, cfg, 1, (u1 - u0) + cfg->ref_distance, W, H, luma + plane * u0,
+                                          alpha ? alpha + plane * u0 : nullptr, recs + pair_recs * u0,
+                                          stats + u0, nullptr);
+            else
+                r = me_b200_run_sequences(c, cfg, u1 - u0, n_frames, W, H, luma + seq_bytes * u0,
+                                          alpha ? alpha + seq_bytes * u0 : nullptr,
+                                          recs + pair_recs * pairs * u0, stats + size_t(pairs) * u0, nullptr);
+        }
+        if (r) msg[g] = g_last_error;
+        rc[g] = r;
+        if (c) me_b200_ctx_destroy(c);
+    };
+    std::vector<std::thread> pool;
+    for (int g = 1; g < ng; ++g) pool.emplace_back(work, g);
+    work(0);
+    for (auto& t : pool) t.join();
+    for (int g = 0; g < ng; ++g)
+        if (rc[g]) return me_fail(rc[g], "device " + std::to_string(g) + ": " + msg[g]);
+    return ok();
+}
+
 me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
                                 int H, const uint8_t* luma, const uint8_t* alpha,
                                 me_block_rec* recs, me_pair_stats* stats, uint8_t* pred) {
@@ -625,6 +711,7 @@ me_status me_b200_block_search(me_ctx* ctx, int algo, int W, int H, const uint8_
     if (algo < ME_ALGO_ES || algo > ME_ALGO_DS)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "not a block search");
     if (range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (range > kMaxSearchRange) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range above 255 is not supported by the B200 path");
     if (size != 8 && size != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
     if ((s = check_rect(W, H, x0, y0, size))) return s;
     if (!cur || !ref || !out_mv) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
@@ -653,6 +740,7 @@ me_status me_b200_brs_select(me_ctx* ctx, int W, int H, const uint8_t* cur, cons
     if (s) return s;
     // cfg.validate(); require_inside; type checks (estimators.cpp:261-268)
     if (range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (range > kMaxSearchRange) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range above 255 is not supported by the B200 path");
     if (size != 8 && size != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
     if ((s = check_rect(W, H, x0, y0, size))) return s;
     if (btype == ME_TRANSPARENT)
@@ -689,6 +777,7 @@ me_status me_b200_prs_refine(me_ctx* ctx, int W, int H, const uint8_t* cur, cons
     me_status s = check_ctx(ctx);
     if (s) return s;
     if (range < 1) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range must be >= 1");
+    if (range > kMaxSearchRange) return me_fail(ME_ERR_INVALID_ARGUMENT, "search_range above 255 is not supported by the B200 path");
     if (size != 8 && size != 16) return me_fail(ME_ERR_INVALID_ARGUMENT, "block_size must be 8 or 16");
     if (!(epsilon > 0.0)) return me_fail(ME_ERR_INVALID_ARGUMENT, "epsilon must be > 0");
     if (!(theta > 0.0)) return me_fail(ME_ERR_INVALID_ARGUMENT, "theta must be > 0");

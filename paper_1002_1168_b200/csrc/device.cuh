@@ -248,7 +248,7 @@ __device__ __forceinline__ void write_rec(me_block_rec* r, int dx, int dy, uint3
                                           uint32_t type, bool release) {
     uint32_t* w = reinterpret_cast<uint32_t*>(r);
     w[1] = cost_q4;
-    w[2] = (cmp & 0xFFFF) | (dpd << 16);
+    w[2] = min(cmp, 0xFFFFu) | (dpd << 16);  // comparisons saturate (ES at S >= 128: (2S+1)^2 > 65535)
     w[3] = (iters & 0xFF) | ((type & 0xFF) << 8);
     if (release)
         st_relaxed(w, pack_mv(dx, dy));

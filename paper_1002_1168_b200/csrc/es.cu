@@ -136,7 +136,8 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
                 }
             }
             // min over the run's K positions of (SAD, |dx|+|dy|, k) in 32 bits
-            // (SAD < 2^16, |dx|+|dy| <= 128, k < 8), then one 64-bit key
+            // (SAD < 2^16, |dx|+|dy| <= 2S < 512 for S <= 255, k < 8), then one
+            // 64-bit key
             const int dx = lo_x + col;
             const int ady = (run0 + run) * K;
             const int adx = abs(dx);
@@ -145,13 +146,13 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
             for (int k = 0; k < K; ++k) {
                 const int wy = ady + k;  // window row index
                 const uint32_t man = uint32_t(adx + abs(lo_y + wy));
-                const uint32_t kk = (acc[k] << 11) | (man << 3) | uint32_t(k);
+                const uint32_t kk = (acc[k] << 12) | (man << 3) | uint32_t(k);
                 m32 = wy < WY ? min(m32, kk) : m32;
             }
             if (m32 != ~0u) {
                 const uint32_t wy = uint32_t(ady) + (m32 & 7u);
-                const unsigned long long key = (static_cast<unsigned long long>(m32 >> 11) << 40) |
-                                               (static_cast<unsigned long long>((m32 >> 3) & 0xFFu) << 24) |
+                const unsigned long long key = (static_cast<unsigned long long>(m32 >> 12) << 40) |
+                                               (static_cast<unsigned long long>((m32 >> 3) & 0x1FFu) << 24) |
                                                static_cast<unsigned long long>(wy * uint32_t(WX) + uint32_t(col));
                 best = key < best ? key : best;
             }

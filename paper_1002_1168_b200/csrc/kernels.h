@@ -16,6 +16,11 @@ struct Batch {
     const uint8_t* luma;   // [n_seq][F][H][W]
     const uint8_t* alpha;  // same shape, or null (all opaque)
     int n_seq, F, W, H, d, pairs, bs, cols, rows;
+    // block-row band [v0, v1) of the baselines' row sharding (v1 < 0: every
+    // row): blocks outside it are not estimated, their records are left
+    // untouched and they add nothing to the pair's stats
+    int v0 = 0, v1 = -1;
+    __host__ __device__ bool in_band(int v) const { return v >= v0 && (v1 < 0 || v < v1); }
     __host__ __device__ int64_t nblocks() const { return int64_t(n_seq) * pairs * rows * cols; }
     __host__ __device__ int steps() const { return (cols - 1) + 2 * (rows - 1) + (pairs - 1) + 1; }
 };

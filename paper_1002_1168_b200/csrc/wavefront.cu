@@ -76,6 +76,13 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             gp = t / b.rows;  // seq * pairs + p
             const int p = int(gp % b.pairs);
             const int seq = int(gp / b.pairs);
+            if (!b.in_band(v)) {  // outside the row band: not this call's work
+#pragma unroll
+                for (int k = 0; k < NB; ++k) a.types[(gp * b.rows + v) * b.cols + hs * NB + k] = uint8_t(ME_TRANSPARENT);
+                gp = -1;
+                goto next;
+            }
+            {
             const size_t fcur = size_t(seq) * b.F + p + b.d, fref = size_t(seq) * b.F + p;
             const size_t off = size_t(v * BS) * b.W + size_t(hs) * 16;
             const uint8_t* ac = b.alpha ? b.alpha + fcur * plane + off : nullptr;
@@ -135,7 +142,9 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
                     n_t += 1;
                 }
             }
+            }
         }
+    next:
         if (a.stats) {
             const int64_t gp0 = __shfl_sync(0xFFFFFFFFu, gp, 0);
             const bool uniform = __all_sync(0xFFFFFFFFu, gp == gp0 || gp < 0);

@@ -79,15 +79,17 @@ class FieldGatherer:
     """Per-step gather of the MV fields into rank `dst`, overlapped with the
     next step: step k's packed field is gathered asynchronously (NCCL runs it
     on its own stream after step k's kernels) while step k+1 computes; two
-    send buffers alternate, and a buffer is refilled only after its previous
-    gather completed (`Work.wait`, a stream dependency under NCCL).  `finish`
-    waits for the last gather; the received fields of the latest completed
-    step are in `fields` on rank `dst`."""
+    send buffers alternate (a buffer is refilled only after its previous
+    gather completed, `Work.wait`, a stream dependency under NCCL), and the
+    receive buffers rotate through three sets, so `fields` — the latest
+    COMPLETED step's fields on rank `dst` — is never the target of a gather in
+    flight.  `finish` waits for the last gather."""
 
     def __init__(self, search_range: int, dst: int = 0, group=None):
         self.S, self.dst, self.group = search_range, dst, group
         self.bufs = [None, None]
-        self.outs = [None, None]
+        self.outs = [None, None, None]
+        self.slot = [0, 0]
         self.work = [None, None]
         self.k = 0
         self.fields = None
@@ -99,14 +101,18 @@ class FieldGatherer:
         i = self.k & 1
         if self.work[i] is not None:
             self.work[i].wait()
-            self.fields = self.outs[i]
+            self.fields = self.outs[self.slot[i]]
         packed = pack_mv(recs, self.S)
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
         if self.bufs[i] is None or self.bufs[i].shape != packed.shape or self.bufs[i].dtype != packed.dtype:
             self.bufs[i] = torch.empty_like(packed)
-            rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
-            self.outs[i] = [torch.empty_like(packed) for _ in range(world)] if rank == self.dst else None
+            self.outs = [None, None, None]
+        j = self.k % 3
+        if rank == self.dst and self.outs[j] is None:
+            self.outs[j] = [torch.empty_like(packed) for _ in range(world)]
         self.bufs[i].copy_(packed)
-        self.work[i] = dist.gather(self.bufs[i], self.outs[i], dst=self.dst, group=self.group, async_op=True)
+        self.slot[i] = j
+        self.work[i] = dist.gather(self.bufs[i], self.outs[j] if rank == self.dst else None, dst=self.dst, group=self.group, async_op=True)
         self.k += 1
 
     def finish(self):
@@ -115,9 +121,91 @@ class FieldGatherer:
         for j in (self.k & 1, (self.k + 1) & 1):  # older first
             if self.work[j] is not None:
                 self.work[j].wait()
-                self.fields = self.outs[j]
+                self.fields = self.outs[self.slot[j]]
                 self.work[j] = None
         return self.fields
+
+
+class ResultGatherer:
+    """Per-step gather of every rank's results into rank `dst`, overlapped with
+    the next step ("int64 SSE gathered with the records"): the
+    packed MV field (`pack_mv`) and the per-pair SearchStats + SSE (48 bytes
+    per pair) of a rank's `counts[rank]` sequences go in ONE uint8 buffer,
+    padded to the largest shard (a gather needs equal sizes), gathered
+    asynchronously on the collective's stream while the next step computes.
+    Send buffers alternate (a buffer is refilled only after its previous gather
+    completed) and the received buffers rotate through three sets, so the
+    result of the latest completed step stays valid until two more steps have
+    been submitted."""
+
+    def __init__(self, search_range: int, counts: List[int], dst: int = 0, group=None):
+        self.S, self.counts, self.dst, self.group = search_range, list(counts), dst, group
+        self.nmax = max(self.counts)
+        self.send = [None, None]
+        self.recv = [None, None, None]
+        self.work = [None, None]
+        self.slot = [0, 0]  # recv set used by the gather in flight from send buffer i
+        self.k = 0
+        self.done_slot = None
+        self.layout = None
+
+    def _pack(self, recs, stats):
+        import torch
+
+        mv = pack_mv(recs, self.S)
+        n = recs.shape[0]
+        mvb = mv.reshape(n, -1).view(torch.uint8) if mv.dtype == torch.int8 else mv.reshape(n, -1).contiguous().view(torch.uint8)
+        stb = stats.reshape(n, -1)
+        if self.layout is None:
+            self.layout = (mv.dtype, tuple(mv.shape[1:]), mvb.shape[1], stb.shape[1], tuple(stats.shape[1:]))
+        return mvb, stb
+
+    def submit(self, recs, stats):
+        import torch
+        import torch.distributed as dist
+
+        i = self.k & 1
+        if self.work[i] is not None:
+            self.work[i].wait()
+            self.done_slot = self.slot[i]
+        mvb, stb = self._pack(recs, stats)
+        per = mvb.shape[1] + stb.shape[1]
+        if self.send[i] is None:
+            self.send[i] = torch.zeros((self.nmax, per), dtype=torch.uint8, device=recs.device)
+        n = recs.shape[0]
+        self.send[i][:n, : mvb.shape[1]].copy_(mvb)
+        self.send[i][:n, mvb.shape[1]:].copy_(stb)
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        j = self.k % 3
+        if rank == self.dst and self.recv[j] is None:
+            self.recv[j] = [torch.empty_like(self.send[i]) for _ in range(world)]
+        self.slot[i] = j
+        self.work[i] = dist.gather(self.send[i], self.recv[j] if rank == self.dst else None, dst=self.dst, group=self.group, async_op=True)
+        self.k += 1
+
+    def finish(self):
+        """Waits for every outstanding gather; on rank dst returns the last
+        completed step's (mv [n_total, pairs, rows, cols, 2] int32,
+        stats [n_total, pairs, 48] uint8) in rank order, else None."""
+        import torch
+        import torch.distributed as dist
+
+        for j in (self.k & 1, (self.k + 1) & 1):  # older first
+            if self.work[j] is not None:
+                self.work[j].wait()
+                self.done_slot = self.slot[j]
+                self.work[j] = None
+        if dist.get_rank(self.group) != self.dst or self.done_slot is None:
+            return None
+        dtype, mvshape, mvbytes, stbytes, stshape = self.layout
+        mvs, sts = [], []
+        for r, buf in enumerate(self.recv[self.done_slot]):
+            n = self.counts[r]
+            m = buf[:n, :mvbytes]
+            m = m.view(torch.int8) if dtype == torch.int8 else m.contiguous().view(torch.int32)
+            mvs.append(unpack_mv(m.reshape((n,) + mvshape)))
+            sts.append(buf[:n, mvbytes: mvbytes + stbytes].reshape((n,) + stshape))
+        return torch.cat(mvs), torch.cat(sts)
 
 
 def max_over_ranks(value: float, device=None) -> float:
