@@ -520,42 +520,6 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
 # ES on config 5 (the INT-pipe headline), sharded by (pair, row band) units
 
 
-def es_units(alpha_dev, bs, pairs, d, n_bands):
-    """Estimated-block count of every (band, pair) unit, band-major."""
-    import torch
-
-    F, H, W = alpha_dev.shape
-    rows, cols = H // bs, W // bs
-    cur = alpha_dev[d:d + pairs].view(pairs, rows, bs, cols, bs)
-    est = (cur.amax(dim=(2, 4)) > 0).to(torch.int64)  # classify_block: any sample set -> not transparent
-    per_row = est.sum(dim=2).cpu().numpy()  # [pairs, rows]
-    edges = np.linspace(0, rows, n_bands + 1).round().astype(int)
-    units = []
-    for b in range(n_bands):
-        for p in range(pairs):
-            units.append((b, p, int(edges[b]), int(edges[b + 1]), int(per_row[p, edges[b]:edges[b + 1]].sum())))
-    return units
-
-
-def split_units(units, world):
-    """Contiguous (band-major) split balanced by estimated-block count."""
-    cost = np.array([u[4] + 1 for u in units], dtype=np.float64)
-    cum = np.concatenate([[0], np.cumsum(cost)])
-    cuts = [0] + [int(np.searchsorted(cum, cum[-1] * r / world)) for r in range(1, world)] + [len(units)]
-    return [units[cuts[r]:cuts[r + 1]] for r in range(world)]
-
-
-def runs_of(my_units):
-    """Groups a rank's units into calls: same band, consecutive pairs."""
-    runs = []
-    for b, p, r0, r1, _ in my_units:
-        if runs and runs[-1][0] == b and runs[-1][2] == p:
-            runs[-1][2] = p + 1
-        else:
-            runs.append([b, p, p + 1, r0, r1])
-    return runs
-
-
 def bench_es_cfg5(args, world, rank, local, dev):
     import torch
     import torch.distributed as dist
@@ -576,9 +540,9 @@ def bench_es_cfg5(args, world, rank, local, dev):
     rows, cols = H // bs, W // bs
     cfg = me_config(algo, bs, S)
     n_bands = 1 if world == 1 else 4
-    units = es_units(alpha[0], bs, pairs, d, n_bands)
-    mine = split_units(units, world)[rank]
-    runs = runs_of(mine)
+    units = mdist.band_units(alpha[0], bs, pairs, d, n_bands)
+    mine = mdist.split_units(units, world)[rank]
+    runs = mdist.unit_runs(mine)
     recs = torch.zeros((1, pairs, rows, cols, 16), dtype=torch.uint8, device=dev)
     stats_acc = torch.zeros((pairs, 6), dtype=torch.int64, device=dev)
     tmp_stats = torch.empty((1, pairs, 48), dtype=torch.uint8, device=dev)
@@ -644,7 +608,7 @@ def bench_es_cfg5(args, world, rank, local, dev):
     # whole-sequence results on rank 0
     if world > 1:
         owner = {}
-        for r, us in enumerate(split_units(units, world)):
+        for r, us in enumerate(mdist.split_units(units, world)):
             for b, p, r0, r1, _ in us:
                 owner[(p, b)] = (r, r0, r1)
         mv = torch.zeros((pairs, rows, cols), dtype=torch.int32, device=dev)
@@ -693,7 +657,7 @@ def bench_es_cfg5(args, world, rank, local, dev):
                      "note": "achieved = oracle-exact comparisons x 256 byte-ops / search-stage time (CUDA events)"},
         "clocks": clk, "parity": parity,
         "cpu_baseline": {"value": v_cpu, "unit": "MB/s", "cores": threads, "kind": kind, "sample": sample, "seconds": dt},
-        "units": {"n": len(units), "bands": n_bands, "per_rank": [len(u) for u in split_units(units, world)]},
+        "units": {"n": len(units), "bands": n_bands, "per_rank": [len(u) for u in mdist.split_units(units, world)]},
     }
 
 

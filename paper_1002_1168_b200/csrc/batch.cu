@@ -112,7 +112,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     Scratch s = carve(b, nbins, scratch);
     cudaError_t e;
     if ((e = cudaMemsetAsync(s.hist, 0, size_t(nbins) * 4, st))) return e;
-    if ((e = cudaMemsetAsync(s.counter, 0, 4, st))) return e;
+    if ((e = cudaMemsetAsync(s.counter, 0, 16, st))) return e;  // ES ticket + the PA launches' claim counters
     if (stats && (e = cudaMemsetAsync(stats, 0, sizeof(me_pair_stats) * size_t(b.n_seq) * b.pairs, st)))
         return e;
 
@@ -147,7 +147,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     if (algo == ME_ALGO_ES)
         e = launch_es(b, cfg.search_range, s.list, nlist, s.counter, recs, stats, num_sms, st);
     else if (algo == ME_ALGO_PA)
-        e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st);
+        e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st, s.counter + 1);
     else
         e = launch_ring(b, algo, cfg.search_range, s.list, nlist, recs, stats, num_sms, st);
     if (e) return e;

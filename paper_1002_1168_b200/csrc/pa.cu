@@ -266,6 +266,7 @@ struct PaArgs {
     int poll_ns;           // dependency poll interval
     int pdl;               // hybrid launches chained by programmatic dependent launch (see PdlScope)
     const int* range;      // [begin, end) of the list for this launch (device) or null: [0, *nlist)
+    int* claim;            // zeroed claim counter of this launch (in-order dynamic claiming) or null
     unsigned long long* trace;  // debug: per entry {claimed, deps ready, done, smid} (ns)
 };
 
@@ -513,6 +514,53 @@ __device__ bool pa_patch_block(const PaParams& P, const PaBlock& B, int lane, bo
     return true;
 }
 
+// In-order work claiming, CTA by CTA.  With `claim` (a zeroed counter per
+// launch), a CTA takes BATCHES of nwarps x STEP consecutive list entries with
+// one global atomicAdd, and warp w of the CTA works on entries w*STEP ..
+// w*STEP+STEP-1 of each batch, batch after batch — the same locality as the
+// static round-robin (a CTA's warps hold consecutive entries, which share
+// reference rows in L1), but batches are handed out in list order to
+// whichever CTAs are running.  Every dependency of an entry lies earlier in
+// the list, so the smallest unfinished entry is always held by a running warp
+// (its warp finished every earlier batch of its CTA): the grid makes progress
+// whatever subset of its CTAs is resident — a concurrent kernel may hold part
+// of the device.  Without `claim`: static round-robin over the whole grid,
+// which needs every CTA resident.
+constexpr int kClaimRing = 4;  // batch bases in flight per CTA
+struct CtaClaim {
+    int* sh;  // [0] batches published, [1] claims started, [2, 2+R) bases, [2+R, 2+2R) reads
+    int* gctr;
+    int k;    // this warp's next batch
+    __device__ static void init(int* sh) {
+        if (threadIdx.x < 2 + 2 * kClaimRing) sh[threadIdx.x] = 0;
+        __syncthreads();
+    }
+    template <int STEP>
+    __device__ int next(int lane, int wid, int nw) {
+        const int slot = k % kClaimRing;
+        int base = 0;
+        if (lane == 0) {
+            volatile int* v = sh;
+            while (v[0] <= k) {
+                if (atomicCAS(&sh[1], k, k + 1) == k) {  // this warp claims batch k for the CTA
+                    if (k >= kClaimRing)                 // every warp has read batch k - R's base
+                        while (v[2 + kClaimRing + slot] < nw) __nanosleep(20);
+                    v[2 + kClaimRing + slot] = 0;
+                    v[2 + slot] = atomicAdd(gctr, STEP * nw);
+                    __threadfence_block();
+                    v[0] = k + 1;
+                } else {
+                    __nanosleep(20);
+                }
+            }
+            base = v[2 + slot];
+            atomicAdd(&sh[2 + kClaimRing + slot], 1);
+        }
+        ++k;
+        return __shfl_sync(0xFFFFFFFFu, base, 0) + STEP * wid;
+    }
+};
+
 template <int BS>
 __global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
     extern __shared__ uint32_t s_pa[];
@@ -528,7 +576,14 @@ __global__ void __launch_bounds__(256, BS == 8 ? 3 : 2) pa_kernel(PaArgs a) {
     // increasing order and the grid is sized so every warp is resident, so
     // the smallest unfinished entry is always being worked on (no deadlock,
     // no grid-wide barrier).
-    for (int item = blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+    __shared__ int s_claim[2 + 2 * kClaimRing];
+    CtaClaim cc{s_claim, a.claim, 0};
+    CtaClaim::init(s_claim);
+    int nxt = 0;
+    for (int rel = a.claim ? cc.next<1>(lane, wid, blockDim.x >> 5) : blockIdx.x * (blockDim.x >> 5) + wid; rel < n;
+         rel = a.claim ? cc.next<1>(lane, wid, blockDim.x >> 5) : nxt) {
+        nxt = a.claim ? 0 : rel + nwarps;
+        const int item = rel;
         const uint2 e = a.list[item];
         if (e.x == kInvalidEntry) continue;
         int h, v, p, seq;
@@ -629,7 +684,14 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     const int k = lane >> 2, q = lane & 3;   // PRS: neighbour k, rows q and q + 4
     const int kx = off8x(k), ky = off8y(k);
     // static round-robin over the wavefront-sorted list (see pa_kernel)
-    for (int item = beg + blockIdx.x * (blockDim.x >> 5) + wid; item < n; item += nwarps) {
+    __shared__ int s_claim[2 + 2 * kClaimRing];
+    CtaClaim cc{s_claim, a.claim, 0};
+    CtaClaim::init(s_claim);
+    int nxt = 0;
+    for (int rel = a.claim ? cc.next<1>(lane, wid, blockDim.x >> 5) : blockIdx.x * (blockDim.x >> 5) + wid; beg + rel < n;
+         rel = a.claim ? cc.next<1>(lane, wid, blockDim.x >> 5) : nxt) {
+        nxt = a.claim ? 0 : rel + nwarps;
+        const int item = beg + rel;
         const uint2 e = __ldg(a.list + item);
         if (e.x == kInvalidEntry) continue;
         unsigned long long t_claim = 0, t_ready = 0;
@@ -894,7 +956,14 @@ __global__ void __launch_bounds__(THREADS, MINB) pa_duo_kernel(const PaArgs a) {
     const int c = hl >> 2, q4 = hl & 3;  // BRS: candidate c, block rows q4 and q4 + 4
     const int k = hl >> 1, q2 = hl & 1;  // PRS: neighbour k, block rows q2 + {0, 2, 4, 6}
     const int kx = off8x(k), ky = off8y(k);
-    for (int item = beg + 2 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 2 * nwarps) {
+    __shared__ int s_claim[2 + 2 * kClaimRing];
+    CtaClaim cc{s_claim, a.claim, 0};
+    CtaClaim::init(s_claim);
+    int nxt = 0;
+    for (int rel = a.claim ? cc.next<2>(lane, wid, blockDim.x >> 5) : 2 * (blockIdx.x * (blockDim.x >> 5) + wid); beg + rel < n;
+         rel = a.claim ? cc.next<2>(lane, wid, blockDim.x >> 5) : nxt) {
+        nxt = a.claim ? 0 : rel + 2 * nwarps;
+        const int item = beg + rel;
         const uint2 e = __ldg(a.list + item + hf);
         const bool act = e.x != kInvalidEntry;  // uniform per half
         unsigned long long t_claim = 0, t_ready = 0;
@@ -1186,7 +1255,14 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
     const uint32_t plane = uint32_t(W) * uint32_t(H);
     const int c = gl >> 1, hh = gl & 1;      // BRS: candidate c, block rows 4 hh .. 4 hh + 3
     const int kx = off8x(gl), ky = off8y(gl);  // PRS: neighbour gl
-    for (int item = beg + 4 * (blockIdx.x * (blockDim.x >> 5) + wid); item < n; item += 4 * nwarps) {
+    __shared__ int s_claim[2 + 2 * kClaimRing];
+    CtaClaim cc{s_claim, a.claim, 0};
+    CtaClaim::init(s_claim);
+    int nxt = 0;
+    for (int rel = a.claim ? cc.next<4>(lane, wid, blockDim.x >> 5) : 4 * (blockIdx.x * (blockDim.x >> 5) + wid); beg + rel < n;
+         rel = a.claim ? cc.next<4>(lane, wid, blockDim.x >> 5) : nxt) {
+        nxt = a.claim ? 0 : rel + 4 * nwarps;
+        const int item = beg + rel;
         const uint2 e = __ldg(a.list + item + grp);
         const bool act = e.x != kInvalidEntry;  // uniform per group
         unsigned long long t_claim = 0, t_ready = 0;
@@ -1893,7 +1969,7 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
 
 cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0, const uint2* list,
                       const int* nlist, const int* ranges, int pa_mode, me_block_rec* recs,
-                      me_pair_stats* stats, int num_sms, cudaStream_t st) {
+                      me_pair_stats* stats, int num_sms, cudaStream_t st, int* claims) {
     cudaError_t e;
     PaArgs pa_args;
     pa_args.b = b;
@@ -1908,6 +1984,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     pa_args.poll_ns = getenv("ME_PA_POLL_NS") ? atoi(getenv("ME_PA_POLL_NS")) : 64;
     pa_args.pdl = 0;
     pa_args.trace = nullptr;
+    pa_args.claim = nullptr;
     const char* trace_path = getenv("ME_PA_TRACE");
     int n_host = 0;
     if (trace_path) {
@@ -1922,10 +1999,14 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     // ME_PA_PDL=0 launches the hybrid's grids in plain stream order
     const bool pdl = pa_mode == 4 && !trace_path && !(getenv("ME_PA_PDL") && atoi(getenv("ME_PA_PDL")) == 0);
     // persistent grids: every warp of a launch must be co-resident (dependency spinning)
+    const bool dyn = !(getenv("ME_PA_CLAIM") && atoi(getenv("ME_PA_CLAIM")) == 0);
+    int n_launch = 0;
     auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range, bool chained = false,
                       bool after_sort = false) -> cudaError_t {
         PaArgs la = pa_args;
         la.range = range;
+        la.claim = dyn && claims ? claims + n_launch : nullptr;  // one zeroed counter per launch
+        ++n_launch;
         la.pdl = pdl ? (after_sort ? 2 : 1) : 0;
         la.warp_words = std::max(la.P.bm_words, warp_words);
         const size_t smem = size_t(threads / 32) * la.warp_words * 4;

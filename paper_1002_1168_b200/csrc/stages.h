@@ -55,9 +55,10 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
                    int num_sms);
 cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
                            me_block_rec* recs, me_pair_stats* stats, cudaStream_t st);
+// claims: 3 zeroed counters (in-order dynamic claiming, one per launch) or null
 cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0, const uint2* list,
                       const int* nlist, const int* ranges, int pa_mode, me_block_rec* recs,
-                      me_pair_stats* stats, int num_sms, cudaStream_t st);
+                      me_pair_stats* stats, int num_sms, cudaStream_t st, int* claims);
 
 // frame_ops.cu: the prediction pass of a batch (only when asked for)
 cudaError_t launch_mc_pred(const Batch& b, const me_block_rec* recs, uint8_t* pred, cudaStream_t st);

@@ -208,6 +208,51 @@ class ResultGatherer:
         return torch.cat(mvs), torch.cat(sts)
 
 
+def band_units(alpha, bs: int, pairs: int, d: int, n_bands: int):
+    """The baselines' sharding units: (band, pair) with the block
+    rows split into n_bands bands, each with its estimated-block count (the
+    work a unit costs: transparent blocks are skipped, estimators.cpp:418).
+    `alpha` is one sequence's [F, H, W] uint8 tensor (any device); a block is
+    estimated unless its CURRENT alpha (frame p + d) is all zero
+    (classify_block, frame.cpp:81-104).  Returns [(band, pair, row0, row1,
+    estimated)] band-major."""
+    import numpy as np
+    import torch
+
+    F, H, W = alpha.shape
+    rows, cols = H // bs, W // bs
+    cur = alpha[d:d + pairs].reshape(pairs, rows, bs, cols, bs)
+    est = (cur.amax(dim=(2, 4)) > 0).to(torch.int64)
+    per_row = est.sum(dim=2).cpu().numpy()  # [pairs, rows]
+    edges = np.linspace(0, rows, n_bands + 1).round().astype(int)
+    return [(b, p, int(edges[b]), int(edges[b + 1]), int(per_row[p, edges[b]:edges[b + 1]].sum()))
+            for b in range(n_bands) for p in range(pairs)]
+
+
+def split_units(units, world: int):
+    """Contiguous split of the (band-major) units over `world` ranks, balanced
+    by estimated-block count (+1 per unit for its fixed cost)."""
+    import numpy as np
+
+    cost = np.array([u[4] + 1 for u in units], dtype=np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    cuts = [0] + [int(np.searchsorted(cum, cum[-1] * r / world)) for r in range(1, world)] + [len(units)]
+    return [units[cuts[r]:cuts[r + 1]] for r in range(world)]
+
+
+def unit_runs(units):
+    """A rank's units grouped into calls: [band, first pair, end pair, row0,
+    row1] for runs of consecutive pairs of one band (one me_b200_run_band_dev
+    call each: the pairs are a frame sub-range of the sequence)."""
+    runs = []
+    for b, p, r0, r1, _ in units:
+        if runs and runs[-1][0] == b and runs[-1][2] == p:
+            runs[-1][2] = p + 1
+        else:
+            runs.append([b, p, p + 1, r0, r1])
+    return runs
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a scalar over all ranks (timings: the slowest rank defines the job)."""
     import torch

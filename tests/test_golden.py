@@ -17,6 +17,9 @@ from backends import GpuBackend, PortBackend
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SEQ_FILES = sorted(glob.glob(os.path.join(GOLD, "seq_*.npz")))
+# configs 3 and 5 at their real geometry and search range (S = 32 / 64):
+# checked on the GPU only (tools/make_golden.py BIG_CASES)
+BIG_FILES = sorted(glob.glob(os.path.join(GOLD, "big_*.npz")))
 REC = np.dtype([("dx", "<i2"), ("dy", "<i2"), ("cost_q4", "<u4"), ("comparisons", "<u2"), ("dpd_steps", "<u2"), ("iterations", "u1"), ("type", "u1"), ("reserved", "<u2")])
 STAT = np.dtype([(n, "<i8") for n in ("block_comparisons", "dpd_refinement_steps", "blocks_opaque", "blocks_boundary", "blocks_transparent", "sse")])
 
@@ -50,6 +53,21 @@ def load_seq(path):
 def test_sequence_golden(kind, path):
     luma, alpha, c, z = load_seq(path)
     recs, stats = backend(kind).run_sequence(c["algo"], luma, alpha, c["bs"], c["S"], halfpel=c["halfpel"], ref_distance=c["ref_distance"])
+    want_r = z["recs"].view(REC).reshape(recs.shape)
+    want_s = z["stats"].view(STAT).reshape(stats.shape)
+    bad = np.argwhere(recs != want_r)
+    assert bad.size == 0, f"{len(bad)} record mismatches, first {tuple(bad[0])}: got {recs[tuple(bad[0])]} want {want_r[tuple(bad[0])]}"
+    assert np.array_equal(stats, want_s)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", BIG_FILES, ids=lambda p: os.path.basename(p)[4:-4])
+def test_big_golden_gpu(path):
+    """1920x1088 (S = 32) and 3840x2160 (S = 64) sequences: the CUDA path's
+    records and stats equal the reference's bit for bit (the S = 32 / 64
+    es_kernel instantiations, the ring searches and PA at those ranges)."""
+    luma, alpha, c, z = load_seq(path)
+    recs, stats = backend("gpu").run_sequence(c["algo"], luma, alpha, c["bs"], c["S"])
     want_r = z["recs"].view(REC).reshape(recs.shape)
     want_s = z["stats"].view(STAT).reshape(stats.shape)
     bad = np.argwhere(recs != want_r)

@@ -442,3 +442,106 @@ def test_pa_config_variants(me_gpu, port, bs, hp, bt, it, step, eps, theta):
                             max_iterations=it, step=step, epsilon=eps, theta=theta), luma, alpha)
         assert_recs(recs[0], want_r, f"cfg{cfg_id} bs{bs} hp{hp} bt{bt} it{it} step{step} eps{eps} theta{theta}")
         assert np.array_equal(stats[0], want_s)
+
+
+# ---------------------------------------------------------------------------
+# Sharding entry points and concurrency
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2, 3])
+def test_row_bands_sum_to_the_whole(me_gpu, port, algo):
+    """me_b200_run_band_dev: the row bands of a batch reproduce the whole
+    batch's records, and their stats (SearchStats + SSE) add up to it."""
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config_sequence(2, 61, 6)
+    lt = torch.from_numpy(luma[None].copy()).cuda()
+    at = torch.from_numpy(alpha[None].copy()).cuda()
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=16, block_size=16))
+    full_r, full_s = B.run_sequences_dev(cfg, lt, at)
+    pairs, rows = 4, luma.shape[1] // 16
+    recs = torch.zeros_like(full_r)
+    total = torch.zeros((1, pairs, 6), dtype=torch.int64, device="cuda")
+    for r0, r1 in ((0, 5), (5, 6), (6, rows)):
+        st = torch.empty((1, pairs, 48), dtype=torch.uint8, device="cuda")
+        B.run_band_dev(cfg, lt, at, r0, r1, recs, st)
+        total += st.view(torch.int64).view(1, pairs, 6)
+    torch.cuda.synchronize()
+    assert torch.equal(recs, full_r)
+    assert torch.equal(total, full_s.view(torch.int64).view(1, pairs, 6))
+    want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=16), luma, alpha)
+    assert_recs(recs[0].cpu().numpy().view(_lib_rec_dtype()).reshape(want_r.shape), want_r)
+
+
+def test_row_band_rejects_pa_and_bad_bands(me_gpu):
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+
+    lt = torch.zeros((1, 4, 64, 64), dtype=torch.uint8, device="cuda")
+    recs = torch.zeros((1, 2, 8, 8, 16), dtype=torch.uint8, device="cuda")
+    st = torch.zeros((1, 2, 48), dtype=torch.uint8, device="cuda")
+    pa = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=8, block_size=8))
+    with pytest.raises(ValueError):
+        B.run_band_dev(pa, lt, None, 0, 4, recs, st)
+    es = me_gpu.BatchConfig(algo=me_gpu.Algo.ES, search=me_gpu.SearchConfig(search_range=8, block_size=8))
+    for r0, r1 in ((0, 0), (-1, 3), (2, 9)):
+        with pytest.raises(ValueError):
+            B.run_band_dev(es, lt, None, r0, r1, recs, st)
+
+
+@pytest.mark.parametrize("algo,bs", [(4, 8), (0, 16), (3, 16)])
+def test_multi_device_entry(me_gpu, port, algo, bs):
+    """me_b200_run_sequences_multi over the visible devices equals the
+    single-device call (a lone baseline sequence shards by frame pairs)."""
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import synth
+
+    n = me_gpu.device_count()
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=16, block_size=bs))
+    luma, alpha = synth.config4_batch(3, 700, 6) if algo == 4 else [x[None] for x in synth.config_sequence(2, 71, 6)]
+    want = me_gpu.run_sequences(cfg, luma, alpha)
+    got = B.run_sequences_multi(cfg, luma, alpha, n_gpus=n)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    with pytest.raises(ValueError):
+        B.run_sequences_multi(cfg, luma, alpha, n_gpus=n + 1)
+
+
+def test_concurrent_large_batches(me_gpu, port):
+    """Two host threads each run a 64-sequence config-4 batch on one GPU at
+    the same time.  Both select the persistent PA grids (hybrid head / quad
+    middle / tail); with in-order claiming neither depends on its grid being
+    fully resident, so the two grids sharing the device both finish, with
+    results equal to the oracle's."""
+    import threading
+
+    from paper_1002_1168_b200 import synth
+
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    inputs = [synth.config4_batch(64, 1000 + 100 * k, 8) for k in range(2)]
+    out, errs = [None, None], []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                out[k] = me_gpu.run_sequences(cfg, *inputs[k])
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=120)
+        assert not t.is_alive(), "concurrent batches did not finish"
+    assert not errs, errs
+    c = oracle.make_cfg(algo=4, search_range=16, block_size=8)
+    for k in range(2):
+        luma, alpha = inputs[k]
+        for i in (0, 31, 63):
+            want_r, want_s = port.run_sequence(c, luma[i], alpha[i])
+            assert_recs(out[k][0][i], want_r, f"batch {k} seq {i}")
+            assert np.array_equal(out[k][1][i], want_s)
