@@ -118,6 +118,41 @@ void* me_b200_ctx_stream(me_ctx* ctx);
  * (ms) in the order ME_STAGE_* into out[n] (n <= ME_NUM_STAGES). */
 enum { ME_STAGE_CLASSIFY = 0, ME_STAGE_SORT = 1, ME_STAGE_SEARCH = 2, ME_STAGE_MC_PSNR = 3, ME_NUM_STAGES = 4 };
 me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable);
+
+/* Kernel-schedule tuning of a context (defaults = the measured best; the
+ * library reads no environment variables).  Every field's 0 selects the
+ * default.  Results never depend on these: every schedule is bit-exact
+ * (tests/test_gpu_parity.py runs them all). */
+enum {
+    ME_PA_SCHED_AUTO = 0,       /* by wavefront width: hybrid (quad middle) or fast */
+    ME_PA_SCHED_GENERIC = 1,    /* pa_kernel: a warp per block, any configuration */
+    ME_PA_SCHED_FAST = 2,       /* pa_fast_kernel over the whole list */
+    ME_PA_SCHED_DUO = 3,        /* pa_duo_kernel (two blocks per warp) over the whole list */
+    ME_PA_SCHED_DUO_HYBRID = 4, /* fast head/tail, duo middle */
+    ME_PA_SCHED_QUAD_HYBRID = 5 /* fast head/tail, quad middle */
+};
+typedef struct me_tuning {
+    int32_t pa_schedule;      /* ME_PA_SCHED_* */
+    int32_t pa_wide_blocks;   /* hybrid: steps with at least this many blocks are "wide" (0: 40 x SMs) */
+    int32_t pa_fast_ctas;     /* CTAs per SM of pa_fast_kernel, 1..6 (0: by wavefront width) */
+    int32_t pa_quad_ctas;     /* CTAs per SM of pa_quad_kernel, 2..4 (0: 3) */
+    int32_t pa_duo_threads;   /* 128 or 256 (0: 256) */
+    int32_t pa_duo_ctas;      /* CTAs per SM of pa_duo_kernel (0: 4 at 256 threads, 7 at 128) */
+    int32_t pa_poll_ns;       /* dependency poll back-off in ns (0: 64) */
+    int32_t pa_static_claim;  /* 1: static round-robin work split (needs the whole grid resident);
+                                 0: in-order CTA-batch claiming */
+    int32_t pa_no_pdl;        /* 1: launch the hybrid's grids in plain stream order */
+    int32_t pa_no_smem_pair;  /* 1: never use the one-CTA shared-memory kernel for a small pair */
+    int32_t pa_key_a, pa_key_s; /* wavefront sort key a * (h + 2v + p) + s * seq (0: 1 and 0) */
+    int32_t sort_no_pdl;      /* 1: scan and fill in plain stream order */
+    int32_t fill_rows;        /* 1: a thread per block row, -1: a thread per block (0: by size) */
+    int32_t fill_rows_per_cta;/* block rows per fill CTA (0: 64) */
+    int32_t h2d_chunks;       /* host-buffer path: pipeline chunks, 1..32 (0: 16) */
+    int32_t mask_pack;        /* host path alpha transfer: 1 bytes, 2 dense bits, 0/3 sparse bits */
+    const char* pa_trace_path;/* debug: per-block PA trace written here (NULL: off) */
+} me_tuning;
+me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* tuning);
+me_status me_b200_ctx_get_tuning(me_ctx* ctx, me_tuning* out);
 me_status me_b200_ctx_stage_ms(me_ctx* ctx, float* out, int n);
 
 /* Bytes the last me_b200_run_sequences call moved host->device and

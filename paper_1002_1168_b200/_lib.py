@@ -57,6 +57,18 @@ class MePairStats(C.Structure):
     ]
 
 
+class MeTuning(C.Structure):
+    """me_tuning (include/me_b200.h): kernel-schedule knobs of a context; zeros = defaults."""
+
+    _fields_ = [(n, C.c_int32) for n in (
+        "pa_schedule", "pa_wide_blocks", "pa_fast_ctas", "pa_quad_ctas", "pa_duo_threads", "pa_duo_ctas", "pa_poll_ns",
+        "pa_static_claim", "pa_no_pdl", "pa_no_smem_pair", "pa_key_a", "pa_key_s", "sort_no_pdl", "fill_rows",
+        "fill_rows_per_cta", "h2d_chunks", "mask_pack")] + [("pa_trace_path", C.c_char_p)]
+
+
+PA_SCHEDULES = {"auto": 0, "warp": 1, "generic": 1, "fast": 2, "duo": 3, "duo-hybrid": 4, "hybrid": 5, "quad": 5}
+
+
 class MeSynthParams(C.Structure):
     _fields_ = [
         ("width", C.c_int32),
@@ -149,6 +161,8 @@ SIGNATURES = {
     "me_b200_predict_frame": (I, [P, I, I, P, P, P, I, P, P, I64P]),
     "me_b200_sse": (I, [P, I, I, P, P, I64P]),
     "me_b200_probe_int_peak": (I, [P, C.POINTER(C.c_double)]),
+    "me_b200_ctx_set_tuning": (I, [P, C.POINTER(MeTuning)]),
+    "me_b200_ctx_get_tuning": (I, [P, C.POINTER(MeTuning)]),
     "me_b200_synth_preset": (I, [I, C.c_uint64, C.POINTER(MeSynthParams)]),
     "me_b200_synth": (I, [C.POINTER(MeSynthParams), P, P]),
     "me_b200_synth_dev": (I, [P, C.POINTER(MeSynthParams), I, P, P, P]),
@@ -204,3 +218,24 @@ def ctx(device: int = 0):
         check(lib().me_b200_ctx_create(device, C.byref(h)))
         cache[device] = h
     return cache[device]
+
+
+def set_tuning(device: int = 0, **fields):
+    """Sets this thread's context tuning (me_b200_ctx_set_tuning); unnamed
+    fields take their defaults.  `pa_schedule` may be a name (PA_SCHEDULES).
+    Returns the previous tuning (pass it back to restore)."""
+    prev = MeTuning()
+    check(lib().me_b200_ctx_get_tuning(ctx(device), C.byref(prev)))
+    t = MeTuning()
+    for k, v in fields.items():
+        if k == "pa_schedule" and isinstance(v, str):
+            v = PA_SCHEDULES[v]
+        if k == "pa_trace_path" and isinstance(v, str):
+            v = v.encode()
+        setattr(t, k, v)
+    check(lib().me_b200_ctx_set_tuning(ctx(device), C.byref(t)))
+    return prev
+
+
+def restore_tuning(prev, device: int = 0):
+    check(lib().me_b200_ctx_set_tuning(ctx(device), C.byref(prev)))

@@ -55,21 +55,43 @@ struct KeyParams {
     int a, s;
 };
 
-KeyParams pa_key(const Batch& b) {
-    KeyParams k{1, 0};
-    if (const char* e = getenv("ME_PA_KEY_A")) k.a = std::max(1, atoi(e));
-    if (const char* e = getenv("ME_PA_KEY_S")) k.s = std::max(0, atoi(e));
+KeyParams pa_key(const Batch& b, const Tuning& t) {
+    KeyParams k{std::max(1, t.key_a), std::max(0, t.key_s)};
     if (int64_t(k.a) * (b.steps() - 1) + int64_t(k.s) * (b.n_seq - 1) + 1 > 12288) k = KeyParams{1, 0};
     return k;
 }
 
-int pa_bins(const Batch& b) {
-    const KeyParams k = pa_key(b);
+int pa_bins(const Batch& b, const Tuning& t) {
+    const KeyParams k = pa_key(b, t);
     return k.a * (b.steps() - 1) + k.s * (b.n_seq - 1) + 1;
 }
 
-size_t scratch_bytes(const Batch& b, int algo) {
-    const int nbins = algo == ME_ALGO_PA ? pa_bins(b) : 1;
+Tuning resolve_tuning(const me_tuning* u) {
+    Tuning t;
+    if (!u) return t;
+    if (u->pa_schedule) t.pa_schedule = u->pa_schedule;
+    t.pa_wide_blocks = u->pa_wide_blocks;
+    t.pa_fast_ctas = u->pa_fast_ctas;
+    if (u->pa_quad_ctas) t.pa_quad_ctas = u->pa_quad_ctas;
+    if (u->pa_duo_threads) t.pa_duo_threads = u->pa_duo_threads;
+    t.pa_duo_ctas = u->pa_duo_ctas;
+    if (u->pa_poll_ns) t.pa_poll_ns = u->pa_poll_ns;
+    t.pa_claim = !u->pa_static_claim;
+    t.pa_pdl = !u->pa_no_pdl;
+    t.pa_smem_pair = !u->pa_no_smem_pair;
+    if (u->pa_key_a) t.key_a = u->pa_key_a;
+    t.key_s = u->pa_key_s;
+    t.sort_pdl = !u->sort_no_pdl;
+    t.fill_rows = u->fill_rows;
+    if (u->fill_rows_per_cta) t.fill_rows_per_cta = u->fill_rows_per_cta;
+    if (u->h2d_chunks) t.h2d_chunks = u->h2d_chunks;
+    if (u->mask_pack) t.mask_pack = u->mask_pack;
+    t.pa_trace = u->pa_trace_path;
+    return t;
+}
+
+size_t scratch_bytes(const Batch& b, int algo, const Tuning& t) {
+    const int nbins = algo == ME_ALGO_PA ? pa_bins(b, t) : 1;
     const size_t nb = size_t(b.nblocks());
     return align_up(nb) + align_up((nb + 3 * size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
            align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4 * kCursorStride) + 256;
@@ -87,14 +109,14 @@ size_t scratch_bytes(const Batch& b, int algo) {
 
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
-                      size_t scratch_size, int num_sms, cudaStream_t st, cudaEvent_t* events,
-                      bool prev0_integer, int* launches) {
+                      size_t scratch_size, int num_sms, cudaStream_t st, const Tuning& tune,
+                      cudaEvent_t* events, bool prev0_integer, int* launches) {
     const int algo = cfg.algo;
     const bool pa = algo == ME_ALGO_PA;
     if (pa) {  // one small pair: the whole pipeline in one shared-memory-resident CTA
         if (events)
             for (int i = 0; i < 3; ++i) cudaEventRecord(events[i], st);
-        const cudaError_t e0 = launch_pa_smem(b, cfg, prev0, prev0_integer, recs, stats, st);
+        const cudaError_t e0 = launch_pa_smem(b, cfg, prev0, prev0_integer, recs, stats, st, tune);
         if (e0 == cudaSuccess) {
             if (launches) *launches = 1 + (pred ? 1 : 0);
             if (events) cudaEventRecord(events[3], st);
@@ -107,8 +129,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         }
         if (e0 != cudaErrorNotSupported) return e0;
     }
-    const int nbins = pa ? pa_bins(b) : 1;
-    if (scratch_size < scratch_bytes(b, algo)) return cudaErrorInvalidValue;
+    const int nbins = pa ? pa_bins(b, tune) : 1;
+    if (scratch_size < scratch_bytes(b, algo, tune)) return cudaErrorInvalidValue;
     Scratch s = carve(b, nbins, scratch);
     cudaError_t e;
     if ((e = cudaMemsetAsync(s.hist, 0, size_t(nbins) * 4, st))) return e;
@@ -126,7 +148,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     ca.nbins = nbins;
     ca.stats = stats;
     {
-        const KeyParams k = pa_key(b);
+        const KeyParams k = pa_key(b, tune);
         ca.key_a = k.a;
         ca.key_s = k.s;
     }
@@ -135,19 +157,19 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     // PA kernel choice (pa.cu): the duo / quad kernels take list entries in
     // pairs / fours, so every wavefront step is padded to a multiple of 2 / 4;
     // the hybrids split the list into narrow / wide / narrow step ranges.
-    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, prev0_integer, num_sms) : 0;
+    const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, prev0_integer, num_sms, tune) : 0;
     int* ranges = pa_mode >= 3 ? s.counter + 8 : nullptr;
     if ((e = launch_scan(s.hist, nbins, pa_mode == 4 ? 4 : pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
-                         pa_wide_threshold(num_sms), ranges, st)))
+                         pa_wide_threshold(num_sms, tune), ranges, st, tune.sort_pdl)))
         return e;
-    if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st))) return e;
+    if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st, tune))) return e;
     const int* nlist = s.offs + nbins;
     if (events) cudaEventRecord(events[2], st);
 
     if (algo == ME_ALGO_ES)
         e = launch_es(b, cfg.search_range, s.list, nlist, s.counter, recs, stats, num_sms, st);
     else if (algo == ME_ALGO_PA)
-        e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st, s.counter + 1);
+        e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st, s.counter + 1, tune);
     else
         e = launch_ring(b, algo, cfg.search_range, s.list, nlist, recs, stats, num_sms, st);
     if (e) return e;

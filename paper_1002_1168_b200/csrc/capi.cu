@@ -306,6 +306,29 @@ void me_b200_ctx_destroy(me_ctx* c) {
 
 void* me_b200_ctx_stream(me_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
+me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* t) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!t) return me_fail(ME_ERR_INVALID_ARGUMENT, "null tuning");
+    if (t->pa_schedule < 0 || t->pa_schedule > ME_PA_SCHED_QUAD_HYBRID || t->pa_fast_ctas < 0 || t->pa_fast_ctas > 6 ||
+        (t->pa_quad_ctas && (t->pa_quad_ctas < 2 || t->pa_quad_ctas > 4)) ||
+        (t->pa_duo_threads && t->pa_duo_threads != 128 && t->pa_duo_threads != 256) || t->pa_poll_ns < 0 ||
+        t->pa_key_a < 0 || t->pa_key_s < 0 || t->fill_rows_per_cta < 0 || t->h2d_chunks < 0 || t->h2d_chunks > 32 ||
+        t->mask_pack < 0 || t->mask_pack > 3)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "tuning field out of range");
+    ctx->tuning = *t;
+    ctx->tune = mek::resolve_tuning(t);
+    return ok();
+}
+
+me_status me_b200_ctx_get_tuning(me_ctx* ctx, me_tuning* out) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!out) return me_fail(ME_ERR_INVALID_ARGUMENT, "null output");
+    *out = ctx->tuning;
+    return ok();
+}
+
 me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable) {
     me_status s = check_ctx(ctx);
     if (s) return s;
@@ -422,11 +445,11 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
         const int ns = std::min(per, n_seq - s0);
         const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, luma + seq_bytes * s0,
                                         alpha ? alpha + seq_bytes * s0 : nullptr);
-        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
         int nl = 0;
         ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs + seq_recs * s0, stats + size_t(pairs) * s0,
                                pred ? pred + size_t(W) * H * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
-                               ctx->num_sms, st, ctx->events(), false, &nl));
+                               ctx->num_sms, st, ctx->tune, ctx->events(), false, &nl));
         ctx->launches += nl;
     }
     ctx->ev_valid = ctx->profiling;
@@ -451,10 +474,10 @@ me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int
     mek::Batch b = make_batch(cfg, n_seq, n_frames, W, H, luma, alpha);
     b.v0 = row0;
     b.v1 = row1;
-    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
     int nl = 0;
     ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
-                           st, ctx->events(), false, &nl));
+                           st, ctx->tune, ctx->events(), false, &nl));
     ctx->launches = nl;
     ctx->ev_valid = ctx->profiling;
     return ok();
@@ -532,8 +555,8 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     // Chunked pipeline: the sequences are independent, so chunk k's H2D (copy
     // stream) overlaps chunk k-1's estimation (compute stream) and chunk
     // k-2's D2H (d2h stream).  PCIe is the bound of this path.
-    const char* nc = getenv("ME_B200_CHUNKS");
-    const int nchunks = std::min(n_seq, std::max(1, std::min(kPipelineChunks, nc ? atoi(nc) : 16)));
+
+    const int nchunks = std::min(n_seq, std::max(1, std::min(kPipelineChunks, ctx->tune.h2d_chunks)));
     uint8_t* dl = static_cast<uint8_t*>(ctx->in_luma.p);
     uint8_t* da = static_cast<uint8_t*>(ctx->in_alpha.p);
     me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
@@ -541,8 +564,8 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     uint8_t* dp = static_cast<uint8_t*>(ctx->out_pred.p);
     // Binary alpha masks cross PCIe bit-packed (packed on the host cores while
     // the previous chunk's copies are in flight, expanded on the device).
-    const bool pack = alpha && !getenv("ME_B200_NO_MASK_PACK");
-    const bool sparse = !getenv("ME_B200_DENSE_MASK_PACK");
+    const bool pack = alpha && ctx->tune.mask_pack != 1;
+    const bool sparse = ctx->tune.mask_pack != 2;
     const size_t max_chunk = seq_bytes * size_t((n_seq + nchunks - 1) / nchunks);
     if (pack)
         for (int i = 0; i < 2; ++i) {
@@ -594,11 +617,11 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
         ME_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[k], 0));
         const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, dl + seq_bytes * s0,
                                         alpha ? da + seq_bytes * s0 : nullptr);
-        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
         int nl = 0;
         ME_CUDA(mek::run_batch(b, *cfg, nullptr, dr + seq_recs * s0, ds + size_t(pairs) * s0,
                                pred ? dp + plane * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
-                               ctx->num_sms, ctx->stream, nullptr, false, &nl));
+                               ctx->num_sms, ctx->stream, ctx->tune, nullptr, false, &nl));
         ctx->launches += nl + (packed_chunk ? 1 : 0);
         ME_CUDA(cudaEventRecord(ctx->ev_out[k], ctx->stream));
         ME_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_out[k], 0));
@@ -685,13 +708,13 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
     if (prev_mv)
         for (size_t i = 0; i < size_t(cols) * rows * 2 && prev_integer; ++i) prev_integer = (prev_mv[i] & 1) == 0;
     const mek::Batch b = make_batch(&c1, 1, 2, W, H, L, alpha_dev);
-    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo)));
+    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
     // records and stats in one device buffer -> one D2H into pinned memory
     me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
     me_pair_stats* ds = reinterpret_cast<me_pair_stats*>(dr + size_t(cols) * rows);
     int nl = 0;
     ME_CUDA(mek::run_batch(b, c1, prev_dev, dr, ds, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
-                           ctx->stream, ctx->events(), prev_integer, &nl));
+                           ctx->stream, ctx->tune, ctx->events(), prev_integer, &nl));
     ctx->launches = nl;
     ctx->ev_valid = ctx->profiling;
     ME_CUDA(cudaMemcpyAsync(ctx->pin_b.p, dr, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -25,8 +25,31 @@ struct Batch {
     __host__ __device__ int steps() const { return (cols - 1) + 2 * (rows - 1) + (pairs - 1) + 1; }
 };
 
+// Kernel-schedule tuning with the defaults applied (from a context's
+// me_tuning, include/me_b200.h; the defaults are the measured best).
+struct Tuning {
+    int pa_schedule = ME_PA_SCHED_AUTO;
+    int pa_wide_blocks = 0;  // 0: 40 x SMs
+    int pa_fast_ctas = 0;    // 0: by wavefront width
+    int pa_quad_ctas = 3;
+    int pa_duo_threads = 256;
+    int pa_duo_ctas = 0;     // 0: 4 (256 threads) or 7 (128)
+    int pa_poll_ns = 64;
+    bool pa_claim = true;    // in-order CTA-batch claiming
+    bool pa_pdl = true;
+    bool pa_smem_pair = true;
+    int key_a = 1, key_s = 0;
+    bool sort_pdl = true;
+    int fill_rows = 0;       // 1 a thread per row, -1 a thread per block, 0 by size
+    int fill_rows_per_cta = 64;
+    int h2d_chunks = 16;
+    int mask_pack = 3;       // 1 bytes, 2 dense bits, 3 sparse bits
+    const char* pa_trace = nullptr;
+};
+Tuning resolve_tuning(const me_tuning* t);
+
 // Scratch needed by run_batch (bytes), given the step-bin count.
-size_t scratch_bytes(const Batch& b, int algo);
+size_t scratch_bytes(const Batch& b, int algo, const Tuning& t);
 
 // Full device pipeline: classify -> (ES | rings | PA wavefront) -> MC + PSNR.
 // `prev0` (nullable, [rows*cols][2] int32) supplies pair 0's temporal
@@ -39,7 +62,7 @@ size_t scratch_bytes(const Batch& b, int algo);
 // `launches` (nullable) receives the number of kernels launched.
 cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0,
                       me_block_rec* recs, me_pair_stats* stats, uint8_t* pred, void* scratch,
-                      size_t scratch_size, int num_sms, cudaStream_t st,
+                      size_t scratch_size, int num_sms, cudaStream_t st, const Tuning& tune,
                       cudaEvent_t* events = nullptr, bool prev0_integer = false, int* launches = nullptr);
 
 // Single-block entry points (all pointers device pointers; outputs in `out`,

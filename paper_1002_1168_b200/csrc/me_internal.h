@@ -61,8 +61,12 @@ struct HostBuf {
     }
 };
 
+#include "kernels.h"
+
 struct me_ctx {
     int device = 0;
+    me_tuning tuning = {};  // as set by me_b200_ctx_set_tuning (zeros: defaults)
+    mek::Tuning tune;       // resolved
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     // scratch for the batched pipeline

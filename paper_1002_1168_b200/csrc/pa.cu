@@ -1916,23 +1916,22 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
 
 
 // Steps with at least this many estimated blocks run two blocks per warp.
-int pa_wide_threshold(int num_sms) {
-    const char* e = getenv("ME_PA_WIDE");
-    return e ? atoi(e) : num_sms * 40;  // measured: 3000-9000 within 1 %, duo-only 3 % slower
+int pa_wide_threshold(int num_sms, const Tuning& t) {
+    return t.pa_wide_blocks > 0 ? t.pa_wide_blocks : num_sms * 40;  // measured: 3000-9000 within 1 %, duo-only 3 % slower
 }
 
 int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
-                   int num_sms) {
+                   int num_sms, const Tuning& t) {
     const int step = cfg.halfpel ? 1 : cfg.step;
     const bool fast = b.bs == 8 && step == 2 && cfg.max_iterations <= 4 && (!prev0 || prev0_integer) &&
                       size_t(b.n_seq) * b.F * b.W * b.H < (size_t(1) << 32);
-    const char* mode = getenv("ME_PA_MODE");
-    if (!fast || (mode && std::string(mode) == "warp")) return 0;
-    if (mode && std::string(mode) == "fast") return 1;
+    const int sched = t.pa_schedule;
+    if (!fast || sched == ME_PA_SCHED_GENERIC) return 0;
+    if (sched == ME_PA_SCHED_FAST) return 1;
     if (prev0) return 1;  // the two-blocks-per-warp kernel takes no external prev field
-    if (mode && std::string(mode) == "duo") return 2;
-    if (mode && std::string(mode) == "duo-hybrid") return 3;
-    if (mode && (std::string(mode) == "hybrid" || std::string(mode) == "quad")) return 4;
+    if (sched == ME_PA_SCHED_DUO) return 2;
+    if (sched == ME_PA_SCHED_DUO_HYBRID) return 3;
+    if (sched == ME_PA_SCHED_QUAD_HYBRID) return 4;
     const int64_t per_step = b.nblocks() / std::max(1, b.steps());
     return per_step >= int64_t(num_sms) * 160 ? 4 : 1;
 }
@@ -1941,11 +1940,11 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
 // returns cudaErrorNotSupported when not eligible (the caller runs the
 // batched pipeline instead).
 cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
-                           me_block_rec* recs, me_pair_stats* stats, cudaStream_t st) {
+                           me_block_rec* recs, me_pair_stats* stats, cudaStream_t st, const Tuning& t) {
     const int step = cfg.halfpel ? 1 : cfg.step;
     if (!(b.n_seq == 1 && b.pairs == 1 && b.bs == 8 && step == 2 && cfg.max_iterations <= 4 &&
           (!prev0 || prev0_integer) && (size_t(b.W) * b.H) % 16 == 0) ||
-        getenv("ME_PA_NO_SMEM"))
+        !t.pa_smem_pair)
         return cudaErrorNotSupported;
     const int plane_pad = b.W * b.H + 16;
     const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * 13 + 16;
@@ -1969,7 +1968,7 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
 
 cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0, const uint2* list,
                       const int* nlist, const int* ranges, int pa_mode, me_block_rec* recs,
-                      me_pair_stats* stats, int num_sms, cudaStream_t st, int* claims) {
+                      me_pair_stats* stats, int num_sms, cudaStream_t st, int* claims, const Tuning& t) {
     cudaError_t e;
     PaArgs pa_args;
     pa_args.b = b;
@@ -1981,11 +1980,11 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     pa_args.prev0 = prev0;
     pa_args.stats = stats;
     pa_args.fast = (pa_args.P.step == 2 && cfg.max_iterations <= 4) ? 1 : 0;
-    pa_args.poll_ns = getenv("ME_PA_POLL_NS") ? atoi(getenv("ME_PA_POLL_NS")) : 64;
+    pa_args.poll_ns = t.pa_poll_ns;
     pa_args.pdl = 0;
     pa_args.trace = nullptr;
     pa_args.claim = nullptr;
-    const char* trace_path = getenv("ME_PA_TRACE");
+    const char* trace_path = t.pa_trace;
     int n_host = 0;
     if (trace_path) {
         cudaStreamSynchronize(st);
@@ -1993,13 +1992,11 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         cudaMalloc(&pa_args.trace, size_t(n_host) * 32);
         cudaMemset(pa_args.trace, 0, size_t(n_host) * 32);
     }
-    const char* cta = getenv("ME_PA_CTA");
-    const char* minb = getenv("ME_PA_MINB");
     using PaKernel = void (*)(const PaArgs);
-    // ME_PA_PDL=0 launches the hybrid's grids in plain stream order
-    const bool pdl = pa_mode == 4 && !trace_path && !(getenv("ME_PA_PDL") && atoi(getenv("ME_PA_PDL")) == 0);
+    // pa_no_pdl launches the hybrid's grids in plain stream order
+    const bool pdl = pa_mode == 4 && !trace_path && t.pa_pdl;
     // persistent grids: every warp of a launch must be co-resident (dependency spinning)
-    const bool dyn = !(getenv("ME_PA_CLAIM") && atoi(getenv("ME_PA_CLAIM")) == 0);
+    const bool dyn = t.pa_claim;
     int n_launch = 0;
     auto launch = [&](PaKernel kern, int threads, int warp_words, const int* range, bool chained = false,
                       bool after_sort = false) -> cudaError_t {
@@ -2038,14 +2035,14 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         // (measured 3-6 % on configs 2, 3, 5 and 4-32 sequences); wider ones
         // need the blocks in flight of 4 CTAs per SM
         const int64_t per_step = b.nblocks() / std::max(1, b.steps());
-        const int mb = minb ? atoi(minb) : (pa_mode == 1 && per_step < int64_t(num_sms) * 100 ? 1 : 4);
+        const int mb = t.pa_fast_ctas > 0 ? t.pa_fast_ctas : (pa_mode == 1 && per_step < int64_t(num_sms) * 100 ? 1 : 4);
         fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         if (trace_path) fast = pa_fast_kernel<4, true>;
     }
-    const int duo_threads = cta ? atoi(cta) : 256;
+    const int duo_threads = t.pa_duo_threads == 128 ? 128 : 256;
     PaKernel duo = pa_duo_kernel<256, 4>;
     {
-        const int mb = minb ? atoi(minb) : 4;
+        const int mb = t.pa_duo_ctas > 0 ? t.pa_duo_ctas : duo_threads == 128 ? 7 : 4;
         if (trace_path)
             duo = pa_duo_kernel<256, 4, true>;
         else if (duo_threads == 128)
@@ -2063,11 +2060,10 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     } else if (pa_mode == 4) {  // narrow steps -> fast, the wide middle -> quad, narrow tail -> fast
         // 3 CTAs (24 warps, 96 blocks in flight) per SM at 80 registers:
         // measured 8 % faster than 4 at 64 (spills) and 1 % than 2 at 112
-        const char* qm = getenv("ME_PA_QMINB");
-        const int mb = qm ? atoi(qm) : 3;
+        const int mb = t.pa_quad_ctas;
         PaKernel quad = mb == 4 ? pa_quad_kernel<4> : mb == 2 ? pa_quad_kernel<2> : pa_quad_kernel<3>;
         if (trace_path) quad = pa_quad_kernel<3, true>;
-        if (!(e = launch(fast, 256, kFastWarpWords, ranges, pdl_sort(), pdl_sort())) &&
+        if (!(e = launch(fast, 256, kFastWarpWords, ranges, t.sort_pdl, t.sort_pdl)) &&
             !(e = launch(quad, 256, kQuadWarpWords, ranges + 2, true)))
             e = launch(fast, 256, kFastWarpWords, ranges + 4, true);
     } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast

@@ -32,10 +32,11 @@ struct ClassArgs {
 
 // wavefront.cu: classify -> per-step histogram -> scan -> fill (the sorted list)
 cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st);
-bool pdl_sort();  // scan, fill and the PA head chained by programmatic dependent launch
+// (pdl: scan, fill and the PA head chained by programmatic dependent launch)
 cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
-                        int wide, int* ranges, cudaStream_t st);
-cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st);
+                        int wide, int* ranges, cudaStream_t st, bool pdl);
+cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st,
+                        const Tuning& t);
 
 // es.cu: full search over the list; single-block full search
 cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist, int* counter,
@@ -50,15 +51,15 @@ cudaError_t launch_ring_single(int algo, const uint8_t* cur, const uint8_t* ref,
                                int x0, int y0, int size, int range, int64_t* out, cudaStream_t st);
 
 // pa.cu: the proposed algorithm's wavefront (kernel choice, list ranges)
-int pa_wide_threshold(int num_sms);
+int pa_wide_threshold(int num_sms, const Tuning& t);
 int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
-                   int num_sms);
+                   int num_sms, const Tuning& t);
 cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* prev0, bool prev0_integer,
-                           me_block_rec* recs, me_pair_stats* stats, cudaStream_t st);
+                           me_block_rec* recs, me_pair_stats* stats, cudaStream_t st, const Tuning& t);
 // claims: 3 zeroed counters (in-order dynamic claiming, one per launch) or null
 cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0, const uint2* list,
                       const int* nlist, const int* ranges, int pa_mode, me_block_rec* recs,
-                      me_pair_stats* stats, int num_sms, cudaStream_t st, int* claims);
+                      me_pair_stats* stats, int num_sms, cudaStream_t st, int* claims, const Tuning& t);
 
 // frame_ops.cu: the prediction pass of a batch (only when asked for)
 cudaError_t launch_mc_pred(const Batch& b, const me_block_rec* recs, uint8_t* pred, cudaStream_t st);

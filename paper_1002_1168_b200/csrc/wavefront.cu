@@ -370,11 +370,6 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(ClassArgs a, int* cursor
 // Launchers
 // ---------------------------------------------------------------------------
 
-// ME_PDL_SORT=0 launches scan and fill in plain stream order
-bool pdl_sort() {
-    static const bool on = !(getenv("ME_PDL_SORT") && atoi(getenv("ME_PDL_SORT")) == 0);
-    return on;
-}
 
 static cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t lc = {};
@@ -408,8 +403,8 @@ cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
 }
 
 cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
-                        int wide, int* ranges, cudaStream_t st) {
-    if (pdl_sort()) {
+                        int wide, int* ranges, cudaStream_t st, bool pdl) {
+    if (pdl) {
         cudaLaunchConfig_t lc = pdl_config(dim3(1), dim3(1024), 0, st);
         cudaLaunchAttribute at[1];
         pdl_attr(lc, at);
@@ -419,11 +414,12 @@ cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cur
     return cudaGetLastError();
 }
 
-cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st) {
+cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st,
+                        const Tuning& t) {
     const Batch& b = ca.b;
     // <= 64 rows per CTA, >= 2 CTAs per SM
     const int64_t nrows = int64_t(b.n_seq) * b.pairs * b.rows;
-    const int64_t rmax = getenv("ME_FILL_RPC") ? atoi(getenv("ME_FILL_RPC")) : 64;  // measured: 64 <= 32, 128 < 256
+    const int64_t rmax = t.fill_rows_per_cta;  // measured: 64 <= 32, 128 < 256
     const int64_t rpc = std::max<int64_t>(4, std::min<int64_t>(rmax, nrows / (2 * num_sms)));
     const int grid = int((nrows + rpc - 1) / rpc);
     const size_t smem = 2 * size_t(ca.nbins) * 4;
@@ -433,12 +429,11 @@ cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_s
         return e;
     // large batches: a thread per block row (measured 60 -> 31 us on cfg4);
     // few rows (single sequences) keep the per-block kernel's parallelism
-    const char* fr = getenv("ME_FILL_ROWS");
-    if (fr ? atoi(fr) != 0 : nrows >= int64_t(num_sms) * 64) {
+    if (t.fill_rows ? t.fill_rows > 0 : nrows >= int64_t(num_sms) * 64) {
         if (smem > 48 * 1024 &&
             (e = cudaFuncSetAttribute(fill_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
             return e;
-        if (pdl_sort()) {
+        if (t.sort_pdl) {
             cudaLaunchConfig_t lc = pdl_config(dim3(unsigned((nrows + 255) / 256)), dim3(256), smem, st);
             cudaLaunchAttribute at[1];
             pdl_attr(lc, at);

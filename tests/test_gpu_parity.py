@@ -246,9 +246,24 @@ def test_estimate_field_random_prev(me_gpu, port, odd):
     assert_recs(recs, want)
 
 
+@pytest.fixture
+def tuning(me_gpu):
+    """Sets this thread's context tuning for one test (me_b200_ctx_set_tuning), restored after."""
+    from paper_1002_1168_b200 import _lib
+
+    saved = []
+
+    def set_(**kw):
+        saved.append(_lib.set_tuning(0, **kw))
+
+    yield set_
+    if saved:
+        _lib.restore_tuning(saved[0], 0)
+
+
 @pytest.mark.parametrize("bt,it", [(0, 4), (1, 4), (0, 7)])
-@pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid", "warp"])
-def test_pa_kernel_modes(me_gpu, port, mode, bt, it, monkeypatch):
+@pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid", "warp", "hybrid-static"])
+def test_pa_kernel_modes(me_gpu, port, mode, bt, it, tuning):
     """Every PA kernel schedule (one block per warp, two per warp, the hybrid
     splits of the sorted list with two or four blocks per warp in the wide
     range, the generic kernel) on the same batch; the hybrids' wide threshold
@@ -256,8 +271,7 @@ def test_pa_kernel_modes(me_gpu, port, mode, bt, it, monkeypatch):
     BoundaryTemporal::Shape and a longer PRS iteration limit."""
     from paper_1002_1168_b200 import synth
 
-    monkeypatch.setenv("ME_PA_MODE", mode)
-    monkeypatch.setenv("ME_PA_WIDE", "4")
+    tuning(pa_schedule=mode.split("-static")[0], pa_wide_blocks=4, pa_static_claim=int(mode.endswith("-static")))
     luma, alpha = synth.config4_batch(5, 700, frames=6)
     cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8),
                              prs=me_gpu.PrsConfig(max_iterations=it), boundary_temporal=me_gpu.BoundaryTemporal(bt))
@@ -300,14 +314,12 @@ def test_concurrent_host_threads(me_gpu, port):
 
 @pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid"])
 @pytest.mark.parametrize("shape", [(16, 16), (48, 32), (64, 80)])
-def test_pa_kernel_modes_small_frames(me_gpu, port, mode, shape, monkeypatch):
+def test_pa_kernel_modes_small_frames(me_gpu, port, mode, shape, tuning):
     """Every PA schedule on frames a few blocks wide (patches clipped by every
     frame edge, windows smaller than the search range), with masks mixing
     transparent, opaque and boundary blocks and strong motion."""
     H, W = shape
-    monkeypatch.setenv("ME_PA_MODE", mode)
-    monkeypatch.setenv("ME_PA_WIDE", "1")
-    monkeypatch.setenv("ME_PA_NO_SMEM", "1")  # the batched kernels, not the one-CTA pair kernel
+    tuning(pa_schedule=mode, pa_wide_blocks=1, pa_no_smem_pair=1)  # the batched kernels, not the one-CTA pair kernel
     rng = np.random.default_rng(H * 1000 + W)
     n_seq, F = 6, 5
     base = noise(rng, H + 40, W + 40)
