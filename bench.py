@@ -384,6 +384,50 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
     if world > 1:
         dist.barrier()
 
+    # the same batch with the masks resident bit-packed (binary masks: exact;
+    # 1/8 of the mask bytes): classify and the PA kernels read the bit planes
+    bits_layout = None
+    if algo == "PA" and not args.no_bits:
+        bits, binary = B.pack_mask_dev(alpha, device=local)
+        if binary:
+            recs_b = torch.empty_like(recs)
+            stats_b = torch.empty_like(stats)
+            for _ in range(warmup):
+                B.run_sequences_bits_dev(cfg, luma, bits, recs_b, stats_b, device=local, stream=stream.cuda_stream)
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            clocks_b = ClockSampler(local).start()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                B.run_sequences_bits_dev(cfg, luma, bits, recs_b, stats_b, device=local, stream=stream.cuda_stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            clk_b = clocks_b.stop()
+            ms_b = mdist.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
+            _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
+            st_b = np.zeros(4)
+            for _ in range(n_stage):
+                B.run_sequences_bits_dev(cfg, luma, bits, recs_b, stats_b, device=local, stream=stream.cuda_stream)
+                _lib.check(lib.me_b200_ctx_stage_ms(ctxh, stage, 4))
+                st_b += np.array(stage[:])
+            _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))
+            st_b /= n_stage
+            same = bool(torch.equal(recs_b, recs) and torch.equal(stats_b, stats))
+            bytes_b = n_seq * F * W * H * 9 // 8 + n_seq * pairs * rows * cols * 16
+            ach_b = bytes_b / (float(st_b.sum()) / 1e3) / 1e9
+            bits_layout = {"ms_per_step": ms_b, "value": total_units / (ms_b / 1e3), "unit": "MB/s",
+                           "stages_ms": {"classify": st_b[0], "sort": st_b[1], "search": st_b[2], "mc_psnr": st_b[3]},
+                           "identical_to_byte_masks": same, "clocks": clk_b,
+                           "roofline": {"bound": "hbm", "achieved": ach_b, "peak": peaks()[0], "unit": "GB/s", "frac": ach_b / peaks()[0],
+                                        "algorithmic_bytes_per_step": bytes_b},
+                           "note": "masks resident in HBM as bit planes (me_b200_run_sequences_bits_dev; packed once by me_b200_pack_mask_dev outside the timed region): 1/8 of the mask bytes, shape SADs as popc(XOR) of bit rows"}
+            if not same:
+                raise SystemExit("bit-packed mask run differs from the byte-mask run")
+            del recs_b, stats_b
+        del bits
+
     # results of the whole batch on rank 0 (the gather's payload at N > 1)
     if world > 1:
         if rank == 0:
@@ -505,6 +549,7 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
             "parity": parity,
+            "bits_layout": bits_layout,
             "estimated_blocks": est,
             "macroblocks_per_step": int(total_units),
         }
@@ -675,6 +720,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-es", action="store_true", help="skip the es_cfg5 leg of the default run")
+    ap.add_argument("--no-bits", action="store_true", help="skip the bit-packed-mask layout leg")
     ap.add_argument("--es-steps", type=int, default=5)
     ap.add_argument("--es-frames", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=0)

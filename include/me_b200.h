@@ -202,6 +202,24 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
                                     const uint8_t* alpha, me_block_rec* recs,
                                     me_pair_stats* stats, uint8_t* pred, void* stream);
 
+/* Same, with BINARY masks bit-packed in device memory: alpha_bits is
+ * [n_seq][n_frames][height][width / 8] bytes, bit i of byte j = pel 8j + i,
+ * set = inside (me_b200_pack_mask_dev makes it; 8-byte aligned).  1/8 of the
+ * mask bytes in HBM; block classes come from the bits and boundary blocks'
+ * shape SADs are popc(XOR) of bit rows (metrics.cpp:65-84 is a mismatch count,
+ * which for 0/255 masks is the XOR count).  Results equal
+ * me_b200_run_sequences_dev on the 0/255 byte masks. */
+me_status me_b200_run_sequences_bits_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames,
+                                         int width, int height, const uint8_t* luma,
+                                         const uint8_t* alpha_bits, me_block_rec* recs,
+                                         me_pair_stats* stats, uint8_t* pred, void* stream);
+
+/* Packs n device mask bytes (n % 64 == 0) into the bit plane above and sets
+ * *binary (host) to 1 when every byte was 0 or 255 (the bit form is then
+ * exact), else 0.  Synchronous on `stream`. */
+me_status me_b200_pack_mask_dev(me_ctx* ctx, const uint8_t* alpha, size_t n, uint8_t* bits, int* binary,
+                                void* stream);
+
 /* A block-row band [row0, row1) of the same batch (baselines ES/TSS/FSS/DS
  * only; PA blocks depend on the rows above -> ME_ERR_INVALID_ARGUMENT): the
  * unit of the row sharding across GPUs.  Records of the band's

@@ -94,6 +94,47 @@ def _check_dev_buffers(luma, alpha, recs, stats, pred, device, recs_shape, stats
     chk("pred", pred, pred_shape)
 
 
+def pack_mask_dev(alpha, device: int = 0, stream=None):
+    """Device mask bytes [..., H, W] -> (bit plane uint8 [..., H, W // 8] with
+    bit i of byte j = pel 8j + i, binary): me_b200_pack_mask_dev.  The bit
+    form is exact when `binary` (every byte 0 or 255)."""
+    import torch
+
+    if alpha.dtype != torch.uint8 or not alpha.is_contiguous() or alpha.numel() % 64:
+        raise ValueError("alpha: contiguous uint8 CUDA tensor with a multiple of 64 elements")
+    bits = torch.empty(alpha.shape[:-1] + (alpha.shape[-1] // 8,), dtype=torch.uint8, device=alpha.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(alpha.device).cuda_stream
+    flag = C.c_int()
+    check(lib().me_b200_pack_mask_dev(ctx(device), C.c_void_p(alpha.data_ptr()), alpha.numel(), C.c_void_p(bits.data_ptr()), C.byref(flag), C.c_void_p(stream)))
+    return bits, bool(flag.value)
+
+
+def run_sequences_bits_dev(cfg: BatchConfig, luma, alpha_bits, recs=None, stats=None, pred=None, device: int = 0, stream=None):
+    """run_sequences_dev with BINARY masks as device bit planes
+    (me_b200_run_sequences_bits_dev): alpha_bits [n_seq, F, H, W // 8]."""
+    import torch
+
+    n_seq, F, H, W = luma.shape
+    bs = cfg.search.block_size
+    pairs = F - cfg.search.ref_distance
+    rows, cols = H // bs, W // bs
+    if recs is None:
+        recs = torch.empty((n_seq, pairs, rows, cols, 16), dtype=torch.uint8, device=luma.device)
+    if stats is None:
+        stats = torch.empty((n_seq, pairs, 48), dtype=torch.uint8, device=luma.device)
+    _check_dev_buffers(luma, None, recs, stats, pred, device, (n_seq, pairs, rows, cols, 16), (n_seq, pairs, 48), (n_seq, pairs, H, W))
+    if alpha_bits.dtype != torch.uint8 or not alpha_bits.is_contiguous() or tuple(alpha_bits.shape) != (n_seq, F, H, W // 8):
+        raise ValueError("alpha_bits: contiguous uint8 [n_seq, F, H, W // 8]")
+    if stream is None:
+        stream = torch.cuda.current_stream(luma.device).cuda_stream
+    c = cfg.c()
+    check(lib().me_b200_run_sequences_bits_dev(ctx(device), C.byref(c), n_seq, F, W, H, C.c_void_p(luma.data_ptr()), C.c_void_p(alpha_bits.data_ptr()),
+                                               C.c_void_p(recs.data_ptr()), C.c_void_p(stats.data_ptr()),
+                                               C.c_void_p(pred.data_ptr()) if pred is not None else None, C.c_void_p(stream)))
+    return recs, stats
+
+
 def run_band_dev(cfg: BatchConfig, luma, alpha, row0: int, row1: int, recs, stats, device: int = 0, stream=None):
     """The block-row band [row0, row1) of a device-resident batch
     (me_b200_run_band_dev; baselines only): writes the band's records, and its

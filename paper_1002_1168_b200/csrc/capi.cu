@@ -291,7 +291,7 @@ void me_b200_ctx_destroy(me_ctx* c) {
         cudaStreamDestroy(c->copy_stream);
         cudaStreamDestroy(c->d2h_stream);
     }
-    for (DevBuf* b : {&c->types, &c->worklist, &c->counters, &c->tasks, &c->in_luma, &c->in_alpha,
+    for (DevBuf* b : {&c->types, &c->worklist, &c->counters, &c->tasks, &c->in_luma, &c->in_alpha, &c->in_bits,
                       &c->out_recs, &c->out_stats, &c->out_pred, &c->aux})
         b->release();
     c->pin_a.release();
@@ -456,6 +456,62 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
     return ok();
 }
 
+me_status me_b200_run_sequences_bits_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames,
+                                         int W, int H, const uint8_t* luma, const uint8_t* alpha_bits,
+                                         me_block_rec* recs, me_pair_stats* stats, uint8_t* pred,
+                                         void* stream) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
+    if (!luma || !alpha_bits || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    if ((reinterpret_cast<uintptr_t>(luma) | reinterpret_cast<uintptr_t>(recs)) & 15 ||
+        reinterpret_cast<uintptr_t>(alpha_bits) & 7)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "device buffers must be 16-byte (masks 8-byte) aligned");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t seq_bytes = size_t(n_frames) * size_t(W) * size_t(H);
+    const int per = int(std::max<size_t>(1, std::min<size_t>(size_t(n_seq), ((size_t(1) << 32) - 1) / seq_bytes)));
+    const int pairs = n_frames - cfg->ref_distance;
+    const size_t seq_recs = size_t(pairs) * (W / cfg->block_size) * (H / cfg->block_size);
+    ctx->launches = 0;
+    for (int s0 = 0; s0 < n_seq; s0 += per) {
+        const int ns = std::min(per, n_seq - s0);
+        mek::Batch b = make_batch(cfg, ns, n_frames, W, H, luma + seq_bytes * s0, nullptr);
+        b.alpha_bits = alpha_bits + seq_bytes / 8 * s0;
+        if (cfg->algo == ME_ALGO_PA && !mek::pa_takes_bits(b, *cfg, ctx->num_sms, ctx->tune)) {
+            // this PA schedule (16x16 blocks, half-pel, duo kernels) reads mask bytes
+            ME_CUDA(ctx->aux.reserve(seq_bytes * ns));
+            ME_CUDA(mek::unpack_mask(b.alpha_bits, static_cast<uint8_t*>(ctx->aux.p), seq_bytes * ns, st));
+            b.alpha = static_cast<const uint8_t*>(ctx->aux.p);
+            b.alpha_bits = nullptr;
+            ctx->launches += 1;
+        }
+        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
+        int nl = 0;
+        ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs + seq_recs * s0, stats + size_t(pairs) * s0,
+                               pred ? pred + size_t(W) * H * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
+                               ctx->num_sms, st, ctx->tune, ctx->events(), false, &nl));
+        ctx->launches += nl;
+    }
+    ctx->ev_valid = ctx->profiling;
+    return ok();
+}
+
+me_status me_b200_pack_mask_dev(me_ctx* ctx, const uint8_t* alpha, size_t n, uint8_t* bits, int* binary,
+                                void* stream) {
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!alpha || !bits || !binary || n % 64) return me_fail(ME_ERR_INVALID_ARGUMENT, "bad mask buffers");
+    ME_CUDA(ctx->aux.reserve(16));
+    int* flag = static_cast<int*>(ctx->aux.p);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ME_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+    ME_CUDA(mek::pack_mask_dev(alpha, n, bits, flag, st));
+    ME_CUDA(cudaMemcpyAsync(binary, flag, 4, cudaMemcpyDeviceToHost, st));
+    ME_CUDA(cudaStreamSynchronize(st));
+    *binary = !*binary;  // flag counts non-binary bytes
+    return ok();
+}
+
 me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
                                int H, const uint8_t* luma, const uint8_t* alpha, int row0, int row1,
                                me_block_rec* recs, me_pair_stats* stats, void* stream) {
@@ -548,6 +604,7 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     const size_t seq_recs = size_t(pairs) * (W / cfg->block_size) * (H / cfg->block_size);
     ME_CUDA(ctx->in_luma.reserve(seq_bytes * n_seq + 256));
     if (alpha) ME_CUDA(ctx->in_alpha.reserve(seq_bytes * n_seq + 256));
+    if (alpha) ME_CUDA(ctx->in_bits.reserve(seq_bytes * n_seq / 8 + 256));
     ME_CUDA(ctx->out_recs.reserve(seq_recs * n_seq * sizeof(me_block_rec)));
     ME_CUDA(ctx->out_stats.reserve(size_t(n_seq) * pairs * sizeof(me_pair_stats)));
     if (pred) ME_CUDA(ctx->out_pred.reserve(plane * pairs * n_seq));
@@ -559,6 +616,7 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
     const int nchunks = std::min(n_seq, std::max(1, std::min(kPipelineChunks, ctx->tune.h2d_chunks)));
     uint8_t* dl = static_cast<uint8_t*>(ctx->in_luma.p);
     uint8_t* da = static_cast<uint8_t*>(ctx->in_alpha.p);
+    uint8_t* dbits = static_cast<uint8_t*>(ctx->in_bits.p);
     me_block_rec* dr = static_cast<me_block_rec*>(ctx->out_recs.p);
     me_pair_stats* ds = static_cast<me_pair_stats*>(ctx->out_stats.p);
     uint8_t* dp = static_cast<uint8_t*>(ctx->out_pred.p);
@@ -580,7 +638,8 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
         const size_t o = seq_bytes * s0, n = seq_bytes * ns;
         ME_CUDA(cudaMemcpyAsync(dl + o, luma + o, n, cudaMemcpyHostToDevice, ctx->copy_stream));
         ctx->h2d_bytes += int64_t(n);
-        bool packed_chunk = false;  // one expansion kernel when the mask went bit-packed
+        bool packed_chunk = false;  // the mask went bit-packed (binary)
+        int unpack_launches = 0;    // the sparse form's expansion to the dense bit plane
         if (alpha) {
             const int slot = k & 1;
             bool packed = false;
@@ -597,13 +656,15 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
                         ME_CUDA(cudaMemcpyAsync(db, hb, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
                         ctx->h2d_bytes += int64_t(bytes);
                         ME_CUDA(cudaEventRecord(ctx->ev_pack[slot], ctx->copy_stream));
-                        ME_CUDA(mek::unpack_mask_sparse(db, da + o, n, ctx->copy_stream));
+                        // to the dense bit plane the kernels read (not to bytes)
+                        ME_CUDA(mek::unpack_mask_sparse_bits(db, dbits + o / 8, n, ctx->copy_stream));
+                        unpack_launches = 1;
                     }
                 } else if ((packed = pack_binary_mask(alpha + o, n, hb))) {
-                    ME_CUDA(cudaMemcpyAsync(db, hb, n / 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+                    // the dense bit plane itself
+                    ME_CUDA(cudaMemcpyAsync(dbits + o / 8, hb, n / 8, cudaMemcpyHostToDevice, ctx->copy_stream));
                     ctx->h2d_bytes += int64_t(n / 8);
                     ME_CUDA(cudaEventRecord(ctx->ev_pack[slot], ctx->copy_stream));
-                    ME_CUDA(mek::unpack_mask(db, da + o, n, ctx->copy_stream));
                 }
                 packed_chunk = packed;
             }
@@ -615,14 +676,25 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
         ME_CUDA(cudaEventRecord(ctx->ev_in[k], ctx->copy_stream));
         // estimation of chunk k (compute stream) and its D2H (d2h stream)
         ME_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[k], 0));
-        const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, dl + seq_bytes * s0,
-                                        alpha ? da + seq_bytes * s0 : nullptr);
-        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
+        mek::Batch b = make_batch(cfg, ns, n_frames, W, H, dl + seq_bytes * s0,
+                                  alpha ? da + seq_bytes * s0 : nullptr);
         int nl = 0;
+        if (packed_chunk) {  // binary masks: the kernels read the bit plane (popc(XOR) shape SADs)
+            b.alpha = nullptr;
+            b.alpha_bits = dbits + seq_bytes * s0 / 8;
+            if (cfg->algo == ME_ALGO_PA && !mek::pa_takes_bits(b, *cfg, ctx->num_sms, ctx->tune)) {
+                ME_CUDA(mek::unpack_mask(b.alpha_bits, da + seq_bytes * s0, n, ctx->stream));  // this schedule reads bytes
+                b.alpha = da + seq_bytes * s0;
+                b.alpha_bits = nullptr;
+                ++nl;
+            }
+        }
+        ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
+        int nb = 0;
         ME_CUDA(mek::run_batch(b, *cfg, nullptr, dr + seq_recs * s0, ds + size_t(pairs) * s0,
                                pred ? dp + plane * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
-                               ctx->num_sms, ctx->stream, ctx->tune, nullptr, false, &nl));
-        ctx->launches += nl + (packed_chunk ? 1 : 0);
+                               ctx->num_sms, ctx->stream, ctx->tune, nullptr, false, &nb));
+        ctx->launches += nl + nb + unpack_launches;
         ME_CUDA(cudaEventRecord(ctx->ev_out[k], ctx->stream));
         ME_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_out[k], 0));
         ME_CUDA(cudaMemcpyAsync(recs + seq_recs * s0, dr + seq_recs * s0, seq_recs * ns * sizeof(me_block_rec),

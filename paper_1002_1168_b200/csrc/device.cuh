@@ -153,6 +153,20 @@ __device__ __forceinline__ uint32_t row_shape(const uint8_t* ca, const uint8_t* 
     return m;
 }
 
+// 8 mask bits of row y of a bit-packed plane (`wb` bytes per row) from pel x
+// on (bit 0 = pel x); pels x .. x+7 lie inside the row.
+__device__ __forceinline__ uint32_t mask_bits8(const uint8_t* bits, uint32_t wb, int x, int y) {
+    const uint8_t* r = bits + size_t(y) * wb + (x >> 3);
+    const uint32_t sh = uint32_t(x & 7);
+    const uint32_t lo = __ldg(r), hi = sh ? __ldg(r + 1) : 0u;
+    return ((lo | (hi << 8)) >> sh) & 0xFFu;
+}
+
+// 4 mask bits -> 4 bytes 0x00 / 0xFF (bit i -> byte i)
+__device__ __forceinline__ uint32_t mask_expand4(uint32_t nib) {
+    return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
 // Rounds 4*s/4 to nearest, ties to even (std::nearbyint, compensation.cpp:64).
 __device__ __forceinline__ int round_q4(int i4) {
     const int q = i4 >> 2, rem = i4 & 3;

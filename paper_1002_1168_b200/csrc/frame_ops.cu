@@ -62,6 +62,24 @@ __global__ void unpack_sparse_kernel(const uint32_t* __restrict__ pres, const ui
     }
 }
 
+// The same sparse form expanded to the dense bit plane (one 64-bit word per 64
+// pixels): the layout the classify and PA kernels read directly.
+__global__ void unpack_sparse_bits_kernel(const uint32_t* __restrict__ pres, const uint32_t* __restrict__ base,
+                                          const unsigned long long* __restrict__ lit, unsigned long long* __restrict__ out,
+                                          size_t nwords) {
+    const int lane = threadIdx.x & 31;
+    const size_t ngroups = (nwords + 31) / 32;
+    for (size_t gi = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; gi < ngroups;
+         gi += (size_t(gridDim.x) * blockDim.x) >> 5) {
+        const size_t w = gi * 32 + lane;
+        if (w >= nwords) continue;
+        const uint32_t m = __ldg(pres + gi);
+        unsigned long long x = 0;
+        if ((m >> lane) & 1u) x = __ldg(lit + __ldg(base + gi) + __popc(m & ((1u << lane) - 1u)));
+        out[w] = x;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // mc_kernel: predict_frame (compensation.cpp:30-71) fused with the psnr SSE
 // (metrics.cpp:108-124) and the per-pair SearchStats reduction.  One thread
@@ -268,6 +286,50 @@ cudaError_t unpack_mask_sparse(const uint8_t* packed, uint8_t* out, size_t n, cu
     const auto* lit = reinterpret_cast<const unsigned long long*>(packed + sparse_mask_header_bytes(n));
     const int grid = int(std::min<size_t>((ngroups * 32 + 255) / 256, 148 * 16));
     unpack_sparse_kernel<<<grid, 256, 0, st>>>(pres, base, lit, reinterpret_cast<uint4*>(out), nwords);
+    return cudaGetLastError();
+}
+
+// bytes -> bit plane (bit = byte != 0), 64 pixels per thread; *nonbinary
+// counts 64-pixel words holding a byte other than 0 / 255.
+__global__ void pack_mask_kernel(const uint4* __restrict__ in, unsigned long long* __restrict__ out, size_t nwords,
+                                 int* nonbinary) {
+    for (size_t w = size_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords; w += size_t(gridDim.x) * blockDim.x) {
+        unsigned long long x = 0;
+        uint32_t odd = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = __ldg(in + 4 * w + q);
+            const uint32_t vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t nz = __vcmpne4(vs[k], 0u);                     // 0xFF per nonzero byte
+                odd |= nz & __vcmpne4(vs[k], 0xFFFFFFFFu);                     // neither 0 nor 255
+                const uint32_t b4 = ((nz & 0x01010101u) * 0x01020408u) >> 24;  // byte k -> bit k
+                x |= (unsigned long long)(b4 & 15u) << (16 * q + 4 * k);
+            }
+        }
+        out[w] = x;
+        if (odd) atomicAdd(nonbinary, 1);
+    }
+}
+
+cudaError_t pack_mask_dev(const uint8_t* alpha, size_t n, uint8_t* bits, int* nonbinary, cudaStream_t st) {
+    if (n % 64) return cudaErrorInvalidValue;
+    const size_t nwords = n / 64;
+    const int grid = int(std::min<size_t>((nwords + 255) / 256, 148 * 16));
+    pack_mask_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(alpha), reinterpret_cast<unsigned long long*>(bits),
+                                           nwords, nonbinary);
+    return cudaGetLastError();
+}
+
+cudaError_t unpack_mask_sparse_bits(const uint8_t* packed, uint8_t* out_bits, size_t n, cudaStream_t st) {
+    if (n % 64) return cudaErrorInvalidValue;
+    const size_t nwords = n / 64, ngroups = (nwords + 31) / 32;
+    const uint32_t* pres = reinterpret_cast<const uint32_t*>(packed);
+    const uint32_t* base = pres + ngroups;
+    const auto* lit = reinterpret_cast<const unsigned long long*>(packed + sparse_mask_header_bytes(n));
+    const int grid = int(std::min<size_t>((ngroups * 32 + 255) / 256, 148 * 16));
+    unpack_sparse_bits_kernel<<<grid, 256, 0, st>>>(pres, base, lit, reinterpret_cast<unsigned long long*>(out_bits), nwords);
     return cudaGetLastError();
 }
 

@@ -15,6 +15,10 @@ namespace mek {
 struct Batch {
     const uint8_t* luma;   // [n_seq][F][H][W]
     const uint8_t* alpha;  // same shape, or null (all opaque)
+    // binary masks bit-packed instead ([n_seq][F][H][W / 8], bit i of byte j =
+    // pel 8j + i, set = inside): classify and the fast/quad PA kernels score
+    // shapes with popc(XOR) on these (alpha is null then)
+    const uint8_t* alpha_bits = nullptr;
     int n_seq, F, W, H, d, pairs, bs, cols, rows;
     // block-row band [v0, v1) of the baselines' row sharding (v1 < 0: every
     // row): blocks outside it are not estimated, their records are left
@@ -94,6 +98,14 @@ cudaError_t unpack_mask(const uint8_t* bits, uint8_t* out, size_t n, cudaStream_
 // words (uint64, bit i = pixel i); G = ceil(n / 64 / 32).
 inline size_t sparse_mask_header_bytes(size_t n) { return ((n / 64 + 31) / 32 * 8 + 15) & ~size_t(15); }
 cudaError_t unpack_mask_sparse(const uint8_t* packed, uint8_t* out, size_t n, cudaStream_t st);
+// Device bytes -> dense bit plane (n % 64 == 0); *nonbinary (device int,
+// zeroed by the caller) counts 64-pixel words with bytes other than 0 / 255.
+cudaError_t pack_mask_dev(const uint8_t* alpha, size_t n, uint8_t* bits, int* nonbinary, cudaStream_t st);
+// ... or to the dense bit plane (n / 8 bytes, the layout Batch::alpha_bits reads).
+cudaError_t unpack_mask_sparse_bits(const uint8_t* packed, uint8_t* out_bits, size_t n, cudaStream_t st);
+// PA on bit-packed masks: true when the batch's kernel schedule reads them
+// (pa_fast_kernel / the quad hybrid); otherwise they are expanded to bytes.
+bool pa_takes_bits(const Batch& b, const me_config& cfg, int num_sms, const Tuning& t);
 cudaError_t predict(const uint8_t* ref, const uint8_t* cur, const int32_t* mv, const uint8_t* types,
                     int W, int H, int bs, uint8_t* pred, me_pair_stats* stats,
                     cudaStream_t st);

@@ -72,7 +72,7 @@ struct me_ctx {
     // scratch for the batched pipeline
     DevBuf types, worklist, counters, tasks;
     // inputs/outputs of the host-pointer entry points
-    DevBuf in_luma, in_alpha, out_recs, out_stats, out_pred, aux;
+    DevBuf in_luma, in_alpha, in_bits, out_recs, out_stats, out_pred, aux;
     HostBuf pin_a, pin_b;
     // stage timing
     bool profiling = false;

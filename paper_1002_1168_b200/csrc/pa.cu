@@ -783,16 +783,25 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         }
         const bool shape = boundary && (c < 3 || a.P.bt_shape);
         uint2 cal = make_uint2(0u, 0u);
-        uint32_t ral0 = 0, ral1 = 0;
+        uint32_t ral0 = 0, ral1 = 0, xbits = 0;
         if (shape) {
-            const uint32_t ao = uint32_t(y0 + sub) * W + uint32_t(x0);
-            cal = __ldg(reinterpret_cast<const uint2*>(a.b.alpha + (ocur + ao)));
-            ld8u(a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1))), ral0, ral1);
+            if (a.b.alpha_bits) {  // popc(XOR) of the 8 mask bits of my row
+                const uint32_t wb = uint32_t(W) >> 3;
+                const uint8_t* cb = a.b.alpha_bits + (ocur >> 3);
+                const uint8_t* rb = a.b.alpha_bits + (oref >> 3);
+                xbits = mask_bits8(cb, wb, x0, y0 + sub) ^ mask_bits8(rb, wb, x0 + (myx >> 1), y0 + sub + (myy >> 1));
+            } else {
+                const uint32_t ao = uint32_t(y0 + sub) * W + uint32_t(x0);
+                cal = __ldg(reinterpret_cast<const uint2*>(a.b.alpha + (ocur + ao)));
+                ld8u(a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1))), ral0, ral1);
+            }
         }
         cp_async_wait_all();
         // shape scores (boundary blocks): my candidate, my row
         uint32_t s = 0;
-        if (shape) s = ((__popc(__vcmpne4(cal.x, ral0)) + __popc(__vcmpne4(cal.y, ral1))) >> 3) * (255u * 4u);
+        if (shape)
+            s = (a.b.alpha_bits ? __popc(xbits) : (__popc(__vcmpne4(cal.x, ral0)) + __popc(__vcmpne4(cal.y, ral1))) >> 3) *
+                (255u * 4u);
         __syncwarp();
         if (TRACE) c_patch = clock64();
         // --- brs_select (estimators.cpp:257-301) --------------------------------
@@ -1346,8 +1355,18 @@ __global__ void __launch_bounds__(256, MINB) pa_quad_kernel(const PaArgs a) {
             }
         }
         const bool shape = act && boundary && (c < 3 || a.P.bt_shape);
-        uint32_t sh_cnt = 0;
-        if (shape) {
+        uint32_t sh_cnt = 0;  // mismatching mask samples x 8
+        if (shape && a.b.alpha_bits) {  // bit-packed masks: popc(XOR) of 8-pel rows
+            const uint32_t wb = uint32_t(W) >> 3;
+            const uint8_t* cb = a.b.alpha_bits + (ocur >> 3);
+            const uint8_t* rb = a.b.alpha_bits + (oref >> 3);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int y = y0 + 4 * hh + r;
+                sh_cnt += __popc(mask_bits8(cb, wb, x0, y) ^ mask_bits8(rb, wb, x0 + (myx >> 1), y + (myy >> 1)));
+            }
+            sh_cnt <<= 3;
+        } else if (shape) {
             const uint32_t ao = uint32_t(y0 + 4 * hh) * W + uint32_t(x0);
             const uint8_t* cap = a.b.alpha + (ocur + ao);
             const uint8_t* rap = a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1)));
@@ -1936,6 +1955,11 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
     return per_step >= int64_t(num_sms) * 160 ? 4 : 1;
 }
 
+bool pa_takes_bits(const Batch& b, const me_config& cfg, int num_sms, const Tuning& t) {
+    const int mode = pa_kernel_mode(b, cfg, nullptr, false, num_sms, t);
+    return mode == 1 || mode == 4;
+}
+
 // One small pair in one CTA (pa_smem_kernel) when it fits in shared memory;
 // returns cudaErrorNotSupported when not eligible (the caller runs the
 // batched pipeline instead).
@@ -1944,7 +1968,7 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
     const int step = cfg.halfpel ? 1 : cfg.step;
     if (!(b.n_seq == 1 && b.pairs == 1 && b.bs == 8 && step == 2 && cfg.max_iterations <= 4 &&
           (!prev0 || prev0_integer) && (size_t(b.W) * b.H) % 16 == 0) ||
-        !t.pa_smem_pair)
+        !t.pa_smem_pair || b.alpha_bits)
         return cudaErrorNotSupported;
     const int plane_pad = b.W * b.H + 16;
     const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * 13 + 16;

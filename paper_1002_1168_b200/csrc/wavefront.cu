@@ -51,7 +51,7 @@ __device__ __forceinline__ uint32_t block_sse0(const uint8_t* cur, const uint8_t
 // fetched with 16-byte loads in a single round (the luma is loaded
 // speculatively — it is only needed for transparent blocks' zero-vector SSE,
 // and is the compulsory read of those frames anyway).
-template <int BS>
+template <int BS, bool BITS>
 __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
     extern __shared__ int s_hist[];
     pdl_allow_next();
@@ -86,16 +86,28 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             const size_t fcur = size_t(seq) * b.F + p + b.d, fref = size_t(seq) * b.F + p;
             const size_t off = size_t(v * BS) * b.W + size_t(hs) * 16;
             const uint8_t* ac = b.alpha ? b.alpha + fcur * plane + off : nullptr;
+            // bit-packed masks: the strip's 16 pels of a row are 2 bytes
+            const uint8_t* abits = BITS ? b.alpha_bits + (fcur * plane + off) / 8 : nullptr;
             const uint8_t* cc = b.luma + fcur * plane + off;
             const uint8_t* rc = b.luma + fref * plane + off;
             uint4 al[BS], cu[BS], re[BS];
+            uint32_t ab[BS];  // bit rows (all loads of the strip are issued before any is used)
 #pragma unroll
             for (int y = 0; y < BS; ++y) {
-                al[y] = ac ? __ldg(reinterpret_cast<const uint4*>(ac + size_t(y) * b.W)) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                if (BITS)
+                    ab[y] = __ldg(reinterpret_cast<const uint16_t*>(abits + size_t(y) * (b.W / 8)));
+                else
+                    al[y] = ac ? __ldg(reinterpret_cast<const uint4*>(ac + size_t(y) * b.W)) : make_uint4(~0u, ~0u, ~0u, ~0u);
                 if (a.stats) {
                     cu[y] = __ldg(reinterpret_cast<const uint4*>(cc + size_t(y) * b.W));
                     re[y] = __ldg(reinterpret_cast<const uint4*>(rc + size_t(y) * b.W));
                 }
+            }
+            if (BITS) {
+#pragma unroll
+                for (int y = 0; y < BS; ++y)
+                    al[y] = make_uint4(mask_expand4(ab[y] & 15u), mask_expand4((ab[y] >> 4) & 15u),
+                                       mask_expand4((ab[y] >> 8) & 15u), mask_expand4(ab[y] >> 12));
             }
 #pragma unroll
             for (int k = 0; k < NB; ++k) {
@@ -395,10 +407,11 @@ cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
     int grid = int(std::min<int64_t>((strips + threads - 1) / threads, int64_t(num_sms) * 8));
     if (grid < 1) grid = 1;
     const size_t hist_smem = size_t(ca.nbins) * 4;
+    const bool bits = b.alpha_bits != nullptr;
     if (b.bs == 8)
-        classify_kernel<8><<<grid, threads, hist_smem, st>>>(ca);
+        (bits ? classify_kernel<8, true> : classify_kernel<8, false>)<<<grid, threads, hist_smem, st>>>(ca);
     else
-        classify_kernel<16><<<grid, threads, hist_smem, st>>>(ca);
+        (bits ? classify_kernel<16, true> : classify_kernel<16, false>)<<<grid, threads, hist_smem, st>>>(ca);
     return cudaGetLastError();
 }
 

@@ -557,3 +557,65 @@ def test_concurrent_large_batches(me_gpu, port):
             want_r, want_s = port.run_sequence(c, luma[i], alpha[i])
             assert_recs(out[k][0][i], want_r, f"batch {k} seq {i}")
             assert np.array_equal(out[k][1][i], want_s)
+
+
+# ---------------------------------------------------------------------------
+# Bit-packed binary masks (north star: BAB shape matching with popc(XOR))
+
+
+@pytest.mark.parametrize("mode", ["auto", "fast", "hybrid", "warp", "duo"])
+def test_pa_bit_packed_masks(me_gpu, port, mode, tuning):
+    """PA with the masks as device bit planes equals the byte-mask path and
+    the oracle, under every schedule (fast / quad read the bits; the others
+    get them expanded)."""
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import synth
+
+    tuning(pa_schedule=mode, pa_wide_blocks=4)
+    luma, alpha = synth.config4_batch(4, 810, frames=6)
+    lt, at = torch.from_numpy(luma).cuda(), torch.from_numpy(alpha).cuda()
+    bits, binary = B.pack_mask_dev(at)
+    assert binary
+    assert np.array_equal(bits.cpu().numpy(), np.packbits(alpha != 0, axis=-1, bitorder="little"))
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    r_bits, s_bits = B.run_sequences_bits_dev(cfg, lt, bits)
+    r_byte, s_byte = B.run_sequences_dev(cfg, lt, at)
+    torch.cuda.synchronize()
+    assert torch.equal(r_bits, r_byte) and torch.equal(s_bits, s_byte)
+    got = r_bits.cpu().numpy().view(_lib_rec_dtype()).reshape(r_bits.shape[:4])
+    for i in (0, 3):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
+        assert_recs(got[i], want_r, f"{mode} seq {i}")
+
+
+@pytest.mark.parametrize("algo,bs", [(0, 16), (1, 16), (3, 8), (4, 16)])
+def test_bit_packed_masks_other_algos(me_gpu, port, algo, bs):
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config_sequence(2, 83, 5)
+    lt, at = torch.from_numpy(luma[None].copy()).cuda(), torch.from_numpy(alpha[None].copy()).cuda()
+    bits, binary = B.pack_mask_dev(at)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=16, block_size=bs))
+    r, s = B.run_sequences_bits_dev(cfg, lt, bits)
+    want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=bs), luma, alpha)
+    assert_recs(r[0].cpu().numpy().view(_lib_rec_dtype()).reshape(want_r.shape), want_r)
+    assert np.array_equal(s[0].cpu().numpy().view(_lib_stats_dtype()).reshape(-1), want_s)
+
+
+def test_pack_mask_dev_detects_non_binary(me_gpu):
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+
+    a = torch.zeros((2, 64, 64), dtype=torch.uint8, device="cuda")
+    a[0, 10:20, 5:40] = 255
+    assert B.pack_mask_dev(a)[1]
+    a[1, 3, 3] = 100
+    bits, binary = B.pack_mask_dev(a)
+    assert not binary
+    assert np.array_equal(bits.cpu().numpy(), np.packbits(a.cpu().numpy() != 0, axis=-1, bitorder="little"))
