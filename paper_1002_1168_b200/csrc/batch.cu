@@ -86,6 +86,7 @@ Tuning resolve_tuning(const me_tuning* u) {
     if (u->fill_rows_per_cta) t.fill_rows_per_cta = u->fill_rows_per_cta;
     if (u->h2d_chunks) t.h2d_chunks = u->h2d_chunks;
     if (u->mask_pack) t.mask_pack = u->mask_pack;
+    if (u->ring_ctas) t.ring_ctas = u->ring_ctas;
     t.pa_trace = u->pa_trace_path;
     return t;
 }
@@ -171,7 +172,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     else if (algo == ME_ALGO_PA)
         e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st, s.counter + 1, tune);
     else
-        e = launch_ring(b, algo, cfg.search_range, s.list, nlist, recs, stats, num_sms, st);
+        e = launch_ring(b, algo, cfg.search_range, s.list, nlist, recs, stats, num_sms, st, tune.ring_ctas);
     if (e) return e;
 
     if (events) cudaEventRecord(events[3], st);

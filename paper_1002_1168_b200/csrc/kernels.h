@@ -48,6 +48,7 @@ struct Tuning {
     int fill_rows_per_cta = 64;
     int h2d_chunks = 16;
     int mask_pack = 3;       // 1 bytes, 2 dense bits, 3 sparse bits
+    int ring_ctas = 3;       // CTAs per SM of ring_kernel (3: 80 registers, no spills)
     const char* pa_trace = nullptr;
 };
 Tuning resolve_tuning(const me_tuning* t);

@@ -246,7 +246,8 @@ struct RingArgs {
     me_pair_stats* stats;
 };
 
-__global__ void __launch_bounds__(256, 4) ring_kernel(RingArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) ring_kernel(RingArgs a) {
     extern __shared__ __align__(16) uint32_t s_bits[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t* bitmap = s_bits + wid * a.warp_words;
@@ -301,7 +302,7 @@ __global__ void ring_single_kernel(int algo, const uint8_t* cur, const uint8_t* 
 static int ring_warp_words(int WX, int WY) { return (((WX * WY + 31) / 32 + 3) & ~3) + kStageWords; }
 
 cudaError_t launch_ring(const Batch& b, int algo, int S, const uint2* list, const int* nlist,
-                        me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st) {
+                        me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st, int ctas) {
     RingArgs ra;
     ra.b = b;
     ra.algo = algo;
@@ -317,10 +318,12 @@ cudaError_t launch_ring(const Batch& b, int algo, int S, const uint2* list, cons
     while (warps > 1 && size_t(warps) * ra.warp_words * 4 > 160 * 1024) warps >>= 1;
     const size_t smem = size_t(warps) * ra.warp_words * 4;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+    // register budget: 4 CTAs per SM (64 registers) or 3 (80, no spills)
+    void (*kern)(RingArgs) = ctas == 4 ? ring_kernel<4> : ctas == 2 ? ring_kernel<2> : ring_kernel<3>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ring_kernel, warps * 32, smem);
-    ring_kernel<<<num_sms * (occ > 0 ? occ : 1), warps * 32, smem, st>>>(ra);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
+    kern<<<num_sms * (occ > 0 ? occ : 1), warps * 32, smem, st>>>(ra);
     return cudaGetLastError();
 }
 

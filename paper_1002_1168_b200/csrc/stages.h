@@ -46,7 +46,7 @@ cudaError_t launch_es_single(const uint8_t* cur, const uint8_t* ref, int W, int 
 
 // ring.cu: TSS / FSS / DS over the list; single-block ring search
 cudaError_t launch_ring(const Batch& b, int algo, int S, const uint2* list, const int* nlist,
-                        me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st);
+                        me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st, int ctas);
 cudaError_t launch_ring_single(int algo, const uint8_t* cur, const uint8_t* ref, int W, int H,
                                int x0, int y0, int size, int range, int64_t* out, cudaStream_t st);
 
