@@ -280,8 +280,9 @@ void me_b200_ctx_destroy(me_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (auto& e : c->ev)
-        if (e) cudaEventDestroy(e);
+    for (auto& set : c->ev)
+        for (auto& e : set)
+            if (e) cudaEventDestroy(e);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamSynchronize(c->d2h_stream);
@@ -332,8 +333,6 @@ me_status me_b200_ctx_get_tuning(me_ctx* ctx, me_tuning* out) {
 me_status me_b200_ctx_set_profiling(me_ctx* ctx, int enable) {
     me_status s = check_ctx(ctx);
     if (s) return s;
-    if (enable && !ctx->ev[0])
-        for (auto& e : ctx->ev) ME_CUDA(cudaEventCreate(&e));
     ctx->profiling = enable != 0;
     ctx->ev_valid = false;
     return ok();
@@ -371,9 +370,15 @@ me_status me_b200_ctx_stage_ms(me_ctx* ctx, float* out, int n) {
     if (s) return s;
     if (!ctx->profiling || !ctx->ev_valid)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "no profiled run on this context");
-    ME_CUDA(cudaEventSynchronize(ctx->ev[4]));
-    for (int i = 0; i < n && i < ME_NUM_STAGES; ++i)
-        ME_CUDA(cudaEventElapsedTime(&out[i], ctx->ev[i], ctx->ev[i + 1]));
+    for (int i = 0; i < n && i < ME_NUM_STAGES; ++i) out[i] = 0.f;
+    for (int k = 0; k < ctx->ev_sets; ++k) {  // every sub-batch of the last call
+        ME_CUDA(cudaEventSynchronize(ctx->ev[k][4]));
+        for (int i = 0; i < n && i < ME_NUM_STAGES; ++i) {
+            float ms = 0.f;
+            ME_CUDA(cudaEventElapsedTime(&ms, ctx->ev[k][i], ctx->ev[k][i + 1]));
+            out[i] += ms;
+        }
+    }
     return ok();
 }
 
@@ -441,6 +446,7 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
     const int pairs = n_frames - cfg->ref_distance;
     const size_t seq_recs = size_t(pairs) * (W / cfg->block_size) * (H / cfg->block_size);
     ctx->launches = 0;
+    ctx->ev_sets = 0;
     for (int s0 = 0; s0 < n_seq; s0 += per) {
         const int ns = std::min(per, n_seq - s0);
         const mek::Batch b = make_batch(cfg, ns, n_frames, W, H, luma + seq_bytes * s0,
@@ -449,7 +455,7 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
         int nl = 0;
         ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs + seq_recs * s0, stats + size_t(pairs) * s0,
                                pred ? pred + size_t(W) * H * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
-                               ctx->num_sms, st, ctx->tune, ctx->events(), false, &nl));
+                               ctx->num_sms, st, ctx->tune, ctx->events(s0 / per), false, &nl));
         ctx->launches += nl;
     }
     ctx->ev_valid = ctx->profiling;
@@ -473,6 +479,7 @@ me_status me_b200_run_sequences_bits_dev(me_ctx* ctx, const me_config* cfg, int 
     const int pairs = n_frames - cfg->ref_distance;
     const size_t seq_recs = size_t(pairs) * (W / cfg->block_size) * (H / cfg->block_size);
     ctx->launches = 0;
+    ctx->ev_sets = 0;
     for (int s0 = 0; s0 < n_seq; s0 += per) {
         const int ns = std::min(per, n_seq - s0);
         mek::Batch b = make_batch(cfg, ns, n_frames, W, H, luma + seq_bytes * s0, nullptr);
@@ -489,7 +496,7 @@ me_status me_b200_run_sequences_bits_dev(me_ctx* ctx, const me_config* cfg, int 
         int nl = 0;
         ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs + seq_recs * s0, stats + size_t(pairs) * s0,
                                pred ? pred + size_t(W) * H * pairs * s0 : nullptr, ctx->tasks.p, ctx->tasks.cap,
-                               ctx->num_sms, st, ctx->tune, ctx->events(), false, &nl));
+                               ctx->num_sms, st, ctx->tune, ctx->events(s0 / per), false, &nl));
         ctx->launches += nl;
     }
     ctx->ev_valid = ctx->profiling;
@@ -533,7 +540,7 @@ me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int
     ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
     int nl = 0;
     ME_CUDA(mek::run_batch(b, *cfg, nullptr, recs, stats, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
-                           st, ctx->tune, ctx->events(), false, &nl));
+                           st, ctx->tune, (ctx->ev_sets = 0, ctx->events()), false, &nl));
     ctx->launches = nl;
     ctx->ev_valid = ctx->profiling;
     return ok();
@@ -786,7 +793,7 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
     me_pair_stats* ds = reinterpret_cast<me_pair_stats*>(dr + size_t(cols) * rows);
     int nl = 0;
     ME_CUDA(mek::run_batch(b, c1, prev_dev, dr, ds, nullptr, ctx->tasks.p, ctx->tasks.cap, ctx->num_sms,
-                           ctx->stream, ctx->tune, ctx->events(), prev_integer, &nl));
+                           ctx->stream, ctx->tune, (ctx->ev_sets = 0, ctx->events()), prev_integer, &nl));
     ctx->launches = nl;
     ctx->ev_valid = ctx->profiling;
     ME_CUDA(cudaMemcpyAsync(ctx->pin_b.p, dr, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -76,9 +76,20 @@ struct me_ctx {
     HostBuf pin_a, pin_b;
     // stage timing
     bool profiling = false;
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    // one set of 5 stage events per sub-batch of the last call (a batch
+    // spanning 4 GiB runs as several); me_b200_ctx_stage_ms sums them
+    std::vector<std::vector<cudaEvent_t>> ev;
+    int ev_sets = 0;
     bool ev_valid = false;
-    cudaEvent_t* events() { return profiling ? ev : nullptr; }
+    cudaEvent_t* events(int set = 0) {
+        if (!profiling) return nullptr;
+        while (int(ev.size()) <= set) {
+            ev.emplace_back(5, nullptr);
+            for (auto& e : ev.back()) cudaEventCreate(&e);
+        }
+        ev_sets = set + 1;
+        return ev[set].data();
+    }
     // host-pointer pipeline: H2D / D2H streams and per-chunk events
     cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_in[32] = {}, ev_out[32] = {};

@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report into a small text file for profiles/:
 key throughput/occupancy/memory metrics, warp-stall breakdown and the hottest
-SASS instructions (stall samples).  usage: ncu_summary.py REPORT.ncu-rep OUT.txt"""
+SASS instructions (stall samples).  usage: ncu_summary.py REPORT.ncu-rep OUT.txt [KERNEL_REGEX]"""
 import csv
 import io
 import subprocess
@@ -24,8 +24,9 @@ def ncu(args):
     return subprocess.run(["ncu"] + args, capture_output=True, text=True, check=True).stdout
 
 
-def main(rep, out):
-    raw = list(csv.reader(io.StringIO(ncu(["-i", rep, "--page", "raw", "--csv"]))))
+def main(rep, out, kernel=None):
+    filt = ["-k", "regex:" + kernel] if kernel else []
+    raw = list(csv.reader(io.StringIO(ncu(["-i", rep, "--page", "raw", "--csv"] + filt))))
     h, u, v = raw[0], raw[1], raw[2]
     lines = ["# ncu --set full summary of %s" % rep.split("/")[-1], "# kernel: %s" % v[h.index("Kernel Name")], ""]
     for k in KEYS:
@@ -42,10 +43,15 @@ def main(rep, out):
                 pass
     for val, n in sorted(st, reverse=True)[:10]:
         lines.append("  %-28s %.2f" % (n, val))
-    src = list(csv.reader(io.StringIO(ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "sass"]))))
-    hh = src[1]
+    src = list(csv.reader(io.StringIO(ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + filt))))
+    hi = next(i for i, r in enumerate(src) if r and r[0] == "Address")  # the first kernel's table
+    hh = src[hi]
     iE, iS = hh.index("Instructions Executed"), hh.index("Warp Stall Sampling (All Samples)")
-    data = src[2:]
+    data = []
+    for r in src[hi + 1:]:
+        if not r or r[0] == "Kernel Name":
+            break
+        data.append(r)
     tot = sum(int(r[iS]) for r in data) or 1
     totE = sum(int(r[iE]) for r in data)
     lines += ["", "# hottest SASS (stall samples, share, executions); total samples %d, executed %d" % (tot, totE)]
@@ -56,4 +62,4 @@ def main(rep, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
