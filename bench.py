@@ -565,6 +565,53 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
 # ES on config 5 (the INT-pipe headline), sharded by (pair, row band) units
 
 
+def bench_critical_path(args, local, dev):
+    """PA on the single-sequence configs 1, 2, 3 and 5 (BASELINE.md section 3:
+    critical-path bound, not HBM): per configuration the wavefront length
+    (steps t = h + 2v + p) and the measured time per step of the search."""
+    import torch
+
+    from paper_1002_1168_b200 import _lib
+    from paper_1002_1168_b200 import batch as B
+    from paper_1002_1168_b200 import synth
+    import ctypes as C
+
+    import paper_1002_1168_b200 as me
+
+    lib, ctxh = me.lib(), _lib.ctx(local)
+    stage = (C.c_float * 4)()
+    out = {}
+    for cid, S in ((1, 16), (2, 16), (3, 32), (5, 64)):
+        F = {1: 10, 2: 30, 3: 60, 5: 30}[cid]
+        luma, alpha = synth.config4_batch_dev(1, BASE_SEED, F, config_id=cid, device=local)
+        cfg = me_config("PA", 8, S)
+        H, W = luma.shape[2], luma.shape[3]
+        cols, rows, pairs = W // 8, H // 8, F - 2
+        steps = (cols - 1) + 2 * (rows - 1) + (pairs - 1) + 1
+        recs = torch.empty((1, pairs, rows, cols, 16), dtype=torch.uint8, device=dev)
+        stats = torch.empty((1, pairs, 48), dtype=torch.uint8, device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        for _ in range(3):
+            B.run_sequences_dev(cfg, luma, alpha, recs, stats, device=local)
+        _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
+        tot, search, n = 0.0, 0.0, 10
+        for _ in range(n):
+            flush.fill_(1)  # L2 flushed between runs
+            B.run_sequences_dev(cfg, luma, alpha, recs, stats, device=local)
+            _lib.check(lib.me_b200_ctx_stage_ms(ctxh, stage, 4))
+            tot += sum(stage[:4])
+            search += stage[2]
+        _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 0))
+        tot, search = tot / n, search / n
+        est = int(((recs[..., 13] != 0)).sum().item())  # type byte: opaque / boundary
+        out[f"cfg{cid}"] = {"geometry": f"{W}x{H} x {F}f, S={S}, 8x8 blocks", "wavefront_steps": steps, "estimated_blocks": est,
+                            "pipeline_ms": tot, "search_ms": search, "us_per_step": 1e3 * search / steps,
+                            "macroblocks_per_s": pairs * (W // 16) * (H // 16) / (tot / 1e3)}
+        del luma, alpha, recs, stats, flush
+    torch.cuda.empty_cache()
+    return {"model": "search time = wavefront steps x per-step latency (pa_fast_kernel, one CTA per SM; CUDA events, L2 flushed)", **out}
+
+
 def bench_es_cfg5(args, world, rank, local, dev):
     import torch
     import torch.distributed as dist
@@ -584,7 +631,7 @@ def bench_es_cfg5(args, world, rank, local, dev):
     _, _, H, W = luma.shape
     rows, cols = H // bs, W // bs
     cfg = me_config(algo, bs, S)
-    n_bands = 1 if world == 1 else 4
+    n_bands = args.es_bands or (1 if world == 1 else 4)
     units = mdist.band_units(alpha[0], bs, pairs, d, n_bands)
     mine = mdist.split_units(units, world)[rank]
     runs = mdist.unit_runs(mine)
@@ -601,7 +648,7 @@ def bench_es_cfg5(args, world, rank, local, dev):
             n = p1 - p0
             lv, av = luma[:, p0:p1 + d], alpha[:, p0:p1 + d]
             rv, sv = recs[:, p0:p1], tmp_stats[:, :n]
-            if world == 1:
+            if n_bands == 1:
                 B.run_sequences_dev(cfg, lv, av, rv, sv, device=local, stream=stream.cuda_stream)
             else:
                 B.run_band_dev(cfg, lv, av, r0, r1, rv, sv, device=local, stream=stream.cuda_stream)
@@ -636,7 +683,7 @@ def bench_es_cfg5(args, world, rank, local, dev):
     for b, p0, p1, r0, r1 in runs:
         n = p1 - p0
         lv, av = luma[:, p0:p1 + d], alpha[:, p0:p1 + d]
-        if world == 1:
+        if n_bands == 1:
             B.run_sequences_dev(cfg, lv, av, recs[:, p0:p1], tmp_stats[:, :n], device=local, stream=stream.cuda_stream)
         else:
             B.run_band_dev(cfg, lv, av, r0, r1, recs[:, p0:p1], tmp_stats[:, :n], device=local, stream=stream.cuda_stream)
@@ -721,8 +768,10 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-es", action="store_true", help="skip the es_cfg5 leg of the default run")
     ap.add_argument("--no-bits", action="store_true", help="skip the bit-packed-mask layout leg")
+    ap.add_argument("--no-critical", action="store_true", help="skip the single-sequence critical-path leg")
     ap.add_argument("--es-steps", type=int, default=5)
     ap.add_argument("--es-frames", type=int, default=0)
+    ap.add_argument("--es-bands", type=int, default=0, help="ES block-row bands per pair (default 1 on one GPU, 4 on several)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     args = ap.parse_args()
     wl = args.workload
@@ -755,6 +804,8 @@ def main():
                     "cpu_baseline": es["cpu_baseline"], "e2e": None, "clocks": es["clocks"], "parity": es["parity"]}
         else:
             line["es_cfg5"] = es
+            if wl == "cfg4-pa" and not args.no_critical and world == 1:
+                line["critical_path"] = bench_critical_path(args, local, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
