@@ -1,3 +1,4 @@
+# quad-kernel DRAM traffic and L2 hit rate vs batch size (the L2 working-set measurement in DESIGN.md)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/l2
 for n in 64 128 256; do

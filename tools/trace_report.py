@@ -1,4 +1,5 @@
-"""Analyse a PA wavefront trace (ME_PA_TRACE=file): per list entry
+"""Analyse a PA wavefront trace (tuning field pa_trace_path, set with
+paper_1002_1168_b200._lib.set_tuning(pa_trace_path=...)): per list entry
 {claim, deps ready, done, smid} (globaltimer ns) followed by the list.
 usage: trace_report.py TRACE.bin COLS ROWS PAIRS"""
 import sys
