@@ -5,7 +5,8 @@
  * function cites the reference file:line it restates (paths relative to
  * /root/reference/proj).  It is the checker for the CUDA product path and the
  * "port" CPU baseline; it is never linked into libme_b200.so.  Pinned against
- * the unmodified reference (oracle/_ref) by tests/test_oracle_pin.py.
+ * the unmodified reference (oracle/_ref) by tests/test_oracle_vs_ref.py (live)
+ * and tests/test_golden.py (reference-made vectors, tools/make_golden.py).
  *
  * Floating point follows the reference's build (x86-64 SSE2 doubles, no FMA
  * contraction; this file is compiled with -ffp-contract=off).

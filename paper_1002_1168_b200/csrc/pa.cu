@@ -1952,7 +1952,9 @@ int pa_kernel_mode(const Batch& b, const me_config& cfg, const int32_t* prev0, b
     if (sched == ME_PA_SCHED_DUO_HYBRID) return 3;
     if (sched == ME_PA_SCHED_QUAD_HYBRID) return 4;
     const int64_t per_step = b.nblocks() / std::max(1, b.steps());
-    return per_step >= int64_t(num_sms) * 160 ? 4 : 1;
+    // measured on CIF batches (tools/pa_schedule_probe.py): the quad hybrid
+    // from ~60 sequences on (120 blocks per step per SM), fast below
+    return per_step >= int64_t(num_sms) * 120 ? 4 : 1;
 }
 
 bool pa_takes_bits(const Batch& b, const me_config& cfg, int num_sms, const Tuning& t) {
@@ -2053,13 +2055,17 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     };
     PaKernel fast = pa_fast_kernel<4>;
     {
-        // narrow wavefronts (< 100 blocks per step per SM, e.g. single
-        // sequences and batches up to ~32 CIF sequences) are latency-bound:
-        // one CTA per SM with 128 registers per thread runs each block sooner
-        // (measured 3-6 % on configs 2, 3, 5 and 4-32 sequences); wider ones
-        // need the blocks in flight of 4 CTAs per SM
+        // a single sequence is latency-bound: one CTA per SM with 128
+        // registers per thread runs each block sooner (measured 3-6 % on
+        // configs 2, 3, 5); small batches (< 80 blocks per step per SM, up to
+        // ~36 CIF sequences) need more blocks in flight: 2 CTAs (measured
+        // 4-25 % better than 1 or 4 at 8-32 sequences); wider ones 4 (the
+        // hybrid's head and tail)
         const int64_t per_step = b.nblocks() / std::max(1, b.steps());
-        const int mb = t.pa_fast_ctas > 0 ? t.pa_fast_ctas : (pa_mode == 1 && per_step < int64_t(num_sms) * 100 ? 1 : 4);
+        const int mb = t.pa_fast_ctas > 0 ? t.pa_fast_ctas
+                       : pa_mode != 1      ? 4
+                       : b.n_seq == 1      ? 1
+                       : per_step < int64_t(num_sms) * 80 ? 2 : 4;
         fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         if (trace_path) fast = pa_fast_kernel<4, true>;
     }
