@@ -77,7 +77,7 @@ typedef struct me_config {
 typedef struct me_block_rec {
     int16_t dx, dy;          /* half-pel vector (MotionField::vectors) */
     uint32_t cost_q4;        /* 4 x SAD at (dx, dy) */
-    uint16_t comparisons;    /* this block's share of SearchStats::block_comparisons */
+    uint16_t comparisons;    /* this block's share of SearchStats::block_comparisons (saturates at 65535) */
     uint16_t dpd_steps;      /* this block's share of SearchStats::dpd_refinement_steps */
     uint8_t iterations;      /* PRS recenters (descent_log size - 1); 0 for the baselines */
     uint8_t type;            /* me_block_type (MotionField::types) */

@@ -482,7 +482,7 @@ int orc_estimate_field(const me_config* c, int w, int h, const uint8_t* cur, con
                 int64_t cmp;
                 uint32_t cq;
                 orc_block_search(c->algo, w, h, cur, ref, x0, y0, bs, c->search_range, mv, &cmp, &cq);
-                r->comparisons = (uint16_t)cmp;
+                r->comparisons = (uint16_t)(cmp > 65535 ? 65535 : cmp); /* saturated (ES at S >= 128) */
                 r->cost_q4 = cq;
                 st->block_comparisons += cmp;
             } else {

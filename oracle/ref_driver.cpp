@@ -21,6 +21,7 @@
 // Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline
 // legs load this library.
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -132,7 +133,7 @@ int run_pair(const me_config* c, const Frame& cur, const Frame& ref, const Alpha
         }
         r.dx = int16_t(v.dx);
         r.dy = int16_t(v.dy);
-        r.comparisons = uint16_t(bs.block_comparisons);
+        r.comparisons = uint16_t(std::min<std::int64_t>(bs.block_comparisons, 65535));  // saturated (ES at S >= 128)
         r.dpd_steps = uint16_t(bs.dpd_refinement_steps);
         r.iterations = algo == Algo::PA ? uint8_t(log.size() - 1) : 0;
         r.cost_q4 = algo == Algo::PA ? q4(log.back()) : q4(sad_texture(cur, ref, rect, v));

@@ -619,3 +619,59 @@ def test_pack_mask_dev_detects_non_binary(me_gpu):
     bits, binary = B.pack_mask_dev(a)
     assert not binary
     assert np.array_equal(bits.cpu().numpy(), np.packbits(a.cpu().numpy() != 0, axis=-1, bitorder="little"))
+
+
+# ---------------------------------------------------------------------------
+# Large search ranges (the ES tie-break key and the 16-bit record
+# count at S >= 128) and the S <= 255 implementation limit
+
+
+@pytest.mark.parametrize("S", [127, 128, 200, 255])
+@pytest.mark.parametrize("algo", [0, 3])
+def test_large_search_range(me_gpu, port, S, algo):
+    """ES / DS at S >= 128 on a 544 x 528 frame: MVs and the exact comparison
+    count (ES window area up to 511^2 > 65535) match the oracle.  Smooth,
+    tie-prone content so the Manhattan tie-break (|dx| + |dy| up to 2S, 9
+    bits of the key) decides."""
+    rng = np.random.default_rng(S + algo)
+    base = np.convolve(noise(rng, 528, 560).ravel(), np.ones(15) / 15, "same").reshape(528, 560)
+    cur = (base[:, :544] // 16 * 16).astype(np.uint8)
+    ref = np.ascontiguousarray(shift_clamped(cur, 9, -5))
+    cur = np.ascontiguousarray(cur)
+    for x0, y0 in ((0, 0), (256, 256), (528, 512), (272, 16)):
+        st = me_gpu.SearchStats()
+        fn = me_gpu.full_search if algo == 0 else me_gpu.ds_search
+        mv = fn(cur, ref, me_gpu.BlockRect(x0, y0, 16), me_gpu.SearchConfig(search_range=S, block_size=16), st)
+        want_mv, want_cmp, _ = port.block_search(algo, cur, ref, x0, y0, 16, S)
+        assert mv == tuple(want_mv) and st.block_comparisons == want_cmp, (S, x0, y0)
+
+
+def test_search_range_limit(me_gpu):
+    rng = np.random.default_rng(3)
+    cur = noise(rng, 64, 64)
+    with pytest.raises(ValueError):
+        me_gpu.full_search(cur, cur, me_gpu.BlockRect(0, 0, 16), me_gpu.SearchConfig(search_range=256, block_size=16), me_gpu.SearchStats())
+
+
+def test_es_batch_large_range_records(me_gpu, port):
+    """The batched ES path at S = 160: records (comparisons saturate at
+    65535 in the 16-bit field) and the exact int64 per-pair stats."""
+    import torch
+
+    from paper_1002_1168_b200 import batch as B
+
+    rng = np.random.default_rng(160)
+    base = np.convolve(noise(rng, 352, 352).ravel(), np.ones(7) / 7, "same").reshape(352, 352).astype(np.uint8)
+    luma = np.stack([base, shift_clamped(base, 2, 1), shift_clamped(base, 40, -33)])
+    alpha = np.zeros_like(luma)
+    alpha[:, 96:224, 64:288] = 255
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.ES, search=me_gpu.SearchConfig(search_range=160, block_size=16, ref_distance=2))
+    r, s = B.run_sequences_dev(cfg, torch.from_numpy(luma[None].copy()).cuda(), torch.from_numpy(alpha[None].copy()).cuda())
+    got_r = r[0].cpu().numpy().view(_lib_rec_dtype()).reshape(1, 22, 22)
+    got_s = s[0].cpu().numpy().view(_lib_stats_dtype()).reshape(-1)
+    want_r, want_s = port.run_sequence(oracle.make_cfg(algo=0, search_range=160, block_size=16), luma, alpha)
+    assert np.array_equal(got_s, want_s)
+    for f in ("dx", "dy", "cost_q4", "type"):
+        assert np.array_equal(got_r[f], want_r[f]), f
+    assert np.array_equal(got_r["comparisons"], want_r["comparisons"])  # both saturate at 65535
+    assert got_r["comparisons"].max() == 65535
