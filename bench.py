@@ -389,6 +389,10 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
     bits_layout = None
     if algo == "PA" and not args.no_bits:
         bits, binary = B.pack_mask_dev(alpha, device=local)
+        if world > 1:  # every rank takes the same branch (collectives inside)
+            flag = torch.tensor([1 if binary else 0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            binary = bool(flag.item())
         if binary:
             recs_b = torch.empty_like(recs)
             stats_b = torch.empty_like(stats)
