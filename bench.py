@@ -390,7 +390,7 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
     if algo == "PA" and not args.no_bits:
         bits, binary = B.pack_mask_dev(alpha, device=local)
         if world > 1:  # every rank takes the same branch (collectives inside)
-            flag = torch.tensor([1 if binary else 0], device=dev)
+            flag = torch.tensor([1 if binary else 0], device=mdist.coll_device(dev))
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
             binary = bool(flag.item())
         if binary:
@@ -658,11 +658,13 @@ def bench_es_cfg5(args, world, rank, local, dev):
                 B.run_band_dev(cfg, lv, av, r0, r1, rv, sv, device=local, stream=stream.cuda_stream)
             stats_acc[p0:p1] += sv[0].view(torch.int64).view(n, 6)
         if world > 1:  # MV words of my units + my partial stats -> rank 0
-            mvw = mdist.mv_words(recs[0])
+            cd = mdist.coll_device(dev)
+            mvw = mdist.mv_words(recs[0]).to(cd)
+            sacc = stats_acc.to(cd)
             outs = [torch.empty_like(mvw) for _ in range(world)] if rank == 0 else None
-            sts = [torch.empty_like(stats_acc) for _ in range(world)] if rank == 0 else None
+            sts = [torch.empty_like(sacc) for _ in range(world)] if rank == 0 else None
             dist.gather(mvw, outs, dst=0)
-            dist.gather(stats_acc, sts, dst=0)
+            dist.gather(sacc, sts, dst=0)
             return outs, sts
         return None, None
 
@@ -777,6 +779,8 @@ def main():
     ap.add_argument("--es-frames", type=int, default=0)
     ap.add_argument("--es-bands", type=int, default=0, help="ES block-row bands per pair (default 1 on one GPU, 4 on several)")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help="gloo: host collectives (tests)")
+    ap.add_argument("--same-device", action="store_true", help="test switch: every rank uses cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
     wl = args.workload
     if args.impl == "reference":
@@ -792,10 +796,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    if args.same_device:  # test switch: every rank on cuda:0 (gloo collectives through the host)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     line = bench_pa_batch(args, wl, world, rank, local, dev) if wl != "cfg5-es" else None
     es = None
     if wl == "cfg5-es" or (wl == "cfg4-pa" and not args.no_es):

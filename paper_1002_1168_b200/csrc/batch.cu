@@ -87,6 +87,7 @@ Tuning resolve_tuning(const me_tuning* u) {
     if (u->h2d_chunks) t.h2d_chunks = u->h2d_chunks;
     if (u->mask_pack) t.mask_pack = u->mask_pack;
     if (u->ring_ctas) t.ring_ctas = u->ring_ctas;
+    t.host_threads = u->host_threads;
     t.pa_trace = u->pa_trace_path;
     return t;
 }

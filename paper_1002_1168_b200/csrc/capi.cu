@@ -148,11 +148,12 @@ int pack_range_scalar(const uint8_t* src, int64_t w0, int64_t w1, uint8_t* dst) 
 // overlaps).  Returns false when some byte is neither 0 nor 255: such a mask
 // is not binary and is shipped as bytes (the shape SAD compares byte values,
 // so packing would not be exact).
-bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst) {
+bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst, int threads) {
     static const bool avx512 = __builtin_cpu_supports("avx512bw");
     const int64_t nw = int64_t(n / 8), nb = avx512 ? nw / 8 : 0;  // 8-byte words, 64-byte blocks
     int bad = 0;
-#pragma omp parallel reduction(| : bad)
+    const int nth = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel reduction(| : bad) num_threads(nth)
     {
         const int t = omp_get_thread_num(), nt = omp_get_num_threads();
         if (nb) bad |= pack_range_avx512(src, nb * t / nt, nb * (t + 1) / nt, dst);
@@ -166,16 +167,17 @@ bool pack_binary_mask(const uint8_t* src, size_t n, uint8_t* dst) {
 // 0: packs 64 pixels per AVX-512 step (or 8 per scalar step) into tmp, then
 // keeps only the nonzero 64-pixel words.  Returns the encoded size in bytes,
 // or 0 when the mask is not binary.
-size_t pack_sparse_mask(const uint8_t* src, size_t n, uint8_t* dst, uint64_t* tmp) {
+size_t pack_sparse_mask(const uint8_t* src, size_t n, uint8_t* dst, uint64_t* tmp, int threads) {
     static const bool avx512 = __builtin_cpu_supports("avx512bw");
     const int64_t nwords = int64_t(n / 64), ngroups = (nwords + 31) / 32;
     uint32_t* pres = reinterpret_cast<uint32_t*>(dst);
     uint32_t* base = pres + ngroups;
     uint64_t* lit = reinterpret_cast<uint64_t*>(dst + mek::sparse_mask_header_bytes(n));
     int bad = 0;
-    std::vector<int64_t> tcount(size_t(omp_get_max_threads()) + 1, 0);
+    const int nth = threads > 0 ? threads : omp_get_max_threads();
+    std::vector<int64_t> tcount(size_t(nth) + 1, 0);
     int nthreads = 1;
-#pragma omp parallel reduction(| : bad)
+#pragma omp parallel reduction(| : bad) num_threads(nth)
     {
         const int t = omp_get_thread_num(), nt = omp_get_num_threads();
 #pragma omp single
@@ -315,7 +317,8 @@ me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* t) {
         (t->pa_quad_ctas && (t->pa_quad_ctas < 2 || t->pa_quad_ctas > 4)) ||
         (t->pa_duo_threads && t->pa_duo_threads != 128 && t->pa_duo_threads != 256) || t->pa_poll_ns < 0 ||
         t->pa_key_a < 0 || t->pa_key_s < 0 || t->fill_rows_per_cta < 0 || t->h2d_chunks < 0 || t->h2d_chunks > 32 ||
-        t->mask_pack < 0 || t->mask_pack > 3 || t->ring_ctas < 0 || t->ring_ctas == 1 || t->ring_ctas > 4)
+        t->mask_pack < 0 || t->mask_pack > 3 || t->ring_ctas < 0 || t->ring_ctas == 1 || t->ring_ctas > 4 ||
+        t->host_threads < 0)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "tuning field out of range");
     ctx->tuning = *t;
     ctx->tune = mek::resolve_tuning(t);
@@ -344,7 +347,7 @@ me_status me_b200_pack_mask(const uint8_t* mask, size_t n, uint8_t* out, size_t 
     if (out_cap < mek::sparse_mask_header_bytes(n) + n / 8)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "output buffer too small");
     std::vector<uint64_t> tmp(n / 64 + 1);
-    const size_t bytes = pack_sparse_mask(mask, n, out, tmp.data());
+    const size_t bytes = pack_sparse_mask(mask, n, out, tmp.data(), 0);
     if (!bytes) return me_fail(ME_ERR_INVALID_ARGUMENT, "mask is not binary (bytes other than 0 and 255)");
     *out_bytes = bytes;
     return ok();
@@ -658,7 +661,7 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
                 if (n % 64 == 0 && sparse) {
                     // zero 64-pixel words elided (object masks are mostly background)
                     if (ctx->pack_tmp.size() < n / 64) ctx->pack_tmp.resize(max_chunk / 64 + 1);
-                    const size_t bytes = pack_sparse_mask(alpha + o, n, hb, ctx->pack_tmp.data());
+                    const size_t bytes = pack_sparse_mask(alpha + o, n, hb, ctx->pack_tmp.data(), ctx->tune.host_threads);
                     if ((packed = bytes > 0)) {
                         ME_CUDA(cudaMemcpyAsync(db, hb, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
                         ctx->h2d_bytes += int64_t(bytes);
@@ -667,7 +670,7 @@ me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, in
                         ME_CUDA(mek::unpack_mask_sparse_bits(db, dbits + o / 8, n, ctx->copy_stream));
                         unpack_launches = 1;
                     }
-                } else if ((packed = pack_binary_mask(alpha + o, n, hb))) {
+                } else if ((packed = pack_binary_mask(alpha + o, n, hb, ctx->tune.host_threads))) {
                     // the dense bit plane itself
                     ME_CUDA(cudaMemcpyAsync(dbits + o / 8, hb, n / 8, cudaMemcpyHostToDevice, ctx->copy_stream));
                     ctx->h2d_bytes += int64_t(n / 8);

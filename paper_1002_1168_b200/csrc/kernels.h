@@ -49,6 +49,7 @@ struct Tuning {
     int h2d_chunks = 16;
     int mask_pack = 3;       // 1 bytes, 2 dense bits, 3 sparse bits
     int ring_ctas = 3;       // CTAs per SM of ring_kernel (3: 80 registers, no spills)
+    int host_threads = 0;    // host-path mask packing threads (0: OpenMP default)
     const char* pa_trace = nullptr;
 };
 Tuning resolve_tuning(const me_tuning* t);

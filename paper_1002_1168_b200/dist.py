@@ -11,6 +11,17 @@ from __future__ import annotations
 from typing import List, Optional, Tuple
 
 
+def coll_device(device, group=None):
+    """Where collective buffers live: `device` under NCCL, the host under gloo
+    (the CPU tests, and the bench's one-GPU multi-rank check)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_backend(group) == "gloo":
+        return torch.device("cpu")
+    return device
+
+
 def shard(n_total: int, rank: int, world: int) -> Tuple[int, int]:
     """Contiguous balanced split of n_total units: (first, count) of `rank`."""
     if world < 1 or not (0 <= rank < world):
@@ -171,7 +182,7 @@ class ResultGatherer:
         mvb, stb = self._pack(recs, stats)
         per = mvb.shape[1] + stb.shape[1]
         if self.send[i] is None:
-            self.send[i] = torch.zeros((self.nmax, per), dtype=torch.uint8, device=recs.device)
+            self.send[i] = torch.zeros((self.nmax, per), dtype=torch.uint8, device=coll_device(recs.device, self.group))
         n = recs.shape[0]
         self.send[i][:n, : mvb.shape[1]].copy_(mvb)
         self.send[i][:n, mvb.shape[1]:].copy_(stb)
@@ -260,6 +271,6 @@ def max_over_ranks(value: float, device=None) -> float:
 
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return value
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64, device=coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
