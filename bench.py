@@ -474,6 +474,11 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
         pin[1].copy_(alpha)
         hl, ha = pin[0].numpy(), pin[1].numpy()
     if not args.no_e2e:
+        # torchrun sets OMP_NUM_THREADS=1: give each rank its share of the host
+        # cores for the mask packing of the host-buffer path
+        lws = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        if lws > 1:
+            _lib.set_tuning(local, host_threads=max(1, (os.cpu_count() or 1) // lws))
         hrecs = torch.empty((n_seq, pairs, rows, cols, 16), dtype=torch.uint8, pin_memory=True)
         hstats = torch.empty((n_seq, pairs, 48), dtype=torch.uint8, pin_memory=True)
         n_e2e = args.e2e_steps or max(1, min(args.steps, 10))
