@@ -131,6 +131,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         }
         if (e0 != cudaErrorNotSupported) return e0;
     }
+    NvtxRange nv_batch(pa ? "me_b200/batch/pa" : "me_b200/batch/baseline");
     const int nbins = pa ? pa_bins(b, tune) : 1;
     if (scratch_size < scratch_bytes(b, algo, tune)) return cudaErrorInvalidValue;
     Scratch s = carve(b, nbins, scratch);
@@ -154,20 +155,27 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         ca.key_a = k.a;
         ca.key_s = k.s;
     }
-    if ((e = launch_classify(ca, num_sms, st))) return e;
+    {
+        NvtxRange nv("me_b200/classify");
+        if ((e = launch_classify(ca, num_sms, st))) return e;
+    }
     if (events) cudaEventRecord(events[1], st);
     // PA kernel choice (pa.cu): the duo / quad kernels take list entries in
     // pairs / fours, so every wavefront step is padded to a multiple of 2 / 4;
     // the hybrids split the list into narrow / wide / narrow step ranges.
     const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, prev0_integer, num_sms, tune) : 0;
     int* ranges = pa_mode >= 3 ? s.counter + 8 : nullptr;
-    if ((e = launch_scan(s.hist, nbins, pa_mode == 4 ? 4 : pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
-                         pa_wide_threshold(num_sms, tune), ranges, st, tune.sort_pdl)))
-        return e;
-    if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st, tune))) return e;
+    {
+        NvtxRange nv("me_b200/sort");
+        if ((e = launch_scan(s.hist, nbins, pa_mode == 4 ? 4 : pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
+                             pa_wide_threshold(num_sms, tune), ranges, st, tune.sort_pdl)))
+            return e;
+        if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st, tune))) return e;
+    }
     const int* nlist = s.offs + nbins;
     if (events) cudaEventRecord(events[2], st);
 
+    NvtxRange nv_search("me_b200/search");
     if (algo == ME_ALGO_ES)
         e = launch_es(b, cfg.search_range, s.list, nlist, s.counter, recs, stats, num_sms, st);
     else if (algo == ME_ALGO_PA)

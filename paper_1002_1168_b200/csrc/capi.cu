@@ -433,6 +433,7 @@ me_status me_b200_run_sequences_dev(me_ctx* ctx, const me_config* cfg, int n_seq
                                     int W, int H, const uint8_t* luma, const uint8_t* alpha,
                                     me_block_rec* recs, me_pair_stats* stats, uint8_t* pred,
                                     void* stream) {
+    mek::NvtxRange nv("me_b200_run_sequences_dev");
     me_status s = check_ctx(ctx);
     if (s) return s;
     if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
@@ -469,6 +470,7 @@ me_status me_b200_run_sequences_bits_dev(me_ctx* ctx, const me_config* cfg, int 
                                          int W, int H, const uint8_t* luma, const uint8_t* alpha_bits,
                                          me_block_rec* recs, me_pair_stats* stats, uint8_t* pred,
                                          void* stream) {
+    mek::NvtxRange nv("me_b200_run_sequences_bits_dev");
     me_status s = check_ctx(ctx);
     if (s) return s;
     if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
@@ -525,6 +527,7 @@ me_status me_b200_pack_mask_dev(me_ctx* ctx, const uint8_t* alpha, size_t n, uin
 me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
                                int H, const uint8_t* luma, const uint8_t* alpha, int row0, int row1,
                                me_block_rec* recs, me_pair_stats* stats, void* stream) {
+    mek::NvtxRange nv("me_b200_run_band_dev");
     me_status s = check_ctx(ctx);
     if (s) return s;
     if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
@@ -557,6 +560,7 @@ me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int
 me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_frames, int W, int H,
                                       const uint8_t* luma, const uint8_t* alpha, me_block_rec* recs,
                                       me_pair_stats* stats, int n_gpus) {
+    mek::NvtxRange nv("me_b200_run_sequences_multi");
     me_status s = check_batch(cfg, n_seq, n_frames, W, H);
     if (s) return s;
     if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
@@ -604,6 +608,7 @@ me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_fra
 me_status me_b200_run_sequences(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
                                 int H, const uint8_t* luma, const uint8_t* alpha,
                                 me_block_rec* recs, me_pair_stats* stats, uint8_t* pred) {
+    mek::NvtxRange nv("me_b200_run_sequences");
     me_status s = check_ctx(ctx);
     if (s) return s;
     if ((s = check_batch(cfg, n_seq, n_frames, W, H))) return s;
@@ -728,6 +733,7 @@ me_status me_b200_estimate_field(me_ctx* ctx, const me_config* cfg, int W, int H
                                  const uint8_t* cur, const uint8_t* ref, const uint8_t* cur_alpha,
                                  const uint8_t* ref_alpha, const int32_t* prev_mv, int prev_cols,
                                  int prev_rows, me_block_rec* recs, me_pair_stats* stats) {
+    mek::NvtxRange nv("me_b200_estimate_field");
     me_status s = check_ctx(ctx);
     if (s) return s;
     if ((s = validate(cfg))) return s;  // cfg.validate(); prs.validate() (estimators.cpp:390-391)

@@ -7,8 +7,18 @@
 #include <cstdint>
 
 #include "me_b200.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace mek {
+
+// NVTX range over a scope (host timeline: the pipeline's stages and the C ABI
+// calls show up in Nsight Systems; no cost without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Geometry of a batch: n_seq sequences x n_frames frames of W x H luma; pairs
 // tau = d .. F-1 (pair index p = tau - d, cur = frame p + d, ref = frame p).
