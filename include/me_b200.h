@@ -222,6 +222,19 @@ me_status me_b200_run_sequences_bits_dev(me_ctx* ctx, const me_config* cfg, int 
 me_status me_b200_pack_mask_dev(me_ctx* ctx, const uint8_t* alpha, size_t n, uint8_t* bits, int* binary,
                                 void* stream);
 
+/* One sequence (n_frames frames, device pointers) whose first pair takes its
+ * temporal candidates from prev_mv — the previous pair's field as
+ * [rows*cols][2] int32 (dx, dy) on the device, or NULL — exactly as
+ * estimate_field's `prev` (estimators.cpp:384-440, bench.cpp:204): the unit of
+ * chunked streaming, where chunk k's frames [s, s + n + d) continue chunk k-1
+ * (PA only uses prev_mv).  prev_integer = 1 declares every prev vector
+ * integer-pel (it is, for fields of an integer-pel search), which lets the
+ * fast PA kernels take it. */
+me_status me_b200_run_sequence_prev_dev(me_ctx* ctx, const me_config* cfg, int n_frames, int width,
+                                        int height, const uint8_t* luma, const uint8_t* alpha,
+                                        const int32_t* prev_mv, int prev_integer, me_block_rec* recs,
+                                        me_pair_stats* stats, void* stream);
+
 /* A block-row band [row0, row1) of the same batch (baselines ES/TSS/FSS/DS
  * only; PA blocks depend on the rows above -> ME_ERR_INVALID_ARGUMENT): the
  * unit of the row sharding across GPUs.  Records of the band's

@@ -149,6 +149,7 @@ SIGNATURES = {
     "me_b200_run_sequences": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P]),
     "me_b200_run_sequences_bits_dev": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, P, P, P, P]),
     "me_b200_pack_mask_dev": (I, [P, P, C.c_size_t, P, C.POINTER(C.c_int), P]),
+    "me_b200_run_sequence_prev_dev": (I, [P, C.POINTER(MeConfig), I, I, I, P, P, P, I, P, P, P]),
     "me_b200_run_band_dev": (I, [P, C.POINTER(MeConfig), I, I, I, I, P, P, I, I, P, P, P]),
     "me_b200_run_sequences_multi": (I, [C.POINTER(MeConfig), I, I, I, I, P, P, P, P, I]),
     "me_b200_estimate_field": (I, [P, C.POINTER(MeConfig), I, I, P, P, P, P, P, I, I, P, P]),

@@ -524,6 +524,31 @@ me_status me_b200_pack_mask_dev(me_ctx* ctx, const uint8_t* alpha, size_t n, uin
     return ok();
 }
 
+me_status me_b200_run_sequence_prev_dev(me_ctx* ctx, const me_config* cfg, int n_frames, int W, int H,
+                                        const uint8_t* luma, const uint8_t* alpha, const int32_t* prev_mv,
+                                        int prev_integer, me_block_rec* recs, me_pair_stats* stats,
+                                        void* stream) {
+    mek::NvtxRange nv("me_b200_run_sequence_prev_dev");
+    me_status s = check_ctx(ctx);
+    if (s) return s;
+    if ((s = check_batch(cfg, 1, n_frames, W, H))) return s;
+    if (!luma || !recs || !stats) return me_fail(ME_ERR_INVALID_ARGUMENT, "null buffer");
+    if ((reinterpret_cast<uintptr_t>(luma) | reinterpret_cast<uintptr_t>(alpha) |
+         reinterpret_cast<uintptr_t>(recs)) & 15 || reinterpret_cast<uintptr_t>(prev_mv) & 3)
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "device buffers must be 16-byte aligned");
+    if (size_t(n_frames) * W * H >= (size_t(1) << 32))
+        return me_fail(ME_ERR_INVALID_ARGUMENT, "a streamed chunk must stay below 4 GiB");
+    const mek::Batch b = make_batch(cfg, 1, n_frames, W, H, luma, alpha);
+    ME_CUDA(ctx->tasks.reserve(mek::scratch_bytes(b, cfg->algo, ctx->tune)));
+    int nl = 0;
+    ME_CUDA(mek::run_batch(b, *cfg, cfg->algo == ME_ALGO_PA ? prev_mv : nullptr, recs, stats, nullptr, ctx->tasks.p,
+                           ctx->tasks.cap, ctx->num_sms, static_cast<cudaStream_t>(stream), ctx->tune,
+                           (ctx->ev_sets = 0, ctx->events()), prev_integer != 0, &nl));
+    ctx->launches = nl;
+    ctx->ev_valid = ctx->profiling;
+    return ok();
+}
+
 me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int n_frames, int W,
                                int H, const uint8_t* luma, const uint8_t* alpha, int row0, int row1,
                                me_block_rec* recs, me_pair_stats* stats, void* stream) {

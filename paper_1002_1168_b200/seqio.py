@@ -146,19 +146,21 @@ def pinned_empty(shape) -> np.ndarray:
     return np.empty(tuple(shape), np.uint8)
 
 
-def stream_frames(src: SequenceSource, count: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
-    """Luma of frames 0..count-1 read straight into ``out`` (default: pinned
-    memory), one ``readinto`` per frame, chroma skipped; Y4M markers checked."""
-    n = src.frame_count if count is None else count
-    if n < 0 or n > src.frame_count:
-        raise IndexError(f"frame index {n - 1} out of range [0,{src.frame_count})")
+def stream_frames(src: SequenceSource, count: Optional[int] = None, out: Optional[np.ndarray] = None, first: int = 0) -> np.ndarray:
+    """Luma of frames first..first+count-1 read straight into ``out`` (default:
+    pinned memory), one ``readinto`` per frame, chroma skipped; Y4M markers
+    checked."""
+    n = src.frame_count - first if count is None else count
+    if first < 0 or n < 0 or first + n > src.frame_count:
+        raise IndexError(f"frame index {first + n - 1} out of range [0,{src.frame_count})")
     W, H = src.width, src.height
     out = pinned_empty((n, H, W)) if out is None else out
     if out.shape != (n, H, W) or out.dtype != np.uint8 or not out.flags.c_contiguous:
         raise ValueError("out must be a contiguous uint8 array [frames, H, W]")
     csize = W * H // 2
+    stride = W * H * 3 // 2 + (src.frame_marker_bytes if src.format == Y4M else 0)
     with open(src.path, "rb", buffering=0) as f:
-        f.seek(src.header_bytes)
+        f.seek(src.header_bytes + first * stride)
         for i in range(n):
             if src.format == Y4M:
                 m = f.read(src.frame_marker_bytes)
@@ -215,17 +217,118 @@ def binarize(gray: np.ndarray, threshold: int = 128) -> np.ndarray:  # frame.cpp
     return np.where(gray >= threshold, 255, 0).astype(np.uint8)
 
 
-def read_masks(src: MaskSource, count: int, width: int, height: int, out: Optional[np.ndarray] = None) -> np.ndarray:
-    """``[count, H, W]`` binarised masks (read_mask, video_io.cpp:184-192)."""
+def read_masks(src: MaskSource, count: int, width: int, height: int, out: Optional[np.ndarray] = None, first: int = 0) -> np.ndarray:
+    """``[count, H, W]`` binarised masks of frames first.. (read_mask,
+    video_io.cpp:184-192)."""
     if not src.present():
         raise RuntimeError("read_mask called without a mask pattern")
     out = np.empty((count, height, width), np.uint8) if out is None else out
     for i in range(count):
-        gray = read_pgm(src.path_for(i))
+        gray = read_pgm(src.path_for(first + i))
         if gray.shape != (height, width):
-            raise RuntimeError(f"mask {src.path_for(i)} is {gray.shape[1]}x{gray.shape[0]}, video is {width}x{height}")
+            raise RuntimeError(f"mask {src.path_for(first + i)} is {gray.shape[1]}x{gray.shape[0]}, video is {width}x{height}")
         out[i] = binarize(gray, src.threshold)
     return out
+
+
+def estimate_stream(src: SequenceSource, cfg, masks: Optional[MaskSource] = None, chunk: int = 8, device: int = 0):
+    """A sequence file through the GPU in chunks of `chunk` frame pairs, I/O
+    overlapped with the estimation (pinned streaming I/O): a reader
+    thread fills two pinned host slots with chunk k+1's frames (and masks)
+    while chunk k crosses PCIe on a copy stream and runs on a compute stream;
+    chunk k's frames are [s, s + n + d) (pairs s .. s+n-1), and PA's first pair
+    of a chunk takes the previous chunk's last field as its temporal candidates
+    (me_b200_run_sequence_prev_dev), so the result equals one whole-sequence
+    run (run_experiment's pair loop, bench.cpp:155-205).  Returns (recs
+    [pairs, rows, cols], stats [pairs]) in the record / stats dtypes."""
+    import ctypes as C
+    import queue
+    import threading
+
+    import torch
+
+    from . import _lib
+    from .api import Algo
+
+    d, bs = cfg.search.ref_distance, cfg.search.block_size
+    W, H, F = src.width, src.height, src.frame_count
+    pairs = F - d
+    if pairs < 1:
+        raise ValueError("ref_distance must be smaller than the frame count")
+    rows, cols = H // bs, W // bs
+    nchunks = (pairs + chunk - 1) // chunk
+    dev = torch.device("cuda", device)
+    slots = [pinned_empty((2, chunk + d, H, W)) for _ in range(2)]
+    dslots = [torch.empty((2, chunk + d, H, W), dtype=torch.uint8, device=dev) for _ in range(2)]
+    out_r = torch.empty((pairs, rows, cols, 16), dtype=torch.uint8, pin_memory=True)
+    out_s = torch.empty((pairs, 48), dtype=torch.uint8, pin_memory=True)
+    recs = torch.empty((2, chunk, rows, cols, 16), dtype=torch.uint8, device=dev)
+    stats = torch.empty((2, chunk, 48), dtype=torch.uint8, device=dev)
+    prev = torch.zeros((rows * cols, 2), dtype=torch.int32, device=dev)
+    copy_st, comp_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    free = [threading.Event(), threading.Event()]
+    for e in free:
+        e.set()
+    ready: "queue.Queue" = queue.Queue()
+
+    def reader():
+        try:
+            for k in range(nchunks):
+                s0, n = k * chunk, min(chunk, pairs - k * chunk)
+                slot = k & 1
+                free[slot].wait()
+                free[slot].clear()
+                stream_frames(src, n + d, slots[slot][0, : n + d], first=s0)
+                if masks is not None and masks.present():
+                    read_masks(masks, n + d, W, H, slots[slot][1, : n + d], first=s0)
+                ready.put((k, s0, n))
+        except Exception as e:  # reported by the consumer
+            ready.put(e)
+
+    th = threading.Thread(target=reader, daemon=True)
+    th.start()
+    c = cfg.c()
+    lib = _lib.lib()
+    done = [None, None]   # compute of the chunk that last used a device slot
+    pending = None        # (copy event, host slot) of the previous chunk
+    for _ in range(nchunks):
+        item = ready.get()
+        if isinstance(item, Exception):
+            raise item
+        k, s0, n = item
+        slot = k & 1
+        hs = torch.from_numpy(slots[slot])
+        if done[slot] is not None:  # the device slot's previous chunk has been estimated
+            copy_st.wait_event(done[slot])
+        with torch.cuda.stream(copy_st):
+            dslots[slot][:, : n + d].copy_(hs[:, : n + d], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_st)
+        comp_st.wait_event(ev)
+        luma, alpha = dslots[slot][0], dslots[slot][1]
+        rv, sv = recs[slot], stats[slot]
+        _lib.check(lib.me_b200_run_sequence_prev_dev(
+            _lib.ctx(device), C.byref(c), n + d, W, H, C.c_void_p(luma.data_ptr()),
+            C.c_void_p(alpha.data_ptr()) if masks is not None and masks.present() else None,
+            C.c_void_p(prev.data_ptr()) if (k > 0 and cfg.algo == Algo.PA) else None,
+            int(not cfg.search.halfpel), C.c_void_p(rv.data_ptr()), C.c_void_p(sv.data_ptr()),
+            C.c_void_p(comp_st.cuda_stream)))
+        with torch.cuda.stream(comp_st):
+            if cfg.algo == Algo.PA:  # the last pair's field: the next chunk's temporal candidates
+                prev.copy_(rv[n - 1].reshape(rows * cols, 16).view(torch.int16)[:, 0:2].to(torch.int32))
+            out_r[s0: s0 + n].copy_(rv[:n], non_blocking=True)
+            out_s[s0: s0 + n].copy_(sv[:n], non_blocking=True)
+            done[slot] = torch.cuda.Event()
+            done[slot].record(comp_st)
+        if pending is not None:  # the previous chunk's host slot may be refilled
+            pending[0].synchronize()
+            free[pending[1]].set()
+        pending = (ev, slot)
+    if pending is not None:
+        free[pending[1]].set()
+    comp_st.synchronize()
+    th.join()
+    return out_r.numpy().view(_lib.rec_dtype()).reshape(pairs, rows, cols).copy(), out_s.numpy().view(_lib.stats_dtype()).reshape(pairs).copy()
 
 
 def write_i420(path: str, luma: np.ndarray, chroma: Optional[np.ndarray] = None, y4m: bool = False):

@@ -675,3 +675,29 @@ def test_es_batch_large_range_records(me_gpu, port):
         assert np.array_equal(got_r[f], want_r[f]), f
     assert np.array_equal(got_r["comparisons"], want_r["comparisons"])  # both saturate at 65535
     assert got_r["comparisons"].max() == 65535
+
+
+# ---------------------------------------------------------------------------
+# Streaming I/O: a sequence file through the GPU in chunks
+
+
+@pytest.mark.parametrize("algo,bs,chunk", [(4, 8, 5), (4, 8, 7), (0, 16, 6), (3, 16, 4)])
+def test_estimate_stream_equals_whole_sequence(me_gpu, port, tmp_path, algo, bs, chunk):
+    """seqio.estimate_stream (pinned slots filled by a reader thread, H2D on a
+    copy stream, chunks chained through the temporal candidate) gives exactly
+    the whole-sequence result, and the oracle's."""
+    from paper_1002_1168_b200 import seqio, synth
+
+    luma, alpha = synth.config_sequence(2, 95, 17)
+    path = str(tmp_path / "seq.yuv")
+    seqio.write_i420(path, luma)
+    for i in range(luma.shape[0]):
+        seqio.write_gray_pgm(alpha[i], str(tmp_path / f"mask_{i:03d}.pgm"))
+    src = seqio.open_sequence(path, luma.shape[2], luma.shape[1])
+    masks = seqio.MaskSource(pattern=str(tmp_path / "mask_%03d.pgm"))
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=16, block_size=bs))
+    r, s = seqio.estimate_stream(src, cfg, masks, chunk=chunk)
+    want_r, want_s = me_gpu.run_sequences(cfg, luma[None], alpha[None])
+    assert np.array_equal(r, want_r[0]) and np.array_equal(s, want_s[0])
+    o_r, o_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=bs), luma, alpha)
+    assert_recs(r, o_r, "stream")
