@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -582,6 +583,32 @@ me_status me_b200_run_band_dev(me_ctx* ctx, const me_config* cfg, int n_seq, int
 // 0..n_gpus-1, each shard run end to end by its own host thread and context;
 // the results land in the caller's host arrays, so rank 0's gather is the
 // D2H itself.
+// Contexts of the multi-device entry, reused across calls (device buffers and
+// pinned staging are grow-only): a call checks one out per device and returns
+// it, so concurrent callers never share one.
+namespace {
+std::mutex g_multi_mu;
+std::vector<std::vector<me_ctx*>> g_multi_free;
+
+me_status multi_ctx_get(int device, me_ctx** out) {
+    {
+        std::lock_guard<std::mutex> lk(g_multi_mu);
+        if (int(g_multi_free.size()) > device && !g_multi_free[device].empty()) {
+            *out = g_multi_free[device].back();
+            g_multi_free[device].pop_back();
+            return ME_OK;
+        }
+    }
+    return me_b200_ctx_create(device, out);
+}
+
+void multi_ctx_put(int device, me_ctx* c) {
+    std::lock_guard<std::mutex> lk(g_multi_mu);
+    if (int(g_multi_free.size()) <= device) g_multi_free.resize(device + 1);
+    g_multi_free[device].push_back(c);
+}
+}  // namespace
+
 me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_frames, int W, int H,
                                       const uint8_t* luma, const uint8_t* alpha, me_block_rec* recs,
                                       me_pair_stats* stats, int n_gpus) {
@@ -606,7 +633,7 @@ me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_fra
     auto work = [&](int g) {
         const int u0 = int(int64_t(units) * g / ng), u1 = int(int64_t(units) * (g + 1) / ng);
         me_ctx* c = nullptr;
-        me_status r = me_b200_ctx_create(g, &c);
+        me_status r = multi_ctx_get(g, &c);
         if (!r) {
             if (by_pair)  // pairs [u0, u1) = frames [u0, u1 + d)
                 r = me_b200_run_sequences(c, cfg, 1, (u1 - u0) + cfg->ref_distance, W, H, luma + plane * u0,
@@ -619,7 +646,7 @@ me_status me_b200_run_sequences_multi(const me_config* cfg, int n_seq, int n_fra
         }
         if (r) msg[g] = g_last_error;
         rc[g] = r;
-        if (c) me_b200_ctx_destroy(c);
+        if (c) multi_ctx_put(g, c);
     };
     std::vector<std::thread> pool;
     for (int g = 1; g < ng; ++g) pool.emplace_back(work, g);
