@@ -1674,18 +1674,20 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
     uint32_t* s_meta = s_cost + cols * rows;  // dpd << 8 | iterations
     uint8_t* s_type = reinterpret_cast<uint8_t*>(s_meta + cols * rows);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    // stage the planes (16-byte copies) and clear the MV words
+    // stage the planes (16-byte copies) and clear the MV words: the pair's ref
+    // is frame 0 and its cur frame d (ref_distance), which need not be adjacent
     {
-        const uint4* g = reinterpret_cast<const uint4*>(b.luma);
-        for (int i = tid; i < 2 * plane / 16; i += blockDim.x) {
-            const int f = i / (plane / 16), o = i - f * (plane / 16);
-            reinterpret_cast<uint4*>(s_frames + f * size_t(pp))[o] = __ldg(g + i);
+        const int pw = plane / 16;
+        for (int i = tid; i < 2 * pw; i += blockDim.x) {
+            const int f = i / pw, o = i - f * pw;
+            const uint4* g = reinterpret_cast<const uint4*>(b.luma + size_t(f ? b.d : 0) * plane);
+            reinterpret_cast<uint4*>(s_frames + f * size_t(pp))[o] = __ldg(g + o);
         }
         if (has_alpha) {
-            const uint4* ga = reinterpret_cast<const uint4*>(b.alpha);
-            for (int i = tid; i < 2 * plane / 16; i += blockDim.x) {
-                const int f = i / (plane / 16), o = i - f * (plane / 16);
-                reinterpret_cast<uint4*>(s_ra + f * size_t(pp))[o] = __ldg(ga + i);
+            for (int i = tid; i < 2 * pw; i += blockDim.x) {
+                const int f = i / pw, o = i - f * pw;
+                const uint4* ga = reinterpret_cast<const uint4*>(b.alpha + size_t(f ? b.d : 0) * plane);
+                reinterpret_cast<uint4*>(s_ra + f * size_t(pp))[o] = __ldg(ga + o);
             }
         }
         for (int i = tid; i < cols * rows; i += blockDim.x) s_mv[i] = 0u;

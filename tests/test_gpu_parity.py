@@ -701,3 +701,50 @@ def test_estimate_stream_equals_whole_sequence(me_gpu, port, tmp_path, algo, bs,
     assert np.array_equal(r, want_r[0]) and np.array_equal(s, want_s[0])
     o_r, o_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=16, block_size=bs), luma, alpha)
     assert_recs(r, o_r, "stream")
+
+
+# ---------------------------------------------------------------------------
+# Seeded fuzz: random geometry, configuration and content against the oracle
+
+
+def _fuzz_case(seed):
+    rng = np.random.default_rng(seed)
+    W, H = 16 * int(rng.integers(2, 9)), 16 * int(rng.integers(2, 8))
+    F = int(rng.integers(3, 7))
+    d = int(rng.integers(1, min(3, F - 1) + 1))
+    algo = int(rng.integers(0, 5))
+    bs = int(rng.choice([8, 16]))
+    S = int(rng.integers(1, 25))
+    hp = int(algo == 4 and rng.random() < 0.3)
+    bt = int(algo == 4 and rng.random() < 0.3)
+    it = int(rng.integers(1, 8))
+    step = 1 if hp else int(rng.choice([1, 2, 2]))
+    eps = float(rng.choice([0.25, 0.5, 1.0]))
+    theta = float(rng.choice([0.5, 2.0, 4.0]))
+    base = np.convolve(noise(rng, H + 32, W + 32).ravel(), np.ones(int(rng.integers(1, 12))) / 1.0, "same")
+    base = (base.reshape(H + 32, W + 32) // int(rng.integers(1, 64))).astype(np.uint8)
+    sh = rng.integers(-6, 7, size=(F, 2))
+    luma = np.stack([base[16 + sh[t, 1]:16 + sh[t, 1] + H, 16 + sh[t, 0]:16 + sh[t, 0] + W] for t in range(F)])
+    kind = int(rng.integers(0, 3))  # no mask, binary mask, non-binary mask
+    alpha = None
+    if kind:
+        alpha = np.zeros_like(luma)
+        for t in range(F):
+            x0, y0 = int(rng.integers(0, W // 2)), int(rng.integers(0, H // 2))
+            alpha[t, y0:y0 + int(rng.integers(4, H)), x0:x0 + int(rng.integers(4, W))] = 255
+            if kind == 2:
+                alpha[t, rng.integers(0, H, 5), rng.integers(0, W, 5)] = rng.integers(1, 255, 5).astype(np.uint8)
+    return dict(luma=np.ascontiguousarray(luma), alpha=alpha, algo=algo, bs=bs, S=S, halfpel=hp, ref_distance=d, bt=bt,
+                max_iter=it, step=step, eps=eps, theta=theta)
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_fuzz_sequences(me_gpu, port, seed):
+    c = _fuzz_case(1000 + seed)
+    from backends import GpuBackend, PortBackend
+
+    kw = dict(halfpel=c["halfpel"], ref_distance=c["ref_distance"], bt=c["bt"], max_iter=c["max_iter"], step=c["step"], eps=c["eps"], theta=c["theta"])
+    got_r, got_s = GpuBackend().run_sequence(c["algo"], c["luma"], c["alpha"], c["bs"], c["S"], **kw)
+    want_r, want_s = PortBackend().run_sequence(c["algo"], c["luma"], c["alpha"], c["bs"], c["S"], **kw)
+    assert_recs(got_r, want_r, f"fuzz {seed}: { {k: v for k, v in c.items() if k not in ('luma', 'alpha')} }")
+    assert np.array_equal(got_s, want_s)
