@@ -748,3 +748,73 @@ def test_fuzz_sequences(me_gpu, port, seed):
     want_r, want_s = PortBackend().run_sequence(c["algo"], c["luma"], c["alpha"], c["bs"], c["S"], **kw)
     assert_recs(got_r, want_r, f"fuzz {seed}: { {k: v for k, v in c.items() if k not in ('luma', 'alpha')} }")
     assert np.array_equal(got_s, want_s)
+
+
+def _fuzz_batch(seed):
+    """A batch of sequences sharing geometry and configuration (_fuzz_case's
+    draws), with binary masks more often so the bit-plane path is covered."""
+    rng = np.random.default_rng(5000 + seed)
+    c = _fuzz_case(7000 + seed)
+    n_seq = int(rng.integers(2, 6))
+    F, H, W = c["luma"].shape
+    lumas, alphas = [c["luma"]], [c["alpha"]]
+    for i in range(1, n_seq):
+        ci = _fuzz_case(9000 + 100 * seed + i)
+        li = ci["luma"]
+        # same geometry: crop / tile the other case's content to (F, H, W)
+        li = np.resize(li, (F,) + li.shape[1:])
+        li = np.tile(li, (1, (H + li.shape[1] - 1) // li.shape[1], (W + li.shape[2] - 1) // li.shape[2]))[:, :H, :W]
+        lumas.append(np.ascontiguousarray(li))
+        if c["alpha"] is not None:
+            a = np.zeros((F, H, W), np.uint8)
+            for t in range(F):
+                x0, y0 = int(rng.integers(0, W // 2)), int(rng.integers(0, H // 2))
+                a[t, y0:y0 + int(rng.integers(4, H)), x0:x0 + int(rng.integers(4, W))] = 255
+            if rng.random() < 0.3:
+                a[:, rng.integers(0, H, 3), rng.integers(0, W, 3)] = 77
+            alphas.append(a)
+    luma = np.stack(lumas)
+    alpha = None if c["alpha"] is None else np.stack(alphas)
+    return c, luma, alpha
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_fuzz_batches(me_gpu, port, seed):
+    """Whole batches through every batched entry point (host buffers, device
+    bytes, device bit planes when the masks are binary) and, for PA, a random
+    kernel schedule, each against the oracle sequence by sequence."""
+    import torch
+
+    from paper_1002_1168_b200 import _lib, batch as B
+
+    c, luma, alpha = _fuzz_batch(seed)
+    me = me_gpu
+    cfg = me.BatchConfig(algo=me.Algo(c["algo"]), search=me.SearchConfig(search_range=c["S"], block_size=c["bs"], ref_distance=c["ref_distance"], halfpel=bool(c["halfpel"])),
+                         prs=me.PrsConfig(epsilon=c["eps"], theta=c["theta"], max_iterations=c["max_iter"], step=c["step"]), boundary_temporal=me.BoundaryTemporal(c["bt"]))
+    kw = dict(halfpel=c["halfpel"], ref_distance=c["ref_distance"], bt=c["bt"], max_iter=c["max_iter"], step=c["step"], eps=c["eps"], theta=c["theta"])
+    from backends import PortBackend
+
+    want = [PortBackend().run_sequence(c["algo"], luma[i], None if alpha is None else alpha[i], c["bs"], c["S"], **kw) for i in range(len(luma))]
+    what = f"batch fuzz {seed}: n_seq {len(luma)} { {k: v for k, v in c.items() if k not in ('luma', 'alpha')} }"
+    rng = np.random.default_rng(seed)
+    sched = str(rng.choice(["auto", "warp", "fast", "duo", "duo-hybrid", "hybrid"])) if c["algo"] == 4 else "auto"
+    prev = _lib.set_tuning(0, pa_schedule=sched, pa_static_claim=int(rng.random() < 0.2))
+    try:
+        recs, stats = me.run_sequences(cfg, luma, alpha)
+        dl = torch.from_numpy(luma).cuda()
+        da = None if alpha is None else torch.from_numpy(alpha).cuda()
+        r_dev, s_dev = B.run_sequences_dev(cfg, dl, da)
+        sv = lambda t: t.cpu().numpy().view(stats.dtype).reshape(stats.shape)  # noqa: E731
+        outs = [("host", recs, stats), ("dev", B.rec_view(r_dev), sv(s_dev))]
+        if da is not None:
+            bits, binary = B.pack_mask_dev(da)
+            if binary:
+                r_b, s_b = B.run_sequences_bits_dev(cfg, dl, bits)
+                outs.append(("bits", B.rec_view(r_b), sv(s_b)))
+        torch.cuda.synchronize()
+    finally:
+        _lib.restore_tuning(prev, 0)
+    for name, r, s in outs:
+        for i, (wr, ws) in enumerate(want):
+            assert_recs(r[i].reshape(wr.shape), wr, f"{what} [{name}, sched {sched}, seq {i}]")
+            assert np.array_equal(s[i].reshape(ws.shape), ws), f"{what} [{name}] stats seq {i}"
