@@ -37,6 +37,7 @@ struct EsArgs {
 };
 
 constexpr int kEsThreads = 256;
+constexpr uint32_t kEsDead = 0xF0000000u;  // key bits of rows past the window (> any real key: SAD << 12 < 2^28)
 
 // PWC: the staged row stride in words when known at compile time (the
 // launcher instantiates the common search ranges; every row offset in the SAD
@@ -98,19 +99,43 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
             uint32_t* const sm1 = sm + CW;
             uint32_t* const sm2 = sm + 2 * CW;
             uint32_t* const sm3 = sm + 3 * CW;
-            for (int i = tid; i < total; i += kEsThreads) {
-                const int row = __float2int_rz((float(i) + 0.5f) * inv_pw), q = i - row * PW;
-                const uint32_t b0 = seg0 + uint32_t(row) * uint32_t(W);
-                const uint32_t w0 = b0 >> 2, off = b0 & 3u, wl = (b0 + uint32_t(rowbytes) - 1) >> 2;
-                const uint32_t g0 = __ldg(rw + min(w0 + q, wl)), g1 = __ldg(rw + min(w0 + q + 1, wl)),
-                               g2 = __ldg(rw + min(w0 + q + 2, wl));
-                const uint32_t sh = off * 8;
-                // copies s = 0..3: byte offset off + s within (g0, g1, g2)
-                sm[i] = __funnelshift_r(g0, g1, sh);
-                sm1[i] = off + 1 < 4 ? __funnelshift_r(g0, g1, sh + 8) : g1;
-                sm2[i] = off + 2 < 4 ? __funnelshift_r(g0, g1, sh + 16) : __funnelshift_r(g1, g2, sh - 16);
-                sm3[i] = off == 0 ? __funnelshift_r(g0, g1, 24) : __funnelshift_r(g1, g2, sh - 8);
+            // U words per thread per round, every load of the round issued
+            // before any store (the staging is L2-latency-bound otherwise)
+            constexpr int U = 4;
+            for (int i0 = tid; i0 < total; i0 += U * kEsThreads) {
+                uint32_t g[U][3], offs[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = min(i0 + u * kEsThreads, total - 1);
+                    const int row = __float2int_rz((float(i) + 0.5f) * inv_pw), q = i - row * PW;
+                    const uint32_t b0 = seg0 + uint32_t(row) * uint32_t(W);
+                    const uint32_t w0 = b0 >> 2, wl = (b0 + uint32_t(rowbytes) - 1) >> 2;
+                    offs[u] = b0 & 3u;
+                    g[u][0] = __ldg(rw + min(w0 + q, wl));
+                    g[u][1] = __ldg(rw + min(w0 + q + 1, wl));
+                    g[u][2] = __ldg(rw + min(w0 + q + 2, wl));
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * kEsThreads;
+                    if (i >= total) break;
+                    const uint32_t off = offs[u], sh = off * 8, g0 = g[u][0], g1 = g[u][1], g2 = g[u][2];
+                    // copies s = 0..3: byte offset off + s within (g0, g1, g2)
+                    sm[i] = __funnelshift_r(g0, g1, sh);
+                    sm1[i] = off + 1 < 4 ? __funnelshift_r(g0, g1, sh + 8) : g1;
+                    sm2[i] = off + 2 < 4 ? __funnelshift_r(g0, g1, sh + 16) : __funnelshift_r(g1, g2, sh - 16);
+                    sm3[i] = off == 0 ? __funnelshift_r(g0, g1, 24) : __funnelshift_r(g1, g2, sh - 8);
+                }
             }
+        }
+        // per window row of the band: the key's low bits, (|dy| << 3 | k), or
+        // kEsDead for rows past the window, so a position's 32-bit key is two
+        // IMADs (FMA pipe) and the VIMNMX — the kernel is ALU-pipe-bound
+        // (VABSDIFF4 issues at half rate there)
+        uint32_t* const rkey = sm + 4 * CW;
+        for (int i = tid; i < bruns * K; i += kEsThreads) {
+            const int wy = run0 * K + i;
+            rkey[i] = wy < WY ? (uint32_t(abs(lo_y + wy)) << 3) | uint32_t(i % K) : kEsDead;
         }
         __syncthreads();
         // tasks (run, col) in raster order: flat index, run by a float reciprocal
@@ -140,16 +165,12 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
             // 64-bit key
             const int dx = lo_x + col;
             const int ady = (run0 + run) * K;
-            const int adx = abs(dx);
+            const uint32_t adx8 = uint32_t(abs(dx)) << 3;
+            const uint32_t* rk = rkey + run * K;
             uint32_t m32 = ~0u;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int wy = ady + k;  // window row index
-                const uint32_t man = uint32_t(adx + abs(lo_y + wy));
-                const uint32_t kk = (acc[k] << 12) | (man << 3) | uint32_t(k);
-                m32 = wy < WY ? min(m32, kk) : m32;
-            }
-            if (m32 != ~0u) {
+            for (int k = 0; k < K; ++k) m32 = min(m32, acc[k] * 4096u + (rk[k] + adx8));
+            if (m32 < kEsDead) {
                 const uint32_t wy = uint32_t(ady) + (m32 & 7u);
                 const unsigned long long key = (static_cast<unsigned long long>(m32 >> 12) << 40) |
                                                (static_cast<unsigned long long>((m32 >> 3) & 0x1FFu) << 24) |
@@ -259,8 +280,8 @@ int es_band_rows(int bs, int S, int W, int H) {
 size_t es_smem_bytes(int bs, int S, int W, int H) {
     const int WX = min(2 * S + 1, W - bs + 1);
     const int PW = ((WX - 1) >> 2) + (bs >> 2) + 1;
-    const int srows = es_band_rows(bs, S, W, H) + bs - 1;
-    return size_t(4) * (size_t(srows) * PW + 32) * 4;
+    const int brows = es_band_rows(bs, S, W, H), srows = brows + bs - 1;
+    return size_t(4) * (size_t(srows) * PW + 32) * 4 + size_t(brows) * 4;
 }
 
 cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist, int* counter,
