@@ -39,6 +39,40 @@ struct EsArgs {
 constexpr int kEsThreads = 256;
 constexpr uint32_t kEsDead = 0xF0000000u;  // key bits of rows past the window (> any real key: SAD << 12 < 2^28)
 
+// One task: window column col (its staged copy and word offset folded into
+// `base`) x K consecutive dy.  Each staged row is loaded once and feeds every
+// accumulator whose current row it pairs with.  Returns the minimum over the
+// K positions of the 32-bit key (SAD << 12 | (|dx| + |dy|) << 3 | k): SAD <
+// 2^16, |dx| + |dy| <= 2S < 512 for S <= 255, k < 8; rows past the window
+// carry kEsDead (rkey), so the key is two IMADs (FMA pipe) and a VIMNMX.
+template <int BS, int K, int PWC>
+__device__ __forceinline__ uint32_t es_task(const uint32_t (&c)[BS][BS / 4], const uint32_t* base, int PW_rt,
+                                            const uint32_t* rk, uint32_t adx8) {
+    constexpr int NW = BS / 4;
+    const int PW = PWC ? PWC : PW_rt;
+    uint32_t acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0;
+#pragma unroll
+    for (int j = 0; j < K + BS - 1; ++j) {
+        uint32_t w[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) w[i] = base[j * PW + i];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = j - k;
+            if (r >= 0 && r < BS) {
+#pragma unroll
+                for (int i = 0; i < NW; ++i) acc[k] = vad4(c[r][i], w[i], acc[k]);
+            }
+        }
+    }
+    uint32_t m32 = ~0u;
+#pragma unroll
+    for (int k = 0; k < K; ++k) m32 = min(m32, acc[k] * 4096u + (rk[k] + adx8));
+    return m32;
+}
+
 // PWC: the staged row stride in words when known at compile time (the
 // launcher instantiates the common search ranges; every row offset in the SAD
 // loop is then an immediate), 0 = computed from the clipped window.
@@ -138,40 +172,21 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
             rkey[i] = wy < WY ? (uint32_t(abs(lo_y + wy)) << 3) | uint32_t(i % K) : kEsDead;
         }
         __syncthreads();
-        // tasks (run, col) in raster order: flat index, run by a float reciprocal
+        // tasks (run, col) in raster order: flat index, run by a float
+        // reciprocal.  The window's last run usually holds ONE row (WY = 2S + 1
+        // = 8n + 1 for interior blocks): its tasks take a K = 1 body instead of
+        // summing K - 1 rows past the window.
         const float inv_wx = 1.0f / float(WX);
+        const bool tail1 = run0 + bruns == nruns && WY - (nruns - 1) * K == 1;
         for (int ti = tid, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX; run < bruns;
              ti += kEsThreads, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX) {
             const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
-            uint32_t acc[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = 0;
-#pragma unroll
-            for (int j = 0; j < K + BS - 1; ++j) {
-                uint32_t w[NW];
-#pragma unroll
-                for (int i = 0; i < NW; ++i) w[i] = base[j * PW + i];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int r = j - k;
-                    if (r >= 0 && r < BS) {
-#pragma unroll
-                        for (int i = 0; i < NW; ++i) acc[k] = vad4(c[r][i], w[i], acc[k]);
-                    }
-                }
-            }
-            // min over the run's K positions of (SAD, |dx|+|dy|, k) in 32 bits
-            // (SAD < 2^16, |dx|+|dy| <= 2S < 512 for S <= 255, k < 8), then one
-            // 64-bit key
-            const int dx = lo_x + col;
-            const int ady = (run0 + run) * K;
-            const uint32_t adx8 = uint32_t(abs(dx)) << 3;
+            const uint32_t adx8 = uint32_t(abs(lo_x + col)) << 3;
             const uint32_t* rk = rkey + run * K;
-            uint32_t m32 = ~0u;
-#pragma unroll
-            for (int k = 0; k < K; ++k) m32 = min(m32, acc[k] * 4096u + (rk[k] + adx8));
+            const uint32_t m32 = tail1 && run == bruns - 1 ? es_task<BS, 1, PWC>(c, base, PW, rk, adx8)
+                                                          : es_task<BS, K, PWC>(c, base, PW, rk, adx8);
             if (m32 < kEsDead) {
-                const uint32_t wy = uint32_t(ady) + (m32 & 7u);
+                const uint32_t wy = uint32_t((run0 + run) * K) + (m32 & 7u);
                 const unsigned long long key = (static_cast<unsigned long long>(m32 >> 12) << 40) |
                                                (static_cast<unsigned long long>((m32 >> 3) & 0x1FFu) << 24) |
                                                static_cast<unsigned long long>(wy * uint32_t(WX) + uint32_t(col));
