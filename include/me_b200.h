@@ -151,7 +151,7 @@ typedef struct me_tuning {
     int32_t mask_pack;        /* host path alpha transfer: 1 bytes, 2 dense bits, 0/3 sparse bits */
     int32_t ring_ctas;        /* CTAs per SM of the TSS/FSS/DS kernel, 2..4 (0: 3) */
     int32_t host_threads;     /* host-buffer path: threads packing the masks (0: OpenMP default) */
-    const char* pa_trace_path;/* debug: per-block PA trace written here (NULL: off) */
+    const char* pa_trace_path;/* debug: per-block PA trace written here (NULL: off; the context keeps a copy) */
 } me_tuning;
 me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* tuning);
 me_status me_b200_ctx_get_tuning(me_ctx* ctx, me_tuning* out);

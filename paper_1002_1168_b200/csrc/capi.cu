@@ -322,7 +322,10 @@ me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* t) {
         t->host_threads < 0)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "tuning field out of range");
     ctx->tuning = *t;
-    ctx->tune = mek::resolve_tuning(t);
+    // the caller's string need not outlive the call: keep a copy
+    ctx->trace_path = t->pa_trace_path ? t->pa_trace_path : "";
+    ctx->tuning.pa_trace_path = ctx->trace_path.empty() ? nullptr : ctx->trace_path.c_str();
+    ctx->tune = mek::resolve_tuning(&ctx->tuning);
     return ok();
 }
 

@@ -66,6 +66,7 @@ struct HostBuf {
 struct me_ctx {
     int device = 0;
     me_tuning tuning = {};  // as set by me_b200_ctx_set_tuning (zeros: defaults)
+    std::string trace_path; // the context's own copy of tuning.pa_trace_path
     mek::Tuning tune;       // resolved
     cudaStream_t stream = nullptr;
     int num_sms = 148;

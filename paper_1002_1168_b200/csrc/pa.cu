@@ -2069,7 +2069,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
                        : b.n_seq == 1      ? 1
                        : per_step < int64_t(num_sms) * 80 ? 2 : 4;
         fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
-        if (trace_path) fast = pa_fast_kernel<4, true>;
+        if (trace_path) fast = mb == 1 ? pa_fast_kernel<1, true> : mb == 2 ? pa_fast_kernel<2, true> : pa_fast_kernel<4, true>;
     }
     const int duo_threads = t.pa_duo_threads == 128 ? 128 : 256;
     PaKernel duo = pa_duo_kernel<256, 4>;

@@ -17,7 +17,10 @@ for n in [int(x) for x in (sys.argv[1:] or ["16", "32", "64", "128"])]:
     res = {}
     for name, kw in (("auto", {}), ("fast1", dict(pa_schedule="fast", pa_fast_ctas=1)), ("fast2", dict(pa_schedule="fast", pa_fast_ctas=2)),
                      ("fast4", dict(pa_schedule="fast", pa_fast_ctas=4)), ("hybrid", dict(pa_schedule="hybrid")),
-                     ("hybrid-w20", dict(pa_schedule="hybrid", pa_wide_blocks=20 * 148))):
+                     ("hybrid-w20", dict(pa_schedule="hybrid", pa_wide_blocks=20 * 148)),
+                     ("hybrid-w10", dict(pa_schedule="hybrid", pa_wide_blocks=10 * 148)),
+                     ("duo", dict(pa_schedule="duo")), ("duo-hybrid", dict(pa_schedule="duo-hybrid")),
+                     ("duo-hybrid-w10", dict(pa_schedule="duo-hybrid", pa_wide_blocks=10 * 148))):
         _lib.set_tuning(0, **kw)
         for _ in range(3):
             B.run_sequences_dev(cfg, luma, alpha, recs, stats)
