@@ -143,6 +143,8 @@ typedef struct me_tuning {
                                  0: in-order CTA-batch claiming */
     int32_t pa_no_pdl;        /* 1: launch the hybrid's grids in plain stream order */
     int32_t pa_no_smem_pair;  /* 1: never use the one-CTA shared-memory kernel for a small pair */
+    int32_t pa_fast_patches;  /* 1: pa_fast_kernel stages per-candidate patches after the dependency
+                                 wait instead of the whole search window before it (S <= 32) */
     int32_t pa_key_a, pa_key_s; /* wavefront sort key a * (h + 2v + p) + s * seq (0: 1 and 0) */
     int32_t sort_no_pdl;      /* 1: scan and fill in plain stream order */
     int32_t fill_rows;        /* 1: a thread per block row, -1: a thread per block (0: by size) */

@@ -79,6 +79,7 @@ Tuning resolve_tuning(const me_tuning* u) {
     t.pa_claim = !u->pa_static_claim;
     t.pa_pdl = !u->pa_no_pdl;
     t.pa_smem_pair = !u->pa_no_smem_pair;
+    t.pa_fast_window = !u->pa_fast_patches;
     if (u->pa_key_a) t.key_a = u->pa_key_a;
     t.key_s = u->pa_key_s;
     t.sort_pdl = !u->sort_no_pdl;

@@ -52,6 +52,7 @@ struct Tuning {
     bool pa_claim = true;    // in-order CTA-batch claiming
     bool pa_pdl = true;
     bool pa_smem_pair = true;
+    bool pa_fast_window = true;  // pa_fast_kernel stages the whole search window at claim time (S <= 32)
     int key_a = 1, key_s = 0;
     bool sort_pdl = true;
     int fill_rows = 0;       // 1 a thread per row, -1 a thread per block, 0 by size

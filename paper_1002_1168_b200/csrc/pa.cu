@@ -263,6 +263,7 @@ struct PaArgs {
     me_pair_stats* stats;
     int fast;              // patch fast path allowed (step 2, max_iter <= 4)
     int warp_words;        // shared words per warp
+    int win_words;         // pa_fast_kernel: row stride (words) of the staged search window, 0 = per-candidate patches
     int poll_ns;           // dependency poll interval
     int pdl;               // hybrid launches chained by programmatic dependent launch (see PdlScope)
     const int* range;      // [begin, end) of the list for this launch (device) or null: [0, *nlist)
@@ -673,9 +674,15 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
     const PdlScope pdl_scope(a.pdl);
     extern __shared__ uint32_t s_pa[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t* ws = s_pa + wid * kFastWarpWords;
-    uint32_t* patch = ws;                    // [4][16][12]
-    uint32_t* cw = ws + 4 * kFastPatch;      // [8][2] current block
+    // window mode (a.win_words): the block's whole clipped search window
+    // (+4 rows / columns for the walk's neighbours) is staged at claim time,
+    // while the dependencies are awaited, so no load is left between the
+    // dependencies' arrival and the search; else per-candidate patches
+    const int wsw = a.win_words;
+    const int area = a.warp_words - 20;      // patches or window, then cw and visited
+    uint32_t* ws = s_pa + wid * a.warp_words;
+    uint32_t* patch = ws;                    // [4][16][12] or [rows][wsw]
+    uint32_t* cw = ws + area;                // [8][2] current block
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     const int beg = a.range ? a.range[0] : 0, n = a.range ? a.range[1] : *a.nlist;
     const int W = a.b.W, H = a.b.H, S = a.P.S;
@@ -724,6 +731,28 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             const bool in = cs >= 0 && cs + 16 <= W;
             cp_async16(patch + slot * kFastPatch + r * kFastPWW + 4 * ch, in ? rowp + cs : rowp, in);
         };
+        // window mode: frame row wy0 / 16-aligned column cs0 are the window's origin
+        int wy0 = 0, cs0 = 0;
+        if (wsw) {
+            wy0 = y0 + (lo_y >> 1) - 4;
+            cs0 = (x0 + (lo_x >> 1) - 4) & ~15;
+            const int nch = ((((x0 + (hi_x >> 1) - 4) & ~15) + 32) - cs0) >> 4, nr = ((hi_y - lo_y) >> 1) + 16;
+            const float inv_nch = 1.0f / float(nch);
+            for (int i = lane; i < nr * nch; i += 32) {
+                // row by a float reciprocal: exact, (i + 0.5) / nch is never within 0.5 / nch of an integer
+                const int r = __float2int_rz((float(i) + 0.5f) * inv_nch), ch = i - r * nch;
+                const int y = clampi(wy0 + r, 0, H - 1), col = cs0 + 16 * ch;
+                const uint8_t* rowp = a.b.luma + (oref + uint32_t(y) * W);
+                const bool in = col >= 0 && col + 16 <= W;
+                cp_async16(patch + r * wsw + 4 * ch, in ? rowp + col : rowp, in);
+            }
+        }
+        const int PWW = wsw ? wsw : kFastPWW;
+        // a candidate's patch view: row 0 = frame row y0 + cpy - 4, word 0 = the
+        // 16-aligned column at or left of x0 + cpx - 4
+        auto pbase = [&](int slot, int cpx, int cpy) -> const uint32_t* {
+            return wsw ? patch + (y0 + cpy - 4 - wy0) * wsw + ((((x0 + cpx - 4) & ~15) - cs0) >> 2) : patch + slot * kFastPatch;
+        };
         uint32_t mvw = 0;
         bool b_early;
         {
@@ -741,7 +770,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             // B lies two wavefront steps back and is usually final already: its
             // patch (slot 1) goes out before the wait for A, C and T
             const uint32_t mb = __shfl_sync(0xFFFFFFFFu, mvw, 1);
-            b_early = mb != kSentinel;
+            b_early = mb != kSentinel && !wsw;
             if (b_early) stage(1, clip_comp(mv_dx(mb), lo_x, hi_x) >> 1, clip_comp(mv_dy(mb), lo_y, hi_y) >> 1);
             // warp-uniform wait (a vote per poll keeps the warp converged)
             while (__any_sync(0xFFFFFFFFu, back >= 0 && mvw == kSentinel)) {
@@ -762,9 +791,11 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         const uint32_t mine = __shfl_sync(0xFFFFFFFFu, mvw, c);
         const int myx = clip_comp(mv_dx(mine), lo_x, hi_x), myy = clip_comp(mv_dy(mine), lo_y, hi_y);
         // duplicate candidates share a patch: B's slot first (it may be staged
-        // already), else the first equal candidate's
+        // already), else the first equal candidate's.  Window mode needs no
+        // patch slots (and skips these dependent shuffles: the per-block
+        // latency is a chain of ~30-cycle shuffle / shared-memory steps)
         int md = c;
-        {
+        if (!wsw) {
             const int bx = __shfl_sync(0xFFFFFFFFu, myx, 8), by = __shfl_sync(0xFFFFFFFFu, myy, 8);
 #pragma unroll
             for (int j = 2; j >= 0; --j) {
@@ -772,14 +803,14 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                 if (j < c && jx == myx && jy == myy) md = j;
             }
             if (bx == myx && by == myy) md = 1;
-        }
-        // --- round B: the remaining distinct patches and the shape rows in flight
+            // --- round B: the remaining distinct patches and the shape rows in flight
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
-            const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
-            const bool own = __shfl_sync(0xFFFFFFFFu, md, 8 * cc) == cc;  // warp-uniform
-            if (own && !(cc == 1 && b_early)) stage(cc, ccx, ccy);
+            for (int cc = 0; cc < 4; ++cc) {
+                const int ccx = __shfl_sync(0xFFFFFFFFu, myx, 8 * cc) >> 1;
+                const int ccy = __shfl_sync(0xFFFFFFFFu, myy, 8 * cc) >> 1;
+                const bool own = __shfl_sync(0xFFFFFFFFu, md, 8 * cc) == cc;  // warp-uniform
+                if (own && !(cc == 1 && b_early)) stage(cc, ccx, ccy);
+            }
         }
         const bool shape = boundary && (c < 3 || a.P.bt_shape);
         uint2 cal = make_uint2(0u, 0u);
@@ -809,33 +840,28 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         if (!shape) {
             const int po = (x0 + (myx >> 1) - 4) & 15;
             uint32_t w0, w1;
-            prow8(patch + md * kFastPatch + (4 + sub) * kFastPWW, 4 + po, w0, w1);
+            prow8(pbase(md, myx >> 1, myy >> 1) + (4 + sub) * PWW, 4 + po, w0, w1);
             s = vad4(c1, w1, vad4(c0, w0, 0u)) * 4u;
         }
         s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
         s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
         s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
-        uint32_t best = __shfl_sync(0xFFFFFFFFu, s, 0);
-        int win = 0;
-#pragma unroll
-        for (int i = 1; i < 4; ++i) {
-            const uint32_t si = __shfl_sync(0xFFFFFFFFu, s, 8 * i);
-            if (si < best) {  // strict <: A, B, C, T tie order (:295)
-                best = si;
-                win = i;
-            }
-        }
+        // strict <: A, B, C, T tie order (:295) = the minimum of (score, candidate)
+        // (scores < 2^20), one warp reduction
+        const uint32_t bk = __reduce_min_sync(0xFFFFFFFFu, (s << 2) | uint32_t(c));
+        const uint32_t best = bk >> 2;
+        const int win = int(bk & 3u);
         const bool win_shape = boundary && (win < 3 || a.P.bt_shape);
         const int wx = __shfl_sync(0xFFFFFFFFu, myx, 8 * win), wy = __shfl_sync(0xFFFFFFFFu, myy, 8 * win);
         const int wp = __shfl_sync(0xFFFFFFFFu, md, 8 * win);
-        const uint32_t* pw = patch + wp * kFastPatch;
+        const uint32_t* pw = pbase(wp, wx >> 1, wy >> 1);
         const int wo = (x0 + (wx >> 1) - 4) & 15;  // the winner patch's byte offset
         // my two PRS rows of the block
         const uint32_t ra0 = cw[2 * q], ra1 = cw[2 * q + 1], rb0 = cw[2 * q + 8], rb1 = cw[2 * q + 9];
         uint32_t ccost = best;
         if (win_shape) {  // the centre's texture cost was not computed by BRS
             uint32_t w0, w1;
-            prow8(pw + (4 + sub) * kFastPWW, 4 + wo, w0, w1);
+            prow8(pw + (4 + sub) * PWW, 4 + wo, w0, w1);
             uint32_t t = c == 0 ? vad4(c1, w1, vad4(c0, w0, 0u)) : 0u;
             ccost = 4u * __reduce_add_sync(0xFFFFFFFFu, t);
         }
@@ -848,8 +874,8 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
             const int px = ci + kx, py = cj + ky;
             const bool adm = wx + 2 * px >= lo_x && wx + 2 * px <= hi_x && wy + 2 * py >= lo_y && wy + 2 * py <= hi_y;
             uint32_t w0, w1, w2, w3;
-            prow8(pw + (4 + py + q) * kFastPWW, 4 + px + wo, w0, w1);
-            prow8(pw + (8 + py + q) * kFastPWW, 4 + px + wo, w2, w3);
+            prow8(pw + (4 + py + q) * PWW, 4 + px + wo, w0, w1);
+            prow8(pw + (8 + py + q) * PWW, 4 + px + wo, w2, w3);
             uint32_t part = vad4(rb1, w3, vad4(rb0, w2, vad4(ra1, w1, vad4(ra0, w0, 0u))));
             part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
             part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
@@ -907,7 +933,7 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
         uint32_t se = 0;
         if (lane < 8) {
             uint32_t w0, w1;
-            prow8(pw + (4 + cj + lane) * kFastPWW, 4 + ci + wo, w0, w1);
+            prow8(pw + (4 + cj + lane) * PWW, 4 + ci + wo, w0, w1);
             se = sq4(cw[2 * lane + 1], w1, sq4(cw[2 * lane], w0, 0u));
         }
         se = __reduce_add_sync(0xFFFFFFFFu, se);
@@ -2008,6 +2034,17 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     pa_args.prev0 = prev0;
     pa_args.stats = stats;
     pa_args.fast = (pa_args.P.step == 2 && cfg.max_iterations <= 4) ? 1 : 0;
+    // pa_fast_kernel's staged search window: 2S + 16 rows of 16-byte chunks
+    // from the 16-aligned column at or left of x0 - S - 4 (at most
+    // (2S + 15) / 16 + 2 chunks), row stride padded by 4 words against bank
+    // conflicts between the lanes' rows
+    int fast_words = kFastWarpWords;
+    pa_args.win_words = 0;
+    if (t.pa_fast_window && cfg.search_range <= 32) {
+        const int S = cfg.search_range, wsw = 4 * ((2 * S + 15) / 16 + 2) + 4;
+        pa_args.win_words = wsw;
+        fast_words = std::max(4 * kFastPatch, (2 * S + 16) * wsw) + 20;
+    }
     pa_args.poll_ns = t.pa_poll_ns;
     pa_args.pdl = 0;
     pa_args.trace = nullptr;
@@ -2086,7 +2123,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         e = launch(b.bs == 8 ? pa_kernel<8> : pa_kernel<16>, 256,
                    b.bs == 8 ? WPatch<8>::WARP_WORDS : WPatch<16>::WARP_WORDS, nullptr);
     } else if (pa_mode == 1) {
-        e = launch(fast, 256, kFastWarpWords, nullptr);
+        e = launch(fast, 256, fast_words, nullptr);
     } else if (pa_mode == 2) {
         e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, nullptr);
     } else if (pa_mode == 4) {  // narrow steps -> fast, the wide middle -> quad, narrow tail -> fast
@@ -2095,13 +2132,13 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         const int mb = t.pa_quad_ctas;
         PaKernel quad = mb == 4 ? pa_quad_kernel<4> : mb == 2 ? pa_quad_kernel<2> : pa_quad_kernel<3>;
         if (trace_path) quad = pa_quad_kernel<3, true>;
-        if (!(e = launch(fast, 256, kFastWarpWords, ranges, t.sort_pdl, t.sort_pdl)) &&
+        if (!(e = launch(fast, 256, fast_words, ranges, t.sort_pdl, t.sort_pdl)) &&
             !(e = launch(quad, 256, kQuadWarpWords, ranges + 2, true)))
-            e = launch(fast, 256, kFastWarpWords, ranges + 4, true);
+            e = launch(fast, 256, fast_words, ranges + 4, true);
     } else {  // narrow steps -> fast, the wide middle -> duo, narrow tail -> fast
-        if (!(e = launch(fast, 256, kFastWarpWords, ranges)) &&
+        if (!(e = launch(fast, 256, fast_words, ranges)) &&
             !(e = launch(duo, trace_path ? 256 : duo_threads, kDuoWarpWords, ranges + 2)))
-            e = launch(fast, 256, kFastWarpWords, ranges + 4);
+            e = launch(fast, 256, fast_words, ranges + 4);
     }
     if (e) return e;
     if (trace_path) {

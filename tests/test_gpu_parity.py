@@ -312,14 +312,16 @@ def test_concurrent_host_threads(me_gpu, port):
         assert np.array_equal(stats[0], want_s)
 
 
-@pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid"])
+@pytest.mark.parametrize("mode", ["fast", "fast-patches", "duo", "duo-hybrid", "hybrid"])
 @pytest.mark.parametrize("shape", [(16, 16), (48, 32), (64, 80)])
 def test_pa_kernel_modes_small_frames(me_gpu, port, mode, shape, tuning):
     """Every PA schedule on frames a few blocks wide (patches clipped by every
     frame edge, windows smaller than the search range), with masks mixing
-    transparent, opaque and boundary blocks and strong motion."""
+    transparent, opaque and boundary blocks and strong motion; `fast-patches`
+    is pa_fast_kernel with per-candidate patches instead of the staged window."""
     H, W = shape
-    tuning(pa_schedule=mode, pa_wide_blocks=1, pa_no_smem_pair=1)  # the batched kernels, not the one-CTA pair kernel
+    patches = mode == "fast-patches"
+    tuning(pa_schedule="fast" if patches else mode, pa_wide_blocks=1, pa_no_smem_pair=1, pa_fast_patches=int(patches))
     rng = np.random.default_rng(H * 1000 + W)
     n_seq, F = 6, 5
     base = noise(rng, H + 40, W + 40)
