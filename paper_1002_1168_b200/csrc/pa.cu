@@ -264,6 +264,7 @@ struct PaArgs {
     int fast;              // patch fast path allowed (step 2, max_iter <= 4)
     int warp_words;        // shared words per warp
     int win_words;         // pa_fast_kernel: row stride (words) of the staged search window, 0 = per-candidate patches
+    int awin_words;        // ... and of the boundary blocks' staged reference-alpha window (byte masks), 0 = off
     int poll_ns;           // dependency poll interval
     int pdl;               // hybrid launches chained by programmatic dependent launch (see PdlScope)
     const int* range;      // [begin, end) of the list for this launch (device) or null: [0, *nlist)
@@ -747,6 +748,27 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                 cp_async16(patch + r * wsw + 4 * ch, in ? rowp + col : rowp, in);
             }
         }
+        // boundary blocks (byte masks, window mode): the reference alpha over
+        // the candidates' reach (rows y0 + lo_y/2 .. y0 + hi_y/2 + 7, the same
+        // for columns) and this lane's current alpha row, also before the wait
+        const int awsw = a.awin_words;
+        uint32_t* awin = patch + (2 * S + 16) * wsw;
+        int wya0 = 0, csa0 = 0;
+        uint2 cal_pre = make_uint2(0u, 0u);
+        if (awsw && boundary) {
+            wya0 = y0 + (lo_y >> 1);
+            csa0 = (x0 + (lo_x >> 1)) & ~15;
+            const int nch = (((x0 + (hi_x >> 1) + 8 + 15) & ~15) - csa0) >> 4, nr = ((hi_y - lo_y) >> 1) + 8;
+            const float inv_nch = 1.0f / float(nch);
+            for (int i = lane; i < nr * nch; i += 32) {
+                const int r = __float2int_rz((float(i) + 0.5f) * inv_nch), ch = i - r * nch;
+                const int col = csa0 + 16 * ch;
+                const uint8_t* rowp = a.b.alpha + (oref + uint32_t(wya0 + r) * W);
+                const bool in = col >= 0 && col + 16 <= W;
+                cp_async16(awin + r * awsw + 4 * ch, in ? rowp + col : rowp, in);
+            }
+            cal_pre = __ldg(reinterpret_cast<const uint2*>(a.b.alpha + (ocur + uint32_t(y0 + sub) * W + uint32_t(x0))));
+        }
         const int PWW = wsw ? wsw : kFastPWW;
         // a candidate's patch view: row 0 = frame row y0 + cpy - 4, word 0 = the
         // 16-aligned column at or left of x0 + cpx - 4
@@ -821,13 +843,17 @@ __global__ void __launch_bounds__(256, MINB) pa_fast_kernel(const PaArgs a) {
                 const uint8_t* cb = a.b.alpha_bits + (ocur >> 3);
                 const uint8_t* rb = a.b.alpha_bits + (oref >> 3);
                 xbits = mask_bits8(cb, wb, x0, y0 + sub) ^ mask_bits8(rb, wb, x0 + (myx >> 1), y0 + sub + (myy >> 1));
-            } else {
+            } else if (!awsw) {
                 const uint32_t ao = uint32_t(y0 + sub) * W + uint32_t(x0);
                 cal = __ldg(reinterpret_cast<const uint2*>(a.b.alpha + (ocur + ao)));
                 ld8u(a.b.alpha + (oref + ao + uint32_t((myy >> 1) * W + (myx >> 1))), ral0, ral1);
             }
         }
         cp_async_wait_all();
+        if (shape && awsw) {  // from the staged alpha window
+            cal = cal_pre;
+            prow8(awin + (y0 + sub + (myy >> 1) - wya0) * awsw, x0 + (myx >> 1) - csa0, ral0, ral1);
+        }
         // shape scores (boundary blocks): my candidate, my row
         uint32_t s = 0;
         if (shape)
@@ -2040,11 +2066,19 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
     // conflicts between the lanes' rows
     int fast_words = kFastWarpWords;
     pa_args.win_words = 0;
-    if (t.pa_fast_window && cfg.search_range <= 32) {
+    pa_args.awin_words = 0;
+    auto set_window = [&](int ctas_per_sm) {
+        if (!t.pa_fast_window || cfg.search_range > 32) return;
         const int S = cfg.search_range, wsw = 4 * ((2 * S + 15) / 16 + 2) + 4;
         pa_args.win_words = wsw;
-        fast_words = std::max(4 * kFastPatch, (2 * S + 16) * wsw) + 20;
-    }
+        int words = (2 * S + 16) * wsw;
+        // the boundary blocks' alpha window when the shared memory allows (<= 2 CTAs per SM)
+        if (b.alpha && !b.alpha_bits && ctas_per_sm <= 2) {
+            pa_args.awin_words = 4 * ((2 * S + 8 + 15) / 16 + 1) + 4;
+            words += (2 * S + 8) * pa_args.awin_words;
+        }
+        fast_words = std::max(4 * kFastPatch, words) + 20;
+    };
     pa_args.poll_ns = t.pa_poll_ns;
     pa_args.pdl = 0;
     pa_args.trace = nullptr;
@@ -2106,6 +2140,7 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
                        : b.n_seq == 1      ? 1
                        : per_step < int64_t(num_sms) * 80 ? 2 : 4;
         fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
+        set_window(mb);
         if (trace_path) fast = mb == 1 ? pa_fast_kernel<1, true> : mb == 2 ? pa_fast_kernel<2, true> : pa_fast_kernel<4, true>;
     }
     const int duo_threads = t.pa_duo_threads == 128 ? 128 : 256;

@@ -37,6 +37,11 @@ print("tasks", len(tr), "span us %.1f" % done.max(), "steps", step.max() + 1)
 cyc = np.stack([(tr[:, 3] >> (16 * i)) & 0xFFFF for i in range(4)], 1).astype(np.float64)
 for i, name in enumerate(["ready->staged", "staged->brs", "brs->walked", "walked->published"]):
     print("cycles %-18s mean %7.0f p50 %7.0f p90 %7.0f" % (name, cyc[:, i].mean(), *np.percentile(cyc[:, i], [50, 90])))
+bnd = (lst[:, 0] >> 31).astype(bool)
+for flag, name in ((False, "opaque"), (True, "boundary")):
+    m = bnd == flag
+    if m.any():
+        print("  %-8s blocks %6d  ready->staged mean %6.0f  staged->brs %6.0f  brs->walked %6.0f" % (name, m.sum(), cyc[m, 0].mean(), cyc[m, 1].mean(), cyc[m, 2].mean()))
 print("work (ready->done) us: mean %.2f p50 %.2f p90 %.2f p99 %.2f" % ((done - ready).mean(), *np.percentile(done - ready, [50, 90, 99])))
 print("claim->ready us:       mean %.2f p50 %.2f p90 %.2f" % ((ready - claim).mean(), *np.percentile(ready - claim, [50, 90])))
 late = ready[has] - dmax[has]
