@@ -154,6 +154,10 @@ typedef struct me_tuning {
     int32_t ring_ctas;        /* CTAs per SM of the TSS/FSS/DS kernel, 2..4 (0: 3) */
     int32_t host_threads;     /* host-buffer path: threads packing the masks (0: OpenMP default) */
     const char* pa_trace_path;/* debug: per-block PA trace written here (NULL: off; the context keeps a copy) */
+    int32_t pa_key_plain;     /* 1: PA list keyed by the plain step t = h + 2v + p (with pa_key_a / pa_key_s);
+                                 0: batches of <= 60000 blocks per step keyed by t - tmin(sequence), every
+                                 sequence's wavefront starting at key 0 (wider batches: t);
+                                 -1: t - tmin(sequence) at any width */
 } me_tuning;
 me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* tuning);
 me_status me_b200_ctx_get_tuning(me_ctx* ctx, me_tuning* out);

@@ -63,7 +63,7 @@ class MeTuning(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "pa_schedule", "pa_wide_blocks", "pa_fast_ctas", "pa_quad_ctas", "pa_duo_threads", "pa_duo_ctas", "pa_poll_ns",
         "pa_static_claim", "pa_no_pdl", "pa_no_smem_pair", "pa_fast_patches", "pa_key_a", "pa_key_s", "sort_no_pdl", "fill_rows",
-        "fill_rows_per_cta", "h2d_chunks", "mask_pack", "ring_ctas", "host_threads")] + [("pa_trace_path", C.c_char_p)]
+        "fill_rows_per_cta", "h2d_chunks", "mask_pack", "ring_ctas", "host_threads")] + [("pa_trace_path", C.c_char_p), ("pa_key_plain", C.c_int32)]
 
 
 PA_SCHEDULES = {"auto": 0, "warp": 1, "generic": 1, "fast": 2, "duo": 3, "duo-hybrid": 4, "hybrid": 5, "quad": 5}

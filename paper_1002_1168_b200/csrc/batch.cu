@@ -23,6 +23,8 @@ struct Scratch {
     int* offs;
     int* cursor;
     int* counter;
+    int* hist2;  // aligned PA keys: [n_seq][nbins] per-(sequence, step) counts, then tmin [n_seq]
+    int* tmin;
 };
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
@@ -42,6 +44,10 @@ Scratch carve(const Batch& b, int nbins, void* base) {
     s.cursor = reinterpret_cast<int*>(p);
     p += align_up(size_t(nbins) * 4 * kCursorStride);
     s.counter = reinterpret_cast<int*>(p);
+    p += 256;
+    s.hist2 = reinterpret_cast<int*>(p);
+    p += align_up(size_t(b.n_seq) * nbins * 4);
+    s.tmin = reinterpret_cast<int*>(p);
     return s;
 }
 
@@ -55,7 +61,21 @@ struct KeyParams {
     int a, s;
 };
 
+// Aligned keys pay off where the batch's lockstep step count sets the time
+// (latency-bound wavefronts: cfg4 at 32 / 64 / 128 sequences, -5 / -9 / -4 %);
+// at 256 the search is throughput-bound (-1 %) and the extra per-(sequence,
+// step) counting in classify and the scan (+0.02 ms) outweighs it.  A single
+// sequence has nothing to align.
+bool pa_key_aligned(const Batch& b, const Tuning& t) {
+    if (!t.key_align || b.n_seq < 2) return false;
+    if (t.key_align_max_blocks_per_step >= 0 &&
+        b.nblocks() > int64_t(t.key_align_max_blocks_per_step) * b.steps())
+        return false;
+    return int64_t(b.n_seq) * b.steps() <= (int64_t(1) << 24) && b.steps() + b.n_seq <= 48 * 1024;
+}
+
 KeyParams pa_key(const Batch& b, const Tuning& t) {
+    if (pa_key_aligned(b, t)) return KeyParams{1, 0};  // key = t - tmin[seq] in [0, steps)
     KeyParams k{std::max(1, t.key_a), std::max(0, t.key_s)};
     if (int64_t(k.a) * (b.steps() - 1) + int64_t(k.s) * (b.n_seq - 1) + 1 > 12288) k = KeyParams{1, 0};
     return k;
@@ -82,6 +102,8 @@ Tuning resolve_tuning(const me_tuning* u) {
     t.pa_fast_window = !u->pa_fast_patches;
     if (u->pa_key_a) t.key_a = u->pa_key_a;
     t.key_s = u->pa_key_s;
+    t.key_align = u->pa_key_plain != 1;
+    if (u->pa_key_plain == -1) t.key_align_max_blocks_per_step = -1;  // -1: aligned at any batch width
     t.sort_pdl = !u->sort_no_pdl;
     t.fill_rows = u->fill_rows;
     if (u->fill_rows_per_cta) t.fill_rows_per_cta = u->fill_rows_per_cta;
@@ -97,7 +119,8 @@ size_t scratch_bytes(const Batch& b, int algo, const Tuning& t) {
     const int nbins = algo == ME_ALGO_PA ? pa_bins(b, t) : 1;
     const size_t nb = size_t(b.nblocks());
     return align_up(nb) + align_up((nb + 3 * size_t(nbins)) * 8) + align_up(size_t(nbins) * 4) +
-           align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4 * kCursorStride) + 256;
+           align_up(size_t(nbins + 1) * 4) + align_up(size_t(nbins) * 4 * kCursorStride) + 256 +
+           align_up(size_t(b.n_seq) * nbins * 4) + align_up(size_t(b.n_seq) * 4);
 }
 
 // 0: pa_kernel (generic), 1: pa_fast_kernel, 2: pa_duo_kernel, 3: fast / duo /
@@ -137,7 +160,13 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     if (scratch_size < scratch_bytes(b, algo, tune)) return cudaErrorInvalidValue;
     Scratch s = carve(b, nbins, scratch);
     cudaError_t e;
-    if ((e = cudaMemsetAsync(s.hist, 0, size_t(nbins) * 4, st))) return e;
+    // aligned keys (PA): every sequence's wavefront starts at key 0 — the list
+    // interleaves the sequences by their own progress instead of the batch's
+    // absolute step, so the batch has max(span) instead of max(end) - min(start)
+    // lockstep steps (all dependencies stay within a sequence, hence earlier)
+    const bool align = pa && pa_key_aligned(b, tune);  // (the scan holds the key histogram + tmin in shared memory)
+    if ((e = cudaMemsetAsync(align ? s.hist2 : s.hist, 0, size_t(align ? b.n_seq : 1) * nbins * 4, st))) return e;
+    if (align && (e = cudaMemsetAsync(s.tmin, 0x7F, size_t(b.n_seq) * 4, st))) return e;
     if ((e = cudaMemsetAsync(s.counter, 0, 16, st))) return e;  // ES ticket + the PA launches' claim counters
     if (stats && (e = cudaMemsetAsync(stats, 0, sizeof(me_pair_stats) * size_t(b.n_seq) * b.pairs, st)))
         return e;
@@ -155,6 +184,9 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         const KeyParams k = pa_key(b, tune);
         ca.key_a = k.a;
         ca.key_s = k.s;
+        ca.hist2 = align ? s.hist2 : nullptr;
+        ca.tmin = align ? s.tmin : nullptr;
+        ca.tmin_g = align ? s.tmin : nullptr;
     }
     {
         NvtxRange nv("me_b200/classify");
@@ -169,7 +201,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     {
         NvtxRange nv("me_b200/sort");
         if ((e = launch_scan(s.hist, nbins, pa_mode == 4 ? 4 : pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
-                             pa_wide_threshold(num_sms, tune), ranges, st, tune.sort_pdl)))
+                             pa_wide_threshold(num_sms, tune), ranges, st, tune.sort_pdl, ca.hist2, b.n_seq,
+                             s.tmin)))
             return e;
         if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st, tune))) return e;
     }

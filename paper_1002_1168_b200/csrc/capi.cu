@@ -319,7 +319,7 @@ me_status me_b200_ctx_set_tuning(me_ctx* ctx, const me_tuning* t) {
         (t->pa_duo_threads && t->pa_duo_threads != 128 && t->pa_duo_threads != 256) || t->pa_poll_ns < 0 ||
         t->pa_key_a < 0 || t->pa_key_s < 0 || t->fill_rows_per_cta < 0 || t->h2d_chunks < 0 || t->h2d_chunks > 32 ||
         t->mask_pack < 0 || t->mask_pack > 3 || t->ring_ctas < 0 || t->ring_ctas == 1 || t->ring_ctas > 4 ||
-        t->host_threads < 0)
+        t->host_threads < 0 || t->pa_key_plain < -1 || t->pa_key_plain > 1)
         return me_fail(ME_ERR_INVALID_ARGUMENT, "tuning field out of range");
     ctx->tuning = *t;
     // the caller's string need not outlive the call: keep a copy

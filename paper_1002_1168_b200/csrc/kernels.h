@@ -54,6 +54,8 @@ struct Tuning {
     bool pa_smem_pair = true;
     bool pa_fast_window = true;  // pa_fast_kernel stages the whole search window at claim time (S <= 32)
     int key_a = 1, key_s = 0;
+    bool key_align = true;   // PA batches: key = t - tmin[seq] (sequences' wavefronts aligned at their first estimated block)
+    int key_align_max_blocks_per_step = 60000;  // ... up to this many blocks per lockstep step (-1: any)
     bool sort_pdl = true;
     int fill_rows = 0;       // 1 a thread per row, -1 a thread per block, 0 by size
     int fill_rows_per_cta = 64;

@@ -28,13 +28,24 @@ struct ClassArgs {
     int nbins;
     me_pair_stats* stats;  // [n_seq][pairs]: transparent blocks' count and SSE
     int key_a, key_s;      // PA: key = key_a * (h + 2v + p) + key_s * seq (sequence stagger)
+    // PA, aligned keys (key = t - tmin[seq], tmin = the sequence's first step
+    // holding an estimated block): classify counts estimated blocks per
+    // (sequence, step) into hist2 [n_seq][steps]; the scan derives tmin and the
+    // key histogram; the fill reads tmin.  Null: the key_a / key_s key.
+    int* hist2;
+    const int* tmin;  // fill: the keys' offsets (written by the scan)
+    int* tmin_g;      // classify: atomicMin target (the same array, preset to 0x7F7F7F7F)
 };
 
 // wavefront.cu: classify -> per-step histogram -> scan -> fill (the sorted list)
 cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st);
 // (pdl: scan, fill and the PA head chained by programmatic dependent launch)
+// (hist2 / tmin non-null: aligned keys, hist2 [n_seq][nbins] is reduced into the key histogram
+// with tmin [n_seq] from classify (0x7F7F7F7F for a sequence without estimated blocks: 0 is
+// written back); hist is then unused)
 cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
-                        int wide, int* ranges, cudaStream_t st, bool pdl);
+                        int wide, int* ranges, cudaStream_t st, bool pdl, const int* hist2 = nullptr,
+                        int n_seq = 0, int* tmin = nullptr);
 cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_sms, cudaStream_t st,
                         const Tuning& t);
 

@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
     pdl_allow_next();
     constexpr int NB = 16 / BS;  // blocks per strip
     const Batch& b = a.b;
-    for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
+    if (!a.hist2)
+        for (int i = threadIdx.x; i < a.nbins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const int strips = b.cols / NB;  // strips per block row
     const int64_t n = int64_t(b.n_seq) * b.pairs * b.rows * strips;
@@ -69,6 +70,9 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
         const int64_t si = s0 + threadIdx.x;
         uint32_t sse = 0, n_t = 0, n_o = 0, n_b = 0;
         int64_t gp = -1;
+        int hkey[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) hkey[k] = -1;
         if (si < n) {
             const int hs = int(si % strips);
             int64_t t = si / strips;
@@ -90,6 +94,9 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             const uint8_t* abits = BITS ? b.alpha_bits + (fcur * plane + off) / 8 : nullptr;
             const uint8_t* cc = b.luma + fcur * plane + off;
             const uint8_t* rc = b.luma + fref * plane + off;
+            int ty_[NB];
+            uint32_t s_[NB];
+            {
             uint4 al[BS], cu[BS], re[BS];
             uint32_t ab[BS];  // bit rows (all loads of the strip are issued before any is used)
 #pragma unroll
@@ -135,7 +142,14 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
                         }
                     }
                 }
-                const int ty = !any ? ME_TRANSPARENT : (nz ? ME_OPAQUE : ME_BOUNDARY);
+                ty_[k] = !any ? ME_TRANSPARENT : (nz ? ME_OPAQUE : ME_BOUNDARY);
+                s_[k] = s;
+            }
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const int ty = ty_[k];
+                const uint32_t s = s_[k];
                 const int h = hs * NB + k;
                 const int64_t g = (gp * b.rows + v) * b.cols + h;
                 a.types[g] = uint8_t(ty);
@@ -146,7 +160,10 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
                 r.w = uint32_t(ty) << 8;
                 *reinterpret_cast<uint4*>(a.recs + g) = r;
                 if (ty != ME_TRANSPARENT) {
-                    atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
+                    if (a.hist2)  // aligned keys: per (sequence, step) counts, added below
+                        hkey[k] = seq * a.nbins + (h + 2 * v + p);
+                    else
+                        atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
                     n_o += ty == ME_OPAQUE;
                     n_b += ty == ME_BOUNDARY;
                 } else {
@@ -157,6 +174,21 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             }
         }
     next:
+        if (a.hist2) {  // one atomic per distinct (sequence, step) of the warp, and the sequences' first steps
+            int tm = 0x7FFFFFFF, sq = -1;
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const unsigned m = __match_any_sync(0xFFFFFFFFu, hkey[k]);
+                if (hkey[k] >= 0 && lane == __ffs(m) - 1) atomicAdd(&a.hist2[hkey[k]], __popc(m));
+                if (hkey[k] >= 0) {
+                    sq = hkey[k] / a.nbins;
+                    tm = min(tm, hkey[k] - sq * a.nbins);
+                }
+            }
+            const unsigned ms = __match_any_sync(0xFFFFFFFFu, sq);
+            tm = __reduce_min_sync(ms, tm);
+            if (sq >= 0 && lane == __ffs(ms) - 1) atomicMin(a.tmin_g + sq, tm);
+        }
         if (a.stats) {
             const int64_t gp0 = __shfl_sync(0xFFFFFFFFu, gp, 0);
             const bool uniform = __all_sync(0xFFFFFFFFu, gp == gp0 || gp < 0);
@@ -184,6 +216,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             }
         }
     }
+    if (a.hist2) return;
     __syncthreads();
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x)
         if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
@@ -192,13 +225,44 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
 // Exclusive scan of hist into offs[0..nbins] (single CTA), cursor = offs.
 // ranges (optional): the list split at the first and after the last step
 // holding >= wide blocks: {0, b1}, {b1, b2}, {b2, total} (narrow, wide, narrow).
+// Aligned keys (hist2 non-null): a warp per sequence finds its first step
+// holding an estimated block (tmin) and adds its step counts, shifted down by
+// tmin, into the key histogram (shared memory) that the scan then reads.
 __global__ void scan_kernel(const int* hist, int nbins, int pad, int* offs, int* cursor,
-                            uint2* list, int wide, int* ranges) {
+                            uint2* list, int wide, int* ranges, const int* hist2, int n_seq, int* tmin) {
     pdl_wait_prev();
     pdl_allow_next();
     __shared__ int s_part[1024];
     __shared__ int s_lo, s_hi;  // first / last wide step
+    extern __shared__ int s_keyhist[];
     const int T = blockDim.x;
+    if (hist2) {
+        // two passes over hist2 with every thread's loads independent (the
+        // per-sequence warp loop was a chain of dependent L2 round trips)
+        int* s_tmin = s_keyhist + nbins;
+        for (int i = threadIdx.x; i < nbins; i += T) s_keyhist[i] = 0;
+        for (int i = threadIdx.x; i < n_seq; i += T) {
+            const int t0 = tmin[i];  // classify's atomicMin (0x7F7F7F7F: no estimated block)
+            s_tmin[i] = t0 < nbins ? t0 : 0;
+            tmin[i] = s_tmin[i];
+        }
+        __syncthreads();
+        const int total = n_seq * nbins;
+        constexpr int CH = 16;  // independent loads in flight per thread
+        for (int i0 = threadIdx.x; i0 < total; i0 += T * CH) {
+            int x[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) x[j] = i0 + j * T < total ? __ldcg(hist2 + i0 + j * T) : 0;
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                if (!x[j]) continue;
+                const int i = i0 + j * T, sq = i / nbins;
+                atomicAdd(&s_keyhist[i - sq * nbins - s_tmin[sq]], x[j]);
+            }
+        }
+        __syncthreads();
+        hist = s_keyhist;
+    }
     const int per = (nbins + T - 1) / T;
     const int lo = threadIdx.x * per, hi = min(lo + per, nbins);
     auto padded = [&](int v) { return (v + pad - 1) / pad * pad; };
@@ -291,7 +355,7 @@ __global__ void __launch_bounds__(256) fill_kernel(ClassArgs a, int* cursor, uin
             const uint32_t pr = r / uint32_t(b.rows), v = r - pr * uint32_t(b.rows);
             const uint32_t seq = pr / uint32_t(b.pairs), p = pr - seq * uint32_t(b.pairs);
             {
-                const int key = a.pa ? a.key_a * int(h + 2 * v + p) + a.key_s * int(seq) : 0;
+                const int key = !a.pa ? 0 : a.tmin ? int(h + 2 * v + p) - a.tmin[seq] : a.key_a * int(h + 2 * v + p) + a.key_s * int(seq);
                 if (pass == 0) {
                     atomicAdd(&s_cnt[key], 1);
                 } else {
@@ -334,7 +398,8 @@ __global__ void __launch_bounds__(256) fill_rows_kernel(ClassArgs a, int* cursor
         p = pr - seq * uint32_t(b.pairs);
     }
     const uint8_t* types = a.types + size_t(r) * cols;
-    const int key0 = a.pa ? a.key_a * int(2 * v + p) + a.key_s * int(seq) : 0, kstep = a.pa ? a.key_a : 0;
+    const int key0 = !a.pa ? 0 : a.tmin ? (live ? int(2 * v + p) - a.tmin[seq] : 0) : a.key_a * int(2 * v + p) + a.key_s * int(seq);
+    const int kstep = a.pa ? (a.tmin ? 1 : a.key_a) : 0;
     // rows of a multiple of 4 blocks (cfg4: 44) are read as words, and a word
     // of four transparent blocks (ME_TRANSPARENT = 0: most of them) is skipped whole
     const bool words = (cols & 3u) == 0;
@@ -406,7 +471,7 @@ cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
     const int64_t strips = b.nblocks() / (16 / b.bs);
     int grid = int(std::min<int64_t>((strips + threads - 1) / threads, int64_t(num_sms) * 8));
     if (grid < 1) grid = 1;
-    const size_t hist_smem = size_t(ca.nbins) * 4;
+    const size_t hist_smem = ca.hist2 ? 0 : size_t(ca.nbins) * 4;
     const bool bits = b.alpha_bits != nullptr;
     if (b.bs == 8)
         (bits ? classify_kernel<8, true> : classify_kernel<8, false>)<<<grid, threads, hist_smem, st>>>(ca);
@@ -416,14 +481,21 @@ cudaError_t launch_classify(const ClassArgs& ca, int num_sms, cudaStream_t st) {
 }
 
 cudaError_t launch_scan(const int* hist, int nbins, int pad, int* offs, int* cursor, uint2* list,
-                        int wide, int* ranges, cudaStream_t st, bool pdl) {
+                        int wide, int* ranges, cudaStream_t st, bool pdl, const int* hist2, int n_seq,
+                        int* tmin) {
+    const size_t smem = hist2 ? size_t(nbins + n_seq) * 4 : 0;
+    cudaError_t e;
+    if (smem > 40 * 1024 &&
+        (e = cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
+        return e;
     if (pdl) {
-        cudaLaunchConfig_t lc = pdl_config(dim3(1), dim3(1024), 0, st);
+        cudaLaunchConfig_t lc = pdl_config(dim3(1), dim3(1024), smem, st);
         cudaLaunchAttribute at[1];
         pdl_attr(lc, at);
-        return cudaLaunchKernelEx(&lc, scan_kernel, hist, nbins, pad, offs, cursor, list, wide, ranges);
+        return cudaLaunchKernelEx(&lc, scan_kernel, hist, nbins, pad, offs, cursor, list, wide, ranges, hist2,
+                                  n_seq, tmin);
     }
-    scan_kernel<<<1, 1024, 0, st>>>(hist, nbins, pad, offs, cursor, list, wide, ranges);
+    scan_kernel<<<1, 1024, smem, st>>>(hist, nbins, pad, offs, cursor, list, wide, ranges, hist2, n_seq, tmin);
     return cudaGetLastError();
 }
 

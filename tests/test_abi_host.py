@@ -158,3 +158,29 @@ def test_pack_mask_roundtrip(n):
     assert L.me_b200_pack_mask(gray.ctypes.data, n, out.ctypes.data, cap, C.byref(nb)) == _lib.ME_ERR_INVALID_ARGUMENT
     assert "binary" in L.me_b200_last_error().decode()
     assert L.me_b200_pack_mask(mask.ctypes.data, n - 8, out.ctypes.data, cap, C.byref(nb)) == _lib.ME_ERR_INVALID_ARGUMENT
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The ctypes mirrors of the C ABI structs (_lib) have the header's size and
+    field offsets (gcc on include/me_b200.h)."""
+    import ctypes as C
+    import subprocess
+
+    from paper_1002_1168_b200 import _lib
+
+    structs = {"me_tuning": _lib.MeTuning, "me_config": _lib.MeConfig}
+    src = ['#include <stddef.h>', '#include <stdio.h>', '#include "me_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        src.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            src.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src.append("return 0; }")
+    (tmp_path / "l.c").write_text("\n".join(src))
+    inc = os.path.join(ROOT, "include")
+    subprocess.run(["gcc", "-I", inc, str(tmp_path / "l.c"), "-o", str(tmp_path / "l")], check=True)
+    got = subprocess.run([str(tmp_path / "l")], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, got):
+        cname, field, val = line.split()
+        py = structs[cname]
+        want = C.sizeof(py) if field == "size" else getattr(py, field).offset
+        assert int(val) == want, f"{cname}.{field}: C {val} vs ctypes {want}"

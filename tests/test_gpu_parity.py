@@ -261,6 +261,29 @@ def tuning(me_gpu):
         _lib.restore_tuning(saved[0], 0)
 
 
+@pytest.mark.parametrize("key", [1, 0, -1])
+@pytest.mark.parametrize("mode", ["auto", "fast", "hybrid", "hybrid-static"])
+def test_pa_list_keys(me_gpu, port, mode, key, tuning):
+    """The PA list ordered by the plain wavefront step t = h + 2v + p
+    (pa_key_plain 1) or by t - tmin(sequence) (0: batches up to 60 000 blocks
+    per step, -1: any width): the same records and stats.  The batch mixes
+    sequences whose first estimated block comes at different steps, one
+    sequence without masks (every block opaque: tmin 0) and one whose masks are
+    empty (no estimated block: no tmin)."""
+    from paper_1002_1168_b200 import synth
+
+    tuning(pa_schedule=mode.split("-static")[0], pa_wide_blocks=4, pa_static_claim=int(mode.endswith("-static")), pa_key_plain=key)
+    luma, alpha = synth.config4_batch(7, 910, frames=8)
+    alpha[5] = 255
+    alpha[6] = 0
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in range(7):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"{mode} key {key} seq {i}")
+        assert np.array_equal(stats[i], want_s)
+
+
 @pytest.mark.parametrize("bt,it", [(0, 4), (1, 4), (0, 7)])
 @pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid", "warp", "hybrid-static"])
 def test_pa_kernel_modes(me_gpu, port, mode, bt, it, tuning):
@@ -800,7 +823,7 @@ def test_fuzz_batches(me_gpu, port, seed):
     what = f"batch fuzz {seed}: n_seq {len(luma)} { {k: v for k, v in c.items() if k not in ('luma', 'alpha')} }"
     rng = np.random.default_rng(seed)
     sched = str(rng.choice(["auto", "warp", "fast", "duo", "duo-hybrid", "hybrid"])) if c["algo"] == 4 else "auto"
-    prev = _lib.set_tuning(0, pa_schedule=sched, pa_static_claim=int(rng.random() < 0.2))
+    prev = _lib.set_tuning(0, pa_schedule=sched, pa_static_claim=int(rng.random() < 0.2), pa_key_plain=int(rng.integers(-1, 2)))
     try:
         recs, stats = me.run_sequences(cfg, luma, alpha)
         dl = torch.from_numpy(luma).cuda()
