@@ -60,42 +60,41 @@ for q in (10, 50, 90):
 # Critical chain: walk back from the last-published block through the dependency
 # that finished last, splitting the span into per-block work (start -> done, start
 # = max(claim, last dep done)) and claim waits (claim later than the last dep).
-if len(sys.argv) > 5 or True:
-    idx = np.full((nseq, pairs, rows, cols), -1, np.int64)
-    idx[seq, p, v, h] = np.arange(len(done))
-    i = int(np.argmax(done))
-    chain = []
-    while True:
-        chain.append(i)
-        cands = []
-        s_, p_, v_, h_ = seq[i], p[i], v[i], h[i]
-        for (pp, vv, hh) in ((p_, v_, h_ - 1), (p_, v_ - 1, h_), (p_, v_ - 1, h_ + 1), (p_ - 1, v_, h_)):
-            if pp >= 0 and vv >= 0 and 0 <= hh < cols and idx[s_, pp, vv, hh] >= 0:
-                cands.append(idx[s_, pp, vv, hh])
-        if not cands:
-            break
-        j = max(cands, key=lambda k: done[k])
-        if done[j] < claim[i] - 50:  # claimed well after this dep finished: the chain goes through the claim
-            break
-        i = j
-    chain = chain[::-1]
-    ch = np.array(chain)
-    st0 = np.maximum(claim[ch], np.r_[claim[ch[0]], done[ch[:-1]]])
-    work = done[ch] - st0
-    cw = np.maximum(0, claim[ch] - np.r_[claim[ch[0]], done[ch[:-1]]])
-    print("critical chain: %d blocks, first claim %.1f us, end %.1f us; work %.1f us (mean %.2f/block), claim waits %.1f us"
-          % (len(ch), claim[ch[0]], done[ch[-1]], work.sum(), work.mean(), cw[1:].sum()))
-    print("  chain ready->done mean %.2f us, detect (ready - dep done) mean %.2f us" % ((done[ch] - ready[ch]).mean(), (ready[ch][1:] - done[ch[:-1]]).mean()))
-    # DAG depth of the traced list (levels)
-    lev = np.zeros(len(done), np.int64)
-    order = np.argsort(step, kind="stable")
-    for k in order:
-        m = 0
-        s_, p_, v_, h_ = seq[k], p[k], v[k], h[k]
-        for (pp, vv, hh) in ((p_, v_, h_ - 1), (p_, v_ - 1, h_), (p_, v_ - 1, h_ + 1), (p_ - 1, v_, h_)):
-            if pp >= 0 and vv >= 0 and 0 <= hh < cols:
-                j = idx[s_, pp, vv, hh]
-                if j >= 0:
-                    m = max(m, lev[j])
-        lev[k] = m + 1
-    print("DAG depth %d (list steps %d); span / depth = %.2f us per level" % (lev.max(), step.max() + 1, done.max() / lev.max()))
+idx = np.full((nseq, pairs, rows, cols), -1, np.int64)
+idx[seq, p, v, h] = np.arange(len(done))
+i = int(np.argmax(done))
+chain = []
+while True:
+    chain.append(i)
+    cands = []
+    s_, p_, v_, h_ = seq[i], p[i], v[i], h[i]
+    for (pp, vv, hh) in ((p_, v_, h_ - 1), (p_, v_ - 1, h_), (p_, v_ - 1, h_ + 1), (p_ - 1, v_, h_)):
+        if pp >= 0 and vv >= 0 and 0 <= hh < cols and idx[s_, pp, vv, hh] >= 0:
+            cands.append(idx[s_, pp, vv, hh])
+    if not cands:
+        break
+    j = max(cands, key=lambda k: done[k])
+    if done[j] < claim[i] - 50:  # claimed well after this dep finished: the chain goes through the claim
+        break
+    i = j
+chain = chain[::-1]
+ch = np.array(chain)
+st0 = np.maximum(claim[ch], np.r_[claim[ch[0]], done[ch[:-1]]])
+work = done[ch] - st0
+cw = np.maximum(0, claim[ch] - np.r_[claim[ch[0]], done[ch[:-1]]])
+print("critical chain: %d blocks, first claim %.1f us, end %.1f us; work %.1f us (mean %.2f/block), claim waits %.1f us"
+      % (len(ch), claim[ch[0]], done[ch[-1]], work.sum(), work.mean(), cw[1:].sum()))
+print("  chain ready->done mean %.2f us, detect (ready - dep done) mean %.2f us" % ((done[ch] - ready[ch]).mean(), (ready[ch][1:] - done[ch[:-1]]).mean()))
+# DAG depth of the traced list (levels)
+lev = np.zeros(len(done), np.int64)
+order = np.argsort(step, kind="stable")
+for k in order:
+    m = 0
+    s_, p_, v_, h_ = seq[k], p[k], v[k], h[k]
+    for (pp, vv, hh) in ((p_, v_, h_ - 1), (p_, v_ - 1, h_), (p_, v_ - 1, h_ + 1), (p_ - 1, v_, h_)):
+        if pp >= 0 and vv >= 0 and 0 <= hh < cols:
+            j = idx[s_, pp, vv, hh]
+            if j >= 0:
+                m = max(m, lev[j])
+    lev[k] = m + 1
+print("DAG depth %d (list steps %d); span / depth = %.2f us per level" % (lev.max(), step.max() + 1, done.max() / lev.max()))
