@@ -649,7 +649,11 @@ def bench_critical_path(args, local, dev):
     return {"model": "search time = wavefront steps x per-step latency (pa_fast_kernel, one CTA per SM; CUDA events, L2 flushed)", **out}
 
 
-def bench_es_cfg5(args, world, rank, local, dev):
+def bench_units(args, world, rank, local, dev, wl="cfg5-es"):
+    """A baseline search (ES / TSS / FSS / DS) on one sequence, sharded by
+    (pair, block-row band) units balanced by estimated-block count (SURVEY
+    8e; config 5's ES is the default line's es_cfg5 leg, any baseline workload
+    at N > 1 is strong-scaled this way)."""
     import torch
     import torch.distributed as dist
 
@@ -660,10 +664,10 @@ def bench_es_cfg5(args, world, rank, local, dev):
     from paper_1002_1168_b200 import synth
     import ctypes as C
 
-    cfg_id, algo, bs, S = 5, "ES", 16, 64
-    F = args.es_frames or 30
+    cfg_id, algo, bs, S, _ = WORKLOADS[wl]
+    F = args.es_frames or {1: 10, 2: 30, 3: 60, 5: 30}[cfg_id]
     pairs, d = F - 2, 2
-    luma, alpha = synth.config4_batch_dev(1, BASE_SEED, F, config_id=5, device=local)
+    luma, alpha = synth.config4_batch_dev(1, BASE_SEED, F, config_id=cfg_id, device=local)
     torch.cuda.synchronize(dev)
     _, _, H, W = luma.shape
     rows, cols = H // bs, W // bs
@@ -756,12 +760,19 @@ def bench_es_cfg5(args, world, rank, local, dev):
         cmp_total = int(st[:, 0].sum())
     ops = cmp_total * bs * bs
     units_mb = pairs * (W // 16) * (H // 16)
-    # sampled parity: estimated blocks spread over the pairs vs the reference's full_search
+    # parity: ES at 4K — sampled estimated blocks spread over the pairs vs the
+    # reference's full_search (the whole sequence takes minutes on the host);
+    # the other searches — the whole sequence's MV fields + stats vs the reference
     import oracle as O
 
     lh, ah = luma[0].cpu().numpy(), alpha[0].cpu().numpy()
     parity = None
-    if not args.no_parity:
+    if not args.no_parity and not (algo == "ES" and cfg_id == 5):
+        rr = np.zeros((1, pairs, rows, cols), _lib.rec_dtype())
+        rr["dx"], rr["dy"] = dx, dy  # (half-pel, as the records)
+        sn = np.ascontiguousarray(st.astype(np.int64)).view(_lib.stats_dtype()).reshape(1, pairs)
+        parity, _ = digest_parity(rr, sn, lh[None], ah[None], cfg_id, algo, bs, S, os.cpu_count() or 1)
+    elif not args.no_parity:
         orc = O.Oracle("reference" if O.available("reference") else "port")
         rng = np.random.default_rng(5)
         bad, n_chk = 0, 0
@@ -775,15 +786,14 @@ def bench_es_cfg5(args, world, rank, local, dev):
                 bad += (int(dx[p, v, h]), int(dy[p, v, h])) != (rdx, rdy)
         parity = {"blocks_checked": n_chk, "mismatches": bad, "how": f"ES MVs of randomly sampled estimated blocks vs the reference's full_search ({orc.kind})"}
     threads = os.cpu_count() or 1
-    wl = "cfg5-es"
     v_cpu, sample, dt, kind = cpu_sample(wl, lh[None], ah[None], threads)
     peak = ipk.value / 1e12
     ach = ops / (search_ms / 1e3) / 1e12
     return {
-        "workload": f"cfg5-es: BASELINE config 5 (3840x2160 x {F}f, {pairs} pairs), ES S=64 bs=16" + (f", (pair, row-band) units over {world} GPUs" if world > 1 else ""),
+        "workload": f"{wl}: BASELINE config {cfg_id} ({GEOMETRY[cfg_id]} x {F}f, {pairs} pairs), {algo} S={S} bs={bs}" + (f", (pair, row-band) units over {world} GPUs" if world > 1 else ""),
         "metric": "macroblocks/sec", "value": units_mb / (ms / 1e3), "unit": "MB/s", "ms_per_step": ms, "steps": args.es_steps,
         "sad_byte_ops_per_step": ops, "search_ms": search_ms,
-        "roofline": {"bound": "int", "kernel": "es_kernel (search stage)", "achieved": ach, "peak": peak, "unit": "T byte-ops/s", "frac": ach / peak,
+        "roofline": {"bound": "int", "kernel": f"{'es_kernel' if algo == 'ES' else 'ring_kernel'} (search stage)", "achieved": ach, "peak": peak, "unit": "T byte-ops/s", "frac": ach / peak,
                      "peak_source": "VABSDIFF4.U8.ACC microbenchmark measured in this run on this GPU (me_b200_probe_int_peak)",
                      "note": "achieved = oracle-exact comparisons x 256 byte-ops / search-stage time (CUDA events)"},
         "clocks": clk, "parity": parity,
@@ -838,12 +848,14 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
-    line = bench_pa_batch(args, wl, world, rank, local, dev) if wl != "cfg5-es" else None
+    # baseline searches (ES / TSS / FSS / DS) on several GPUs: (pair, row-band) units, strong-scaled
+    units_line = wl == "cfg5-es" or (WORKLOADS[wl][1] != "PA" and world > 1)
+    line = bench_pa_batch(args, wl, world, rank, local, dev) if not units_line else None
     es = None
-    if wl == "cfg5-es" or (wl == "cfg4-pa" and not args.no_es):
-        es = bench_es_cfg5(args, world, rank, local, dev)
+    if units_line or (wl == "cfg4-pa" and not args.no_es):
+        es = bench_units(args, world, rank, local, dev, wl if units_line else "cfg5-es")
     if rank == 0:
-        if line is None:  # --workload cfg5-es: the ES leg is the line
+        if line is None:  # the units leg is the line
             line = {"metric": "macroblocks/sec", "value": es["value"], "unit": "MB/s", "n_gpus": world, "steps": es["steps"], "warmup": max(args.warmup, 3),
                     "ms_per_step": es["ms_per_step"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
                     "data": "synthetic (seeded integer config generator, SURVEY §8d)", "config": {"workload": es["workload"]}, "roofline": es["roofline"],
