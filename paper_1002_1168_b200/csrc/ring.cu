@@ -34,6 +34,7 @@ struct RingCtx {
     uint32_t* bitmap;            // per-warp
     uint32_t* stage;             // per-warp kStageWords, 16-byte aligned
     uint32_t count;
+    int scx, scy;                // centre (pel offsets) of the staged region; scx > 2^20: nothing staged
 };
 
 // BS bytes at an arbitrary address as BS/4 words, from aligned loads (two
@@ -64,14 +65,17 @@ __device__ __forceinline__ void ld_row_aligned(const uint8_t* p, uint32_t (&r)[B
     }
 }
 
-// Small rings (radius <= kStageR: TSS's last steps, every FSS / DS ring) are
-// served from a per-warp shared-memory copy of the region the ring covers:
-// (BS + 2 radius) rows of 16-byte chunks from the aligned address at or left of
-// the region, fetched by the whole warp (each load instruction covers a few
-// rows instead of 32), then every position's rows are read from shared memory.
-constexpr int kStageR = 4;
-constexpr int kStageRowWords = 12;                                     // 48 bytes: 3 chunks
-constexpr int kStageWords = (16 + 2 * kStageR) * kStageRowWords;       // 288 words per warp
+// Small rings (extent <= kStageR: TSS's last steps, every FSS / DS ring) are
+// served from a per-warp shared-memory copy of the region within kStageR pels
+// of a centre: (BS + 2 kStageR) rows of 16-byte chunks from the aligned
+// address at or left of the region, fetched by the whole warp (each load
+// instruction covers a few rows instead of 32).  The copy stays valid while
+// the later rings fit in it (FSS's rounds, DS's steps and TSS's last three
+// rings mostly restage never or once), then every position's rows are read
+// from shared memory.
+constexpr int kStageR = 8;
+constexpr int kStageRowWords = 12;                                     // 48 bytes: 3 chunks (BS + 2 kStageR <= 33)
+constexpr int kStageWords = (16 + 2 * kStageR) * kStageRowWords;       // 384 words per warp
 
 // Scores the n (<= 8) positions (cx, cy) + offs[k] * radius (pel); lanes
 // 4k..4k+3 own position k and return its SAD; bit 4k of adm_mask is set for
@@ -87,28 +91,34 @@ __device__ __forceinline__ uint32_t ring_eval(RingCtx& c, const uint32_t (&cw)[B
     const bool adm = k < n && dx >= c.lo_x && dx <= c.hi_x && dy >= c.lo_y && dy <= c.hi_y;
     uint32_t s = 0;
     if (e >= 1 && e <= kStageR) {  // warp-uniform
-        constexpr int NCH = BS == 16 ? 3 : 2;
-        const int R = BS + 2 * e, rx = c.x0 + cx - e, ry = c.y0 + cy - e;
+        constexpr int E = kStageR, NCH = (BS + 2 * E + 15 + 15) / 16;
         const uintptr_t base = reinterpret_cast<uintptr_t>(c.ref);
-        for (int it = lane; it < R * NCH; it += 32) {
-            const int row = it / NCH, ch = it - NCH * row;
-            const int y = ry + row;
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (y >= 0 && y < c.H) {
-                const uintptr_t rowa = base + size_t(y) * c.W;
-                const uintptr_t cb = ((rowa + uintptr_t(intptr_t(rx))) & ~uintptr_t(15)) + 16u * ch;
-                // only chunks holding a byte of this row (never outside the plane)
-                if (cb + 16 > rowa && cb < rowa + c.W) v = __ldg(reinterpret_cast<const uint4*>(cb));
+        if (abs(cx - c.scx) + e > E || abs(cy - c.scy) + e > E) {  // the ring leaves the staged region: restage
+            c.scx = cx;
+            c.scy = cy;
+            const int R = BS + 2 * E, rx = c.x0 + cx - E, ry = c.y0 + cy - E;
+            __syncwarp();  // every lane is done reading the previous copy
+            for (int it = lane; it < R * NCH; it += 32) {
+                const int row = it / NCH, ch = it - NCH * row;
+                const int y = ry + row;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (y >= 0 && y < c.H) {
+                    const uintptr_t rowa = base + size_t(y) * c.W;
+                    const uintptr_t cb = ((rowa + uintptr_t(intptr_t(rx))) & ~uintptr_t(15)) + 16u * ch;
+                    // only chunks holding a byte of this row (never outside the plane)
+                    if (cb + 16 > rowa && cb < rowa + c.W) v = __ldg(reinterpret_cast<const uint4*>(cb));
+                }
+                *reinterpret_cast<uint4*>(c.stage + row * kStageRowWords + 4 * ch) = v;
             }
-            *reinterpret_cast<uint4*>(c.stage + row * kStageRowWords + 4 * ch) = v;
+            __syncwarp();
         }
-        __syncwarp();
+        const int rx = c.x0 + c.scx - E, ry = c.y0 + c.scy - E;
         if (adm) {
 #pragma unroll
             for (int j = 0; j < BS / 4; ++j) {
-                const int row = dy - cy + e + (lane & 3) + 4 * j;
+                const int row = dy - c.scy + E + (lane & 3) + 4 * j;
                 const uint32_t o = uint32_t((base + size_t(ry + row) * c.W + uintptr_t(intptr_t(rx))) & 15u) +
-                                   uint32_t(dx - cx + e);
+                                   uint32_t(dx - c.scx + E);
                 const uint32_t* w = c.stage + row * kStageRowWords + (o >> 2);
                 const uint32_t sh = (o & 3u) * 8u;
                 uint32_t u[BS / 4 + 1];
@@ -118,7 +128,6 @@ __device__ __forceinline__ uint32_t ring_eval(RingCtx& c, const uint32_t (&cw)[B
                 for (int i = 0; i < BS / 4; ++i) s = vad4(cw[j][i], __funnelshift_r(u[i], u[i + 1], sh), s);
             }
         }
-        __syncwarp();  // the next ring restages
     } else if (adm) {
         const uint8_t* rp = c.ref + size_t(c.y0 + dy + (lane & 3)) * c.W + (c.x0 + dx);
 #pragma unroll
@@ -151,17 +160,16 @@ __device__ __forceinline__ void probe_ring(RingCtx& c, const uint32_t (&cw)[BS /
                                            int& cy, uint32_t& best, int lane) {
     uint32_t adm;
     const uint32_t s = ring_eval<BS>(c, cw, offs, n, radius, reach, cx, cy, lane, adm);
-    int bx = cx, by = cy;
-    for (int i = 0; i < n; ++i) {
-        const uint32_t v = __shfl_sync(0xFFFFFFFFu, s, 4 * i);
-        if (((adm >> (4 * i)) & 1u) && v < best) {
-            best = v;
-            bx = cx + offs[i][0] * radius;
-            by = cy + offs[i][1] * radius;
-        }
+    // sequential strict improvement in listed order = the first admissible
+    // position holding the ring's minimum, taken if below the centre's cost:
+    // one warp reduction of (SAD << 3 | k) (SAD < 2^17)
+    const int k = lane >> 2;
+    const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, ((adm >> (4 * k)) & 1u) ? (s << 3) | uint32_t(k) : ~0u);
+    if (m != ~0u && (m >> 3) < best) {
+        best = m >> 3;
+        cx += offs[m & 7][0] * radius;
+        cy += offs[m & 7][1] * radius;
     }
-    cx = bx;
-    cy = by;
 }
 
 template <int BS>
@@ -182,6 +190,7 @@ __device__ void ring_block(int algo, const uint8_t* cur, const uint8_t* ref, int
     c.bitmap = bitmap;
     c.stage = bitmap + ((((c.hi_x - c.lo_x + 1) * (c.hi_y - c.lo_y + 1) + 31) >> 5) + 3 & ~3);
     c.count = 0;
+    c.scx = c.scy = 1 << 21;  // nothing staged yet
     // the lane's current-block rows (lane & 3) + 4 j, once per block
     uint32_t cw[BS / 4][BS / 4];
 #pragma unroll
