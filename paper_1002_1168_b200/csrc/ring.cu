@@ -114,11 +114,13 @@ __device__ __forceinline__ uint32_t ring_eval(RingCtx& c, const uint32_t (&cw)[B
         }
         const int rx = c.x0 + c.scx - E, ry = c.y0 + c.scy - E;
         if (adm) {
+            // byte offset of staged row `row`'s first chunk: the region's start
+            // misalignment, advancing by W mod 16 per row (32-bit math per row)
+            const uint32_t a0 = uint32_t((base + size_t(ry) * c.W + uintptr_t(intptr_t(rx))) & 15u), wm = uint32_t(c.W) & 15u;
 #pragma unroll
             for (int j = 0; j < BS / 4; ++j) {
                 const int row = dy - c.scy + E + (lane & 3) + 4 * j;
-                const uint32_t o = uint32_t((base + size_t(ry + row) * c.W + uintptr_t(intptr_t(rx))) & 15u) +
-                                   uint32_t(dx - c.scx + E);
+                const uint32_t o = ((a0 + uint32_t(row) * wm) & 15u) + uint32_t(dx - c.scx + E);
                 const uint32_t* w = c.stage + row * kStageRowWords + (o >> 2);
                 const uint32_t sh = (o & 3u) * 8u;
                 uint32_t u[BS / 4 + 1];
