@@ -386,6 +386,19 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
     ms_per_step = ms / args.steps
     total_units = n_total * pairs * (W // 16) * (H // 16)
     value = total_units / (ms_per_step / 1e3)
+    compute_only = None
+    if gatherer is not None:  # compute-only beside compute + gather (the line's value)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            B.run_sequences_dev(cfg, luma, alpha, recs, stats, device=local, stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        c_ms = mdist.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
+        compute_only = {"ms_per_step": c_ms, "value": total_units / (c_ms / 1e3), "unit": "MB/s",
+                        "note": "the same steps without the per-step gather to rank 0 (max over ranks)"}
     # per-stage breakdown (CUDA events on the launching stream), untimed
     n_stage = min(args.steps, 20)
     _lib.check(lib.me_b200_ctx_set_profiling(ctxh, 1))
@@ -588,6 +601,8 @@ def bench_pa_batch(args, wl, world, rank, local, dev):
             "parity": parity,
             "bits_layout": bits_layout,
             "estimated_blocks": est,
+            "estimated_blocks_per_s": est / (ms_per_step / 1e3),
+            "compute_only": compute_only,
             "macroblocks_per_step": int(total_units),
         }
         if parity is not None and parity["mismatches"]:
