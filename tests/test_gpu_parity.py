@@ -427,6 +427,26 @@ def test_ring_searches_batched(me_gpu, port, algo, bs, shape):
 
 @pytest.mark.parametrize("algo", [1, 2, 3])
 @pytest.mark.parametrize("bs", [8, 16])
+@pytest.mark.parametrize("rng_s", [1, 2, 5, 9, 33])
+def test_ring_staged_region_ranges(me_gpu, port, algo, bs, rng_s):
+    """The ring kernel's persistent staged region (8 pels around a centre,
+    restaged when a ring leaves it) against windows smaller and larger than
+    it, clipped at every frame edge (QCIF-sized frame, every block estimated),
+    with fast motion so DS walks far and TSS's big rings leave the region."""
+    rng = np.random.default_rng(7 * algo + bs + 100 * rng_s)
+    h, w = 80, 112
+    base = noise(rng, h + 80, w + 80)
+    base = np.convolve(base.ravel(), np.ones(3) / 3, "same").reshape(base.shape).astype(np.uint8)
+    frames = np.stack([shift_clamped(base, 7 * t, -5 * t)[40:40 + h, 40:40 + w] for t in range(4)])
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo(algo), search=me_gpu.SearchConfig(search_range=rng_s, block_size=bs, ref_distance=1))
+    recs, stats = me_gpu.run_sequences(cfg, frames[None], None)
+    want_r, want_s = port.run_sequence(oracle.make_cfg(algo=algo, search_range=rng_s, block_size=bs, ref_distance=1), frames, None)
+    assert_recs(recs[0], want_r, f"algo{algo} bs{bs} S{rng_s}")
+    assert np.array_equal(stats[0], want_s)
+
+
+@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("bs", [8, 16])
 def test_ring_single_block_odd_width(me_gpu, port, algo, bs):
     """The per-block entry points on a frame whose width is not a multiple of
     4 (no row of either plane is word-aligned)."""
