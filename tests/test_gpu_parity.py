@@ -501,6 +501,31 @@ def test_pa_config_variants(me_gpu, port, bs, hp, bt, it, step, eps, theta):
         assert np.array_equal(stats[0], want_s)
 
 
+@pytest.mark.parametrize("key", [1, -1])
+@pytest.mark.parametrize("bs,hp,bt,it,step,eps,theta", PA_VARIANTS[:4])
+def test_pa_config_variants_batched(me_gpu, port, bs, hp, bt, it, step, eps, theta, key, tuning):
+    """The same variants on a batch of config-4 sequences (the generic and
+    fast kernels over a multi-sequence list, with the plain and the aligned
+    list keys)."""
+    from paper_1002_1168_b200 import synth
+
+    tuning(pa_key_plain=key)
+    luma, alpha = synth.config4_batch(4, 4300 + bs + hp, frames=5)
+    cfg = me_gpu.BatchConfig(
+        algo=me_gpu.Algo.PA,
+        search=me_gpu.SearchConfig(search_range=16, block_size=bs, halfpel=bool(hp)),
+        prs=me_gpu.PrsConfig(epsilon=eps, theta=theta, max_iterations=it, step=step),
+        boundary_temporal=me_gpu.BoundaryTemporal(bt),
+    )
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in range(4):
+        want_r, want_s = port.run_sequence(
+            oracle.make_cfg(algo=4, search_range=16, block_size=bs, halfpel=hp, boundary_temporal=bt,
+                            max_iterations=it, step=step, epsilon=eps, theta=theta), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"seq {i} bs{bs} hp{hp} bt{bt} it{it} key{key}")
+        assert np.array_equal(stats[i], want_s)
+
+
 # ---------------------------------------------------------------------------
 # Sharding entry points (SURVEY 8e) and concurrency
 
