@@ -26,5 +26,5 @@ B.run_sequences_dev(cfg, luma, alpha)
 torch.cuda.synchronize()
 _lib.set_tuning(0)
 print(n, "sequences,", sched, "schedule,", extra, ":", os.path.getsize(path) if os.path.exists(path) else "no trace file", "bytes")
-r = subprocess.run([sys.executable, "tools/trace_report.py", path, "44", "36", "28"], capture_output=True, text=True)
+r = subprocess.run([sys.executable, "tools/trace_report.py", path, "44", "36", "28", "steps"], capture_output=True, text=True)
 print(r.stdout, r.stderr)

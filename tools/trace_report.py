@@ -98,3 +98,12 @@ for k in order:
                 m = max(m, lev[j])
     lev[k] = m + 1
 print("DAG depth %d (list steps %d); span / depth = %.2f us per level" % (lev.max(), step.max() + 1, done.max() / lev.max()))
+# Per-step profile (every 4th step): items, window of claims, last done, the
+# mean claim->ready and ready->done and the mean patch-staging cycles.
+if len(sys.argv) > 5 and sys.argv[5] == "steps":
+    print("step items claim0 claim1 done1 | claim->ready ready->done staged_cyc brs_cyc walk_cyc")
+    for s in st[::2]:
+        m = step == s
+        print("%4d %6d %7.1f %7.1f %7.1f | %5.2f %5.2f %6.0f %6.0f %6.0f" % (
+            s, m.sum(), claim[m].min(), claim[m].max(), done[m].max(), (ready[m] - claim[m]).mean(),
+            (done[m] - ready[m]).mean(), cyc[m, 0].mean(), cyc[m, 1].mean(), cyc[m, 2].mean()))
