@@ -2131,14 +2131,17 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         // a single sequence is latency-bound: one CTA per SM with 128
         // registers per thread runs each block sooner (measured 3-6 % on
         // configs 2, 3, 5); small batches (< 80 blocks per step per SM, up to
-        // ~36 CIF sequences) need more blocks in flight: 2 CTAs (measured
-        // 4-25 % better than 1 or 4 at 8-32 sequences); wider ones 4 (the
-        // hybrid's head and tail)
+        // ~36 CIF sequences) need more blocks in flight: 2 CTAs below 60
+        // blocks per step per SM (measured 4-25 % better than 1 or 4 at 8-16
+        // CIF sequences, 5-7 % better than 3 at 16-24), 3 from 60 to 160
+        // (1-1.5 % better than 2 or 4 at 32-64); wider ones 4 (the hybrid's
+        // head and tail)
         const int64_t per_step = b.nblocks() / std::max(1, b.steps());
         const int mb = t.pa_fast_ctas > 0 ? t.pa_fast_ctas
                        : pa_mode != 1      ? 4
                        : b.n_seq == 1      ? 1
-                       : per_step < int64_t(num_sms) * 80 ? 2 : 4;
+                       : per_step < int64_t(num_sms) * 60 ? 2
+                       : per_step < int64_t(num_sms) * 160 ? 3 : 4;
         fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
         set_window(mb);
         if (trace_path) fast = mb == 1 ? pa_fast_kernel<1, true> : mb == 2 ? pa_fast_kernel<2, true> : pa_fast_kernel<4, true>;
