@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/sched
-timeout 900 python tools/key_probe.py 128,96,64,48,32,24,16,8 default f2:pa_fast_ctas=2 f3:pa_fast_ctas=3 f4:pa_fast_ctas=4 > gpurun_out/sched/fdef.txt 2>&1; echo rc=$?
-cat gpurun_out/sched/fdef.txt
+timeout 300 python tools/key_probe.py 8 default df:pa_dataflow=1 > gpurun_out/sched/df.txt 2>&1; echo rc=$?
+timeout 600 python tools/key_probe.py 32,64,256 default df:pa_dataflow=1 df3:pa_dataflow=1,pa_fast_ctas=3 df2:pa_dataflow=1,pa_fast_ctas=2 >> gpurun_out/sched/df.txt 2>&1; echo rc=$?
+cat gpurun_out/sched/df.txt
