@@ -42,3 +42,24 @@ for name, kw in variants:
     ref = ref or out
     print(f"cfg{cid} PA bs8 {name}: {us:.1f} us per pair{'' if same else ' DIFFERENT'}", flush=True)
 _lib.set_tuning(0)
+
+# the per-pair pipeline's stage times (context events): the search stage of
+# a PA pair is the one-CTA shared-memory kernel
+import ctypes as C  # noqa: E402
+
+lib, h = _lib.lib(), _lib.ctx(0)
+_lib.check(lib.me_b200_ctx_set_profiling(h, 1))
+for algo, bs in ((api.Algo.ES, 16), (api.Algo.PA, 8)):
+    cfg = api.SearchConfig(search_range=16, block_size=bs)
+    acc, n = [0.0] * 4, 0
+    prev = None
+    for f in range(2, frames):
+        field, st = api.estimate_field(algo, luma[f], luma[f - 2], None, None, prev if algo == api.Algo.PA else None, cfg, api.PrsConfig())
+        prev = field
+        out = (C.c_float * 4)()
+        _lib.check(lib.me_b200_ctx_stage_ms(h, out, 4))
+        if f > 3:
+            acc = [a + x for a, x in zip(acc, out)]
+            n += 1
+    print(f"cfg{cid} {api.to_string(algo)} stages (classify, sort, search, mc) us:", [round(1000 * a / n, 1) for a in acc], flush=True)
+_lib.check(lib.me_b200_ctx_set_profiling(h, 0))
