@@ -1706,6 +1706,7 @@ struct PaSmemArgs {
     me_block_rec* recs;
     me_pair_stats* stats;
     int plane_pad;  // bytes per staged plane (plane + 16)
+    long long* trace;  // debug (tuning pa_trace_path): per block {wait start, ready, BRS done, walk done, published} SM clocks
 };
 
 __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
@@ -1724,7 +1725,8 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
     uint32_t* s_mv = reinterpret_cast<uint32_t*>(s_frames + (has_alpha ? 4 : 2) * size_t(pp));
     uint32_t* s_cost = s_mv + cols * rows;  // final cost_q4 of estimated blocks
     uint32_t* s_meta = s_cost + cols * rows;  // dpd << 8 | iterations
-    uint8_t* s_type = reinterpret_cast<uint8_t*>(s_meta + cols * rows);
+    uint32_t* s_prev = s_meta + cols * rows;  // pair 0's temporal candidates, packed (when given)
+    uint8_t* s_type = reinterpret_cast<uint8_t*>(s_prev + (a.prev0 ? cols * rows : 0));
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     // stage the planes (16-byte copies) and clear the MV words: the pair's ref
     // is frame 0 and its cur frame d (ref_distance), which need not be adjacent
@@ -1742,7 +1744,10 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
                 reinterpret_cast<uint4*>(s_ra + f * size_t(pp))[o] = __ldg(ga + o);
             }
         }
-        for (int i = tid; i < cols * rows; i += blockDim.x) s_mv[i] = 0u;
+        for (int i = tid; i < cols * rows; i += blockDim.x) {
+            s_mv[i] = 0u;
+            if (a.prev0) s_prev[i] = pack_mv(a.prev0[2 * i], a.prev0[2 * i + 1]);
+        }
         if (tid == 0) {
             s_sse = s_dpd = 0ull;
             s_cnt[0] = s_cnt[1] = s_cnt[2] = 0u;
@@ -1814,13 +1819,22 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
             const int lo_x = max(-2 * S, -2 * x0), hi_x = min(2 * S, 2 * (W - x0 - 8));
             const int lo_y = max(-2 * S, -2 * y0), hi_y = min(2 * S, 2 * (H - y0 - 8));
             // gather_candidates (estimators.cpp:238-255): A, B, C, T
+            long long tr0 = 0;
+            if (a.trace) tr0 = clock64();
             int dep = -1;
             if (c == 0 && h > 0) dep = g - 1;
             if (c == 1 && v > 0) dep = g - cols;
             if (c == 2 && v > 0 && h + 1 < cols) dep = g - cols + 1;
+            // (the T candidate and this block's current rows do not depend on the wait)
+            const uint32_t tw = c == 3 && a.prev0 ? s_prev[g] : 0u;
+            const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + sub) * W + x0);
+            const uint2 ca_ = *reinterpret_cast<const uint2*>(s_cur + (y0 + q) * W + x0);
+            const uint2 cb_ = *reinterpret_cast<const uint2*>(s_cur + (y0 + q + 4) * W + x0);
             uint32_t mw = dep >= 0 ? vmv[dep] : 0u;
             while (__any_sync(FULL, mw == kSentinel)) mw = dep >= 0 ? vmv[dep] : 0u;
-            if (c == 3 && a.prev0) mw = pack_mv(a.prev0[2 * g], a.prev0[2 * g + 1]);
+            if (c == 3) mw = tw;
+            long long tr1 = 0, tr2 = 0, tr3 = 0;
+            if (a.trace) tr1 = clock64();
             const int myx = clip_comp(mv_dx(mw), lo_x, hi_x), myy = clip_comp(mv_dy(mw), lo_y, hi_y);
             // brs_select (estimators.cpp:257-301): row `sub` of candidate c
             uint32_t s;
@@ -1831,7 +1845,6 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
                 srow8(s_ra + ry * W, rx, r0, r1);
                 s = ((__popc(__vcmpne4(ca.x, r0)) + __popc(__vcmpne4(ca.y, r1))) >> 3) * (255u * 4u);
             } else {
-                const uint2 cr = *reinterpret_cast<const uint2*>(s_cur + (y0 + sub) * W + x0);
                 uint32_t r0, r1;
                 srow8(s_ref + ry * W, rx, r0, r1);
                 s = vad4(cr.y, r1, vad4(cr.x, r0, 0u)) * 4u;
@@ -1839,20 +1852,13 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
             s += __shfl_xor_sync(FULL, s, 1);
             s += __shfl_xor_sync(FULL, s, 2);
             s += __shfl_xor_sync(FULL, s, 4);
-            uint32_t best = __shfl_sync(FULL, s, 0);
-            int win = 0;
-#pragma unroll
-            for (int j = 1; j < 4; ++j) {
-                const uint32_t sj = __shfl_sync(FULL, s, 8 * j);
-                if (sj < best) {  // strict <: A, B, C, T tie order (:295)
-                    best = sj;
-                    win = j;
-                }
-            }
-            const int wx = __shfl_sync(FULL, myx, 8 * win), wy = __shfl_sync(FULL, myy, 8 * win);
-            // my two PRS rows of the block
-            const uint2 ca_ = *reinterpret_cast<const uint2*>(s_cur + (y0 + q) * W + x0);
-            const uint2 cb_ = *reinterpret_cast<const uint2*>(s_cur + (y0 + q + 4) * W + x0);
+            // strict <: A, B, C, T tie order (:295) = the minimum of (score, candidate)
+            // (scores < 2^17), one warp reduction
+            const uint32_t bk = __reduce_min_sync(FULL, (s << 2) | uint32_t(c));
+            const uint32_t best = bk >> 2;
+            const int win = int(bk & 3u);
+            const uint32_t wxy = __shfl_sync(FULL, pack_mv(myx, myy), 8 * win);
+            const int wx = mv_dx(wxy), wy = mv_dy(wxy);
             uint32_t ccost = best;
             if (boundary && (win < 3 || a.P.bt_shape)) {  // the centre's texture cost
                 uint32_t tsum = 0;
@@ -1864,6 +1870,7 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
                 }
                 ccost = 4u * __reduce_add_sync(FULL, tsum);
             }
+            if (a.trace) tr2 = clock64();
             // prs_refine (estimators.cpp:311-382); unique evaluations: a neighbour
             // is new iff it is at Chebyshev distance >= 2 from every earlier centre
             int ci = 0, cj = 0, pc0 = 0, pc1 = 0, pc2 = 0;
@@ -1928,11 +1935,21 @@ __global__ void __launch_bounds__(1024, 1) pa_smem_kernel(const PaSmemArgs a) {
             }
             // only the vector is on the wavefront's critical path: the SSE and
             // the record are produced after the last step (phase 3)
+            if (a.trace) tr3 = clock64();
             if (lane == 0) {
+                // publish first: the dependents read only the MV word (cost and
+                // counters are read by phase 3, after the barrier)
+                vmv[g] = pack_mv(wx + 2 * ci, wy + 2 * cj);
                 s_cost[g] = ccost;
                 s_meta[g] = (dpd << 8) | iters;
-                __threadfence_block();
-                vmv[g] = pack_mv(wx + 2 * ci, wy + 2 * cj);
+                if (a.trace) {
+                    long long* tr = a.trace + size_t(g) * 5;
+                    tr[0] = tr0;
+                    tr[1] = tr1;
+                    tr[2] = tr2;
+                    tr[3] = tr3;
+                    tr[4] = clock64();
+                }
             }
         }
     }
@@ -2027,7 +2044,9 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
         !t.pa_smem_pair || b.alpha_bits)
         return cudaErrorNotSupported;
     const int plane_pad = b.W * b.H + 16;
-    const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * 13 + 16;
+    const size_t smem = size_t(b.alpha ? 4 : 2) * plane_pad + size_t(b.cols) * b.rows * (prev0 ? 17 : 13) + 16;
+    // (a CIF pair would fit in 227 KB, but one CTA's 32 warps hold only ~1.5 of
+    // its ~22-block wavefront steps: 174 us vs 158 through the batched pipeline)
     if (smem > 200 * 1024) return cudaErrorNotSupported;
     PaSmemArgs a;
     a.b = b;
@@ -2036,6 +2055,11 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
     a.recs = recs;
     a.stats = stats;
     a.plane_pad = plane_pad;
+    a.trace = nullptr;
+    if (t.pa_trace) {
+        cudaMalloc(&a.trace, size_t(b.cols) * b.rows * 5 * 8);
+        cudaMemsetAsync(a.trace, 0, size_t(b.cols) * b.rows * 5 * 8, st);
+    }
     static thread_local size_t attr_smem = 0;  // the attribute call costs microseconds: set once per size
     if (smem > attr_smem) {
         cudaError_t e = cudaFuncSetAttribute(pa_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -2043,6 +2067,16 @@ cudaError_t launch_pa_smem(const Batch& b, const me_config& cfg, const int32_t* 
         attr_smem = smem;
     }
     pa_smem_kernel<<<1, 1024, smem, st>>>(a);
+    if (a.trace) {
+        std::vector<long long> h(size_t(b.cols) * b.rows * 5);
+        cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (FILE* f = fopen(t.pa_trace, "wb")) {
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
+        cudaFree(a.trace);
+    }
     return cudaGetLastError();
 }
 
