@@ -34,6 +34,7 @@ struct EsArgs {
     me_block_rec* recs;
     int band_rows_max;  // staged rows per band (multiple of K, + BS - 1 added on top)
     me_pair_stats* stats;
+    int region_words;   // shared memory per block group (NB > 1)
 };
 
 constexpr int kEsThreads = 256;
@@ -76,11 +77,16 @@ __device__ __forceinline__ uint32_t es_task(const uint32_t (&c)[BS][BS / 4], con
 // PWC: the staged row stride in words when known at compile time (the
 // launcher instantiates the common search ranges; every row offset in the SAD
 // loop is then an immediate), 0 = computed from the clipped window.
+// The CTA's threads may form several groups, each searching its own block in
+// its own shared-memory region (small windows: NB blocks per CTA pass, see
+// es_kernel): tid / T = this thread's index / size within its group; every
+// group passes the same CTA barriers (one band per block when NB > 1).
 template <int BS, int K, int PWC = 0>
 __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
                          int S, int band_runs_max, uint32_t* sm, unsigned long long* s_best,
-                         int& out_dx, int& out_dy, uint32_t& out_sad, uint32_t& out_cmp) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+                         int& out_dx, int& out_dy, uint32_t& out_sad, uint32_t& out_cmp,
+                         int tid = threadIdx.x, int T = kEsThreads) {
+    const int lane = tid & 31, wid = tid >> 5;
     const int lo_x = max(-S, -x0), hi_x = min(S, W - x0 - BS);
     const int lo_y = max(-S, -y0), hi_y = min(S, H - y0 - BS);
     const int WX = hi_x - lo_x + 1, WY = hi_y - lo_y + 1;
@@ -136,11 +142,11 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
             // U words per thread per round, every load of the round issued
             // before any store (the staging is L2-latency-bound otherwise)
             constexpr int U = 4;
-            for (int i0 = tid; i0 < total; i0 += U * kEsThreads) {
+            for (int i0 = tid; i0 < total; i0 += U * T) {
                 uint32_t g[U][3], offs[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int i = min(i0 + u * kEsThreads, total - 1);
+                    const int i = min(i0 + u * T, total - 1);
                     const int row = __float2int_rz((float(i) + 0.5f) * inv_pw), q = i - row * PW;
                     const uint32_t b0 = seg0 + uint32_t(row) * uint32_t(W);
                     const uint32_t w0 = b0 >> 2, wl = (b0 + uint32_t(rowbytes) - 1) >> 2;
@@ -151,7 +157,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * kEsThreads;
+                    const int i = i0 + u * T;
                     if (i >= total) break;
                     const uint32_t off = offs[u], sh = off * 8, g0 = g[u][0], g1 = g[u][1], g2 = g[u][2];
                     // copies s = 0..3: byte offset off + s within (g0, g1, g2)
@@ -167,7 +173,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         // IMADs (FMA pipe) and the VIMNMX — the kernel is ALU-pipe-bound
         // (VABSDIFF4 issues at half rate there)
         uint32_t* const rkey = sm + 4 * CW;
-        for (int i = tid; i < bruns * K; i += kEsThreads) {
+        for (int i = tid; i < bruns * K; i += T) {
             const int wy = run0 * K + i;
             rkey[i] = wy < WY ? (uint32_t(abs(lo_y + wy)) << 3) | uint32_t(i % K) : kEsDead;
         }
@@ -179,7 +185,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         const float inv_wx = 1.0f / float(WX);
         const bool tail1 = run0 + bruns == nruns && WY - (nruns - 1) * K == 1;
         for (int ti = tid, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX; run < bruns;
-             ti += kEsThreads, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX) {
+             ti += T, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX) {
             const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
             const uint32_t adx8 = uint32_t(abs(lo_x + col)) << 3;
             const uint32_t* rk = rkey + run * K;
@@ -203,7 +209,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
     __syncthreads();
     if (tid == 0) {
         unsigned long long m = s_best[0];
-        for (int i = 1; i < int(blockDim.x >> 5); ++i) m = s_best[i] < m ? s_best[i] : m;
+        for (int i = 1; i < (T >> 5); ++i) m = s_best[i] < m ? s_best[i] : m;
         const int raster = int(m & 0xFFFFFF);
         out_dx = lo_x + raster % WX;
         out_dy = lo_y + raster / WX;
@@ -212,49 +218,58 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
     }
 }
 
-template <int BS, int K, int PWC>
+// NB > 1 (windows small enough that NB of them fit): the CTA claims NB list
+// entries per pass and splits into NB groups of kEsThreads / NB threads, one
+// block each, so one staging round trip, barrier and reduction serve NB blocks
+// (at S = 16 one block's 165 tasks left 91 of 256 threads idle and the
+// per-block staging and barriers dominated).
+template <int BS, int K, int PWC, int NB>
 __global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ unsigned long long s_best[kEsThreads / 32];
     __shared__ int s_item;
-    __shared__ int s_res[4];
+    __shared__ int s_res[NB][4];
+    constexpr int T = kEsThreads / NB;  // threads per group
     const Batch& b = a.b;
     const int n = *a.nlist;
     const size_t plane = size_t(b.W) * b.H;
     const int band_runs = a.band_rows_max / K;
+    const int grp = threadIdx.x / T, gtid = threadIdx.x - grp * T;
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+        if (threadIdx.x == 0) s_item = atomicAdd(a.counter, NB);
         __syncthreads();
-        const int item = s_item;
-        if (item >= n) return;
+        const int item0 = s_item;
+        if (item0 >= n) return;
+        const int item = item0 + grp;
+        const bool live = item < n;  // (an idle group still passes every barrier)
         int h, v, p, seq;
         bool boundary;
-        const uint32_t g = decode_entry(b, a.list[item], h, v, p, seq, boundary);
+        const uint32_t g = decode_entry(b, a.list[live ? item : item0], h, v, p, seq, boundary);
         const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
         const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
         int dx, dy;
         uint32_t sad, cmp;
-        es_block<BS, K, PWC>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, s_best, dx, dy,
-                        sad, cmp);
-        if (threadIdx.x == 0) {
-            s_res[0] = dx;
-            s_res[1] = dy;
-            s_res[2] = int(sad);
-            s_res[3] = int(cmp);
+        es_block<BS, K, PWC>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm + size_t(grp) * a.region_words,
+                             s_best + grp * (T / 32), dx, dy, sad, cmp, gtid, T);
+        if (gtid == 0) {
+            s_res[grp][0] = dx;
+            s_res[grp][1] = dy;
+            s_res[grp][2] = int(sad);
+            s_res[grp][3] = int(cmp);
         }
         __syncthreads();
-        if (threadIdx.x < 32) {
-            // fused predict_frame + psnr SSE of this block at its vector
-            const int lane = threadIdx.x;
-            const int rdx = s_res[0], rdy = s_res[1];
+        if (live && gtid < 32) {
+            // fused predict_frame + psnr SSE of this block at its vector (the group's first warp)
+            const int lane = gtid;
+            const int rdx = s_res[grp][0], rdy = s_res[grp][1];
             uint32_t sse = lane < BS ? row_sse_fp(cur, ref, b.W, h * BS, v * BS + lane, BS, rdx, rdy) : 0u;
             sse = __reduce_add_sync(0xFFFFFFFFu, sse);
             if (lane == 0) {
                 const int ty = boundary ? ME_BOUNDARY : ME_OPAQUE;
-                write_rec(a.recs + g, 2 * rdx, 2 * rdy, uint32_t(s_res[2]) * 4u, uint32_t(s_res[3]), 0, 0,
+                write_rec(a.recs + g, 2 * rdx, 2 * rdy, uint32_t(s_res[grp][2]) * 4u, uint32_t(s_res[grp][3]), 0, 0,
                           ty, false);
-                if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, uint32_t(s_res[3]), 0, ty);
+                if (a.stats) add_stats(a.stats + (size_t(seq) * b.pairs + p), sse, uint32_t(s_res[grp][3]), 0, ty);
             }
         }
     }
@@ -310,16 +325,34 @@ cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist
     ea.recs = recs;
     ea.band_rows_max = es_band_rows(b.bs, S, b.W, b.H);
     ea.stats = stats;
-    const size_t smem = es_smem_bytes(b.bs, S, b.W, b.H);
+    const size_t smem1 = es_smem_bytes(b.bs, S, b.W, b.H);
     // the row stride of the widest (unclipped) window, fixed for every block
     const int PW = ((min(2 * S + 1, b.W - b.bs + 1) - 1) >> 2) + (b.bs >> 2) + 1;
+    // blocks per CTA pass: 4 while four whole windows fit in ~64 KB (S <= 16), 2 within ~64 KB
+    // (S <= 32), else 1 (bands of rows for the largest windows)
+    const int WY = min(2 * S + 1, b.H - b.bs + 1);
+    const bool whole = ea.band_rows_max >= (WY + 7) / 8 * 8;
+    const int nb = !whole ? 1 : 4 * smem1 <= 64 * 1024 ? 4 : 2 * smem1 <= 64 * 1024 ? 2 : 1;
+    ea.region_words = int((smem1 + 15) / 16 * 4);
+    const size_t smem = size_t(nb) * ea.region_words * 4;
     void (*kern)(EsArgs);
-    if (b.bs == 16)
-        kern = PW == 37 ? es_kernel<16, 8, 37> : PW == 21 ? es_kernel<16, 8, 21> : PW == 13 ? es_kernel<16, 8, 13>
-                                                                                            : es_kernel<16, 8, 0>;
-    else
-        kern = PW == 35 ? es_kernel<8, 8, 35> : PW == 19 ? es_kernel<8, 8, 19> : PW == 11 ? es_kernel<8, 8, 11>
-                                                                                         : es_kernel<8, 8, 0>;
+    if (b.bs == 16) {
+        if (nb == 4)
+            kern = PW == 13 ? es_kernel<16, 8, 13, 4> : es_kernel<16, 8, 0, 4>;
+        else if (nb == 2)
+            kern = PW == 21 ? es_kernel<16, 8, 21, 2> : PW == 13 ? es_kernel<16, 8, 13, 2> : es_kernel<16, 8, 0, 2>;
+        else
+            kern = PW == 37 ? es_kernel<16, 8, 37, 1> : PW == 21 ? es_kernel<16, 8, 21, 1> : PW == 13 ? es_kernel<16, 8, 13, 1>
+                                                                                                  : es_kernel<16, 8, 0, 1>;
+    } else {
+        if (nb == 4)
+            kern = PW == 11 ? es_kernel<8, 8, 11, 4> : es_kernel<8, 8, 0, 4>;
+        else if (nb == 2)
+            kern = PW == 19 ? es_kernel<8, 8, 19, 2> : PW == 11 ? es_kernel<8, 8, 11, 2> : es_kernel<8, 8, 0, 2>;
+        else
+            kern = PW == 35 ? es_kernel<8, 8, 35, 1> : PW == 19 ? es_kernel<8, 8, 19, 1> : PW == 11 ? es_kernel<8, 8, 11, 1>
+                                                                                               : es_kernel<8, 8, 0, 1>;
+    }
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
     int occ = 0;
