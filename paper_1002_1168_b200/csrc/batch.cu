@@ -167,7 +167,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     const bool align = pa && pa_key_aligned(b, tune);  // (the scan holds the key histogram + tmin in shared memory)
     if ((e = cudaMemsetAsync(align ? s.hist2 : s.hist, 0, size_t(align ? b.n_seq : 1) * nbins * 4, st))) return e;
     if (align && (e = cudaMemsetAsync(s.tmin, 0x7F, size_t(b.n_seq) * 4, st))) return e;
-    if ((e = cudaMemsetAsync(s.counter, 0, 16, st))) return e;  // ES ticket + the PA launches' claim counters
+    if ((e = cudaMemsetAsync(s.counter, 0, 256, st))) return e;  // ES ticket, PA claim counters, direct list count
     if (stats && (e = cudaMemsetAsync(stats, 0, sizeof(me_pair_stats) * size_t(b.n_seq) * b.pairs, st)))
         return e;
 
@@ -188,6 +188,9 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
         ca.tmin = align ? s.tmin : nullptr;
         ca.tmin_g = align ? s.tmin : nullptr;
     }
+    // single-bin searches take their list straight from classify
+    ca.list_direct = pa ? nullptr : s.list;
+    ca.nlist_direct = pa ? nullptr : s.counter + 48;
     {
         NvtxRange nv("me_b200/classify");
         if ((e = launch_classify(ca, num_sms, st))) return e;
@@ -198,7 +201,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     // the hybrids split the list into narrow / wide / narrow step ranges.
     const int pa_mode = pa ? pa_kernel_mode(b, cfg, prev0, prev0_integer, num_sms, tune) : 0;
     int* ranges = pa_mode >= 3 ? s.counter + 8 : nullptr;
-    {
+    if (pa) {
         NvtxRange nv("me_b200/sort");
         if ((e = launch_scan(s.hist, nbins, pa_mode == 4 ? 4 : pa_mode >= 2 ? 2 : 1, s.offs, s.cursor, s.list,
                              pa_wide_threshold(num_sms, tune), ranges, st, tune.sort_pdl, ca.hist2, b.n_seq,
@@ -206,7 +209,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
             return e;
         if ((e = launch_fill(ca, s.cursor, s.list, num_sms, st, tune))) return e;
     }
-    const int* nlist = s.offs + nbins;
+    const int* nlist = pa ? s.offs + nbins : ca.nlist_direct;
     if (events) cudaEventRecord(events[2], st);
 
     NvtxRange nv_search("me_b200/search");
@@ -220,8 +223,8 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
 
     if (events) cudaEventRecord(events[3], st);
     if (pred && (e = launch_mc_pred(b, recs, pred, st))) return e;
-    // classify, scan, fill, the search (three launches for the PA hybrid), MC
-    if (launches) *launches = 3 + (pa_mode >= 3 ? 3 : 1) + (pred ? 1 : 0);
+    // classify, scan + fill (PA), the search (three launches for the PA hybrid), MC
+    if (launches) *launches = 1 + (pa ? 2 : 0) + (pa_mode >= 3 ? 3 : 1) + (pred ? 1 : 0);
     if (events) cudaEventRecord(events[4], st);
     return cudaGetLastError();
 }

@@ -35,6 +35,11 @@ struct ClassArgs {
     int* hist2;
     const int* tmin;  // fill: the keys' offsets (written by the scan)
     int* tmin_g;      // classify: atomicMin target (the same array, preset to 0x7F7F7F7F)
+    // single-bin searches (ES, TSS, FSS, DS): classify appends the estimated
+    // blocks' entries to the list itself (warp-aggregated, any order) and counts
+    // them in *nlist_direct — no scan / fill.  Null: the sorted list.
+    uint2* list_direct;
+    int* nlist_direct;
 };
 
 // wavefront.cu: classify -> per-step histogram -> scan -> fill (the sorted list)

@@ -71,8 +71,14 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
         uint32_t sse = 0, n_t = 0, n_o = 0, n_b = 0;
         int64_t gp = -1;
         int hkey[NB];
+        uint2 dent[NB];  // direct list entries (single-bin searches)
+        bool dval[NB];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) hkey[k] = -1;
+        for (int k = 0; k < NB; ++k) {
+            hkey[k] = -1;
+            dval[k] = false;
+            dent[k] = make_uint2(0u, 0u);
+        }
         if (si < n) {
             const int hs = int(si % strips);
             int64_t t = si / strips;
@@ -160,7 +166,11 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
                 r.w = uint32_t(ty) << 8;
                 *reinterpret_cast<uint4*>(a.recs + g) = r;
                 if (ty != ME_TRANSPARENT) {
-                    if (a.hist2)  // aligned keys: per (sequence, step) counts, added below
+                    if (a.list_direct) {  // appended below (any order: the blocks are independent)
+                        dval[k] = true;
+                        dent[k] = make_uint2(uint32_t(h) | (uint32_t(v) << 16) | (ty == ME_BOUNDARY ? kBoundaryBit : 0u),
+                                             uint32_t(p) | (uint32_t(seq) << 16));
+                    } else if (a.hist2)  // aligned keys: per (sequence, step) counts, added below
                         hkey[k] = seq * a.nbins + (h + 2 * v + p);
                     else
                         atomicAdd(&s_hist[a.pa ? a.key_a * (h + 2 * v + p) + a.key_s * seq : 0], 1);
@@ -174,6 +184,19 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             }
         }
     next:
+        if (a.list_direct) {  // one list append per warp and block slot
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, dval[k]);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    int base = 0;
+                    if (lane == leader) base = atomicAdd(a.nlist_direct, __popc(m));
+                    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+                    if (dval[k]) a.list_direct[base + __popc(m & ((1u << lane) - 1u))] = dent[k];
+                }
+            }
+        }
         if (a.hist2) {  // one atomic per distinct (sequence, step) of the warp, and the sequences' first steps
             int tm = 0x7FFFFFFF, sq = -1;
 #pragma unroll
@@ -216,7 +239,7 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             }
         }
     }
-    if (a.hist2) return;
+    if (a.hist2 || a.list_direct) return;
     __syncthreads();
     for (int i = threadIdx.x; i < a.nbins; i += blockDim.x)
         if (s_hist[i]) atomicAdd(&a.hist[i], s_hist[i]);
