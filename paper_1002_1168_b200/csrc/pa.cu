@@ -2171,9 +2171,11 @@ cudaError_t launch_pa(const Batch& b, const me_config& cfg, const int32_t* prev0
         // (1-1.5 % better than 2 or 4 at 32-64); wider ones 4 (the hybrid's
         // head and tail)
         const int64_t per_step = b.nblocks() / std::max(1, b.steps());
+        // (a single sequence searched with per-candidate patches, S > 32: 2 CTAs,
+        // config 5 2.37 -> 2.21 ms; with the staged window, S <= 32: 1)
         const int mb = t.pa_fast_ctas > 0 ? t.pa_fast_ctas
                        : pa_mode != 1      ? 4
-                       : b.n_seq == 1      ? 1
+                       : b.n_seq == 1      ? (cfg.search_range > 32 ? 2 : 1)
                        : per_step < int64_t(num_sms) * 60 ? 2
                        : per_step < int64_t(num_sms) * 160 ? 3 : 4;
         fast = mb == 1 ? pa_fast_kernel<1> : mb == 2 ? pa_fast_kernel<2> : mb == 3 ? pa_fast_kernel<3> : mb == 5 ? pa_fast_kernel<5> : mb == 6 ? pa_fast_kernel<6> : pa_fast_kernel<4>;
