@@ -661,7 +661,7 @@ def bench_critical_path(args, local, dev):
                             "macroblocks_per_s": pairs * (W // 16) * (H // 16) / (tot / 1e3)}
         del luma, alpha, recs, stats, flush
     torch.cuda.empty_cache()
-    return {"model": "search time = wavefront steps x per-step latency (pa_fast_kernel, one CTA per SM; CUDA events, L2 flushed)", **out}
+    return {"model": "search time = wavefront steps x per-step latency (pa_fast_kernel: one CTA per SM with the staged window, S <= 32; two with per-candidate patches, S = 64; CUDA events, L2 flushed)", **out}
 
 
 def bench_units(args, world, rank, local, dev, wl="cfg5-es"):
