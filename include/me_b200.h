@@ -138,7 +138,7 @@ typedef struct me_tuning {
     int32_t pa_quad_ctas;     /* CTAs per SM of pa_quad_kernel, 2..4 (0: 3) */
     int32_t pa_duo_threads;   /* 128 or 256 (0: 256) */
     int32_t pa_duo_ctas;      /* CTAs per SM of pa_duo_kernel (0: 4 at 256 threads, 7 at 128) */
-    int32_t pa_poll_ns;       /* dependency poll back-off in ns (0: 64) */
+    int32_t pa_poll_ns;       /* dependency poll back-off in ns (0: 16) */
     int32_t pa_static_claim;  /* 1: static round-robin work split (needs the whole grid resident);
                                  0: in-order CTA-batch claiming */
     int32_t pa_no_pdl;        /* 1: launch the hybrid's grids in plain stream order */

@@ -48,7 +48,7 @@ struct Tuning {
     int pa_quad_ctas = 3;
     int pa_duo_threads = 256;
     int pa_duo_ctas = 0;     // 0: 4 (256 threads) or 7 (128)
-    int pa_poll_ns = 64;
+    int pa_poll_ns = 16;
     bool pa_claim = true;    // in-order CTA-batch claiming
     bool pa_pdl = true;
     bool pa_smem_pair = true;

@@ -1,7 +1,7 @@
 """PA schedule sweep on the single-sequence configs (1, 2, 3, 5): ms per
 sequence for fast-kernel CTAs per SM and the hybrid at low wide-step
 thresholds, set through me_tuning; every variant's records are compared with
-the first.  usage: seq_schedule_probe.py [config ...]"""
+the first.  usage: seq_schedule_probe.py [config ...] [name:field=v,... ...]"""
 import sys
 
 import torch
@@ -10,14 +10,19 @@ sys.path.insert(0, ".")
 import paper_1002_1168_b200 as me  # noqa: E402
 from paper_1002_1168_b200 import _lib, batch as B, synth  # noqa: E402
 
-for cid in [int(x) for x in (sys.argv[1:] or ["2", "3", "5"])]:
+CONFIGS = [int(x) for x in sys.argv[1:] if ":" not in x and x.isdigit()] or [2, 3, 5]
+VARIANTS = [x for x in sys.argv[1:] if not x.isdigit()]  # name:field=v,... (tuning); first one is the reference
+for cid in CONFIGS:
     luma, alpha = synth.config4_batch_dev(1, 20260000, None, config_id=cid)
     F, H, W = luma.shape[1:]
     cfg = me.BatchConfig(algo=me.Algo.PA, search=me.SearchConfig(search_range=16 if cid <= 2 else (32 if cid == 3 else 64), block_size=8))
     res, first = {}, None
-    for name, kw in (("auto", {}), ("fast2", dict(pa_schedule="fast", pa_fast_ctas=2)), ("fast3", dict(pa_schedule="fast", pa_fast_ctas=3)),
-                     ("fast4", dict(pa_schedule="fast", pa_fast_ctas=4)), ("hyb-w5", dict(pa_schedule="hybrid", pa_wide_blocks=5 * 148)),
-                     ("hyb-w10", dict(pa_schedule="hybrid", pa_wide_blocks=10 * 148)), ("hyb-w20", dict(pa_schedule="hybrid", pa_wide_blocks=20 * 148))):
+    variants = [(spec.partition(":")[0], {k: int(v) for k, v in (x.split("=") for x in spec.partition(":")[2].split(",") if x)})
+                for spec in VARIANTS] if VARIANTS else \
+        (("auto", {}), ("fast2", dict(pa_schedule="fast", pa_fast_ctas=2)), ("fast3", dict(pa_schedule="fast", pa_fast_ctas=3)),
+         ("fast4", dict(pa_schedule="fast", pa_fast_ctas=4)), ("hyb-w5", dict(pa_schedule="hybrid", pa_wide_blocks=5 * 148)),
+         ("hyb-w10", dict(pa_schedule="hybrid", pa_wide_blocks=10 * 148)), ("hyb-w20", dict(pa_schedule="hybrid", pa_wide_blocks=20 * 148)))
+    for name, kw in variants:
         _lib.set_tuning(0, **kw)
         recs = torch.empty((1, F - 2, H // 8, W // 8, 16), dtype=torch.uint8, device="cuda")
         stats = torch.empty((1, F - 2, 48), dtype=torch.uint8, device="cuda")
