@@ -284,6 +284,25 @@ def test_pa_list_keys(me_gpu, port, mode, key, tuning):
         assert np.array_equal(stats[i], want_s)
 
 
+@pytest.mark.parametrize("ctas", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("window", [0, 1])
+def test_pa_fast_ctas_per_sm(me_gpu, port, ctas, window, tuning):
+    """pa_fast_kernel at every CTAs-per-SM instantiation the schedule picks by
+    batch width (1 for single sequences, 2 / 3 / 4 for wider batches and the
+    hybrid's head and tail; 5 / 6 by tuning), with the staged window and with
+    per-candidate patches."""
+    from paper_1002_1168_b200 import synth
+
+    tuning(pa_schedule="fast", pa_fast_ctas=ctas, pa_fast_patches=1 - window)
+    luma, alpha = synth.config4_batch(3, 4100 + ctas, frames=5)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.PA, search=me_gpu.SearchConfig(search_range=16, block_size=8))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in range(3):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=4, search_range=16, block_size=8), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"ctas {ctas} window {window} seq {i}")
+        assert np.array_equal(stats[i], want_s)
+
+
 @pytest.mark.parametrize("bt,it", [(0, 4), (1, 4), (0, 7)])
 @pytest.mark.parametrize("mode", ["fast", "duo", "duo-hybrid", "hybrid", "warp", "hybrid-static"])
 def test_pa_kernel_modes(me_gpu, port, mode, bt, it, tuning):
