@@ -284,6 +284,23 @@ def test_pa_list_keys(me_gpu, port, mode, key, tuning):
         assert np.array_equal(stats[i], want_s)
 
 
+@pytest.mark.parametrize("S", [12, 24, 32, 48])
+@pytest.mark.parametrize("bs", [8, 16])
+def test_es_blocks_per_pass(me_gpu, port, S, bs):
+    """es_kernel's small-window path (NB = 4 / 2 blocks per CTA pass, the
+    compile-time and generic row strides) and its banded large-window path,
+    on a batch whose block count is not a multiple of NB."""
+    from paper_1002_1168_b200 import synth
+
+    luma, alpha = synth.config4_batch(3, 5200 + S + bs, frames=4)
+    cfg = me_gpu.BatchConfig(algo=me_gpu.Algo.ES, search=me_gpu.SearchConfig(search_range=S, block_size=bs))
+    recs, stats = me_gpu.run_sequences(cfg, luma, alpha)
+    for i in range(3):
+        want_r, want_s = port.run_sequence(oracle.make_cfg(algo=int(me_gpu.Algo.ES), search_range=S, block_size=bs), luma[i], alpha[i])
+        assert_recs(recs[i], want_r, f"ES S{S} bs{bs} seq {i}")
+        assert np.array_equal(stats[i], want_s)
+
+
 @pytest.mark.parametrize("ctas", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("window", [0, 1])
 def test_pa_fast_ctas_per_sm(me_gpu, port, ctas, window, tuning):
