@@ -181,22 +181,46 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         // tasks (run, col) in raster order: flat index, run by a float
         // reciprocal.  The window's last run usually holds ONE row (WY = 2S + 1
         // = 8n + 1 for interior blocks): its tasks take a K = 1 body instead of
-        // summing K - 1 rows past the window.
+        // summing K - 1 rows past the window.  The K-row tasks that do not fill
+        // a whole round of the group's threads are split into K one-row tasks
+        // each, queued with the tail run's: the last round then costs a few
+        // one-row sums instead of a whole K-row task on a fraction of the threads
+        // (config 5: 2064 K-row tasks = 8 rounds + 16).
         const float inv_wx = 1.0f / float(WX);
         const bool tail1 = run0 + bruns == nruns && WY - (nruns - 1) * K == 1;
-        for (int ti = tid, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX; run < bruns;
-             ti += T, run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX) {
-            const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
-            const uint32_t adx8 = uint32_t(abs(lo_x + col)) << 3;
-            const uint32_t* rk = rkey + run * K;
-            const uint32_t m32 = tail1 && run == bruns - 1 ? es_task<BS, 1, PWC>(c, base, PW, rk, adx8)
-                                                          : es_task<BS, K, PWC>(c, base, PW, rk, adx8);
+        const int nfull = (tail1 ? bruns - 1 : bruns) * WX;
+        const int F = nfull / T * T, R = nfull - F;  // whole rounds of K-row tasks, leftover K-row tasks
+        const int ntasks = F + R * K + (tail1 ? WX : 0);
+        auto take = [&](int run, int col, int k, uint32_t m32) {
             if (m32 < kEsDead) {
                 const uint32_t wy = uint32_t((run0 + run) * K) + (m32 & 7u);
                 const unsigned long long key = (static_cast<unsigned long long>(m32 >> 12) << 40) |
                                                (static_cast<unsigned long long>((m32 >> 3) & 0x1FFu) << 24) |
                                                static_cast<unsigned long long>(wy * uint32_t(WX) + uint32_t(col));
                 best = key < best ? key : best;
+            }
+        };
+        for (int ti = tid; ti < ntasks; ti += T) {
+            if (ti < F) {
+                const int run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX;
+                const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
+                take(run, col, 0, es_task<BS, K, PWC>(c, base, PW, rkey + run * K, uint32_t(abs(lo_x + col)) << 3));
+            } else {
+                // one row k of a leftover K-row task, or of the one-row tail run
+                const int j = ti - F;
+                int run, col, k;
+                if (j < R * K) {
+                    const int f = F + j / K;
+                    run = __float2int_rz((float(f) + 0.5f) * inv_wx);
+                    col = f - run * WX;
+                    k = j - (j / K) * K;
+                } else {
+                    run = bruns - 1;
+                    col = j - R * K;
+                    k = 0;
+                }
+                const uint32_t* base = sm + (col & 3) * CW + (run * K + k) * PW + (col >> 2);
+                take(run, col, k, es_task<BS, 1, PWC>(c, base, PW, rkey + run * K + k, uint32_t(abs(lo_x + col)) << 3));
             }
         }
     }
