@@ -191,6 +191,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
     // single-bin searches take their list straight from classify
     ca.list_direct = pa ? nullptr : s.list;
     ca.nlist_direct = pa ? nullptr : s.counter + 48;
+    ca.es_runs = algo == ME_ALGO_ES && es_use_runs(b, cfg.search_range) && b.cols < 4096 ? 1 : 0;
     {
         NvtxRange nv("me_b200/classify");
         if ((e = launch_classify(ca, num_sms, st))) return e;
@@ -214,7 +215,7 @@ cudaError_t run_batch(const Batch& b, const me_config& cfg, const int32_t* prev0
 
     NvtxRange nv_search("me_b200/search");
     if (algo == ME_ALGO_ES)
-        e = launch_es(b, cfg.search_range, s.list, nlist, s.counter, recs, stats, num_sms, st);
+        e = launch_es(b, cfg.search_range, s.list, nlist, s.counter, recs, stats, num_sms, st, s.types);
     else if (algo == ME_ALGO_PA)
         e = launch_pa(b, cfg, prev0, s.list, nlist, ranges, pa_mode, recs, stats, num_sms, st, s.counter + 1, tune);
     else

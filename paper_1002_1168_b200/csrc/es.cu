@@ -35,6 +35,7 @@ struct EsArgs {
     int band_rows_max;  // staged rows per band (multiple of K, + BS - 1 added on top)
     me_pair_stats* stats;
     int region_words;   // shared memory per block group (NB > 1)
+    const uint8_t* types;  // run mode: the blocks' types (records)
 };
 
 constexpr int kEsThreads = 256;
@@ -81,18 +82,25 @@ __device__ __forceinline__ uint32_t es_task(const uint32_t (&c)[BS][BS / 4], con
 // its own shared-memory region (small windows: NB blocks per CTA pass, see
 // es_kernel): tid / T = this thread's index / size within its group; every
 // group passes the same CTA barriers (one band per block when NB > 1).
+// Runs of horizontally adjacent blocks (es_kernel's run mode) share ONE staged
+// window, the union of theirs: ux0 >= 0 is its first frame column and
+// urowbytes its width; it is staged by all the CTA's threads (stid of sT) and
+// each group reads its block's positions at their byte offset in it.
 template <int BS, int K, int PWC = 0>
 __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
                          int S, int band_runs_max, uint32_t* sm, unsigned long long* s_best,
                          int& out_dx, int& out_dy, uint32_t& out_sad, uint32_t& out_cmp,
-                         int tid = threadIdx.x, int T = kEsThreads) {
+                         int tid = threadIdx.x, int T = kEsThreads, int ux0 = -1, int urowbytes = 0) {
     const int lane = tid & 31, wid = tid >> 5;
     const int lo_x = max(-S, -x0), hi_x = min(S, W - x0 - BS);
     const int lo_y = max(-S, -y0), hi_y = min(S, H - y0 - BS);
     const int WX = hi_x - lo_x + 1, WY = hi_y - lo_y + 1;
     const int nruns = (WY + K - 1) / K;
-    const int rowbytes = WX + BS - 1;
-    const int PW = PWC ? PWC : ((WX - 1) >> 2) + (BS >> 2) + 1;  // words per staged row (>= the window's)
+    const bool uni = ux0 >= 0;
+    const int rowbytes = uni ? urowbytes : WX + BS - 1;
+    const int coff = uni ? x0 + lo_x - ux0 : 0;  // this block's window start in the staged rows (bytes)
+    const int stid = uni ? int(threadIdx.x) : tid, sT = uni ? kEsThreads : T;  // who stages
+    const int PW = PWC ? PWC : ((rowbytes - BS) >> 2) + (BS >> 2) + 1;  // words per staged row (>= the window's)
     constexpr int NW = BS / 4;
 
     uint32_t c[BS][NW];
@@ -116,7 +124,10 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
     for (int run0 = 0; run0 < nruns; run0 += band_runs_max) {
         const int bruns = min(band_runs_max, nruns - run0);
         const int srows = bruns * K + BS - 1;
-        int CW = srows * PW;
+        // (run mode, one band: a window of 8n + 1 rows ends in a one-row run,
+        // so only WY + BS - 1 rows are ever read)
+        const bool last1 = run0 + bruns == nruns && WY - (nruns - 1) * K == 1;
+        int CW = (uni && last1 ? WY + BS - 1 : srows) * PW;
         CW += ((8 - (CW & 31)) + 32) & 31;  // copy stride = 8 (mod 32) words: conflict-free lanes
         const int row_g0 = y0 + lo_y + run0 * K;  // frame row of staged row 0
         const int rows_valid = min(srows, WY + BS - 1 - run0 * K);
@@ -124,7 +135,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         // aligned when W % 4 == 0 (checked by the launcher's caller)
         const uint32_t* rw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(ref) & ~uintptr_t(3));
         const uint32_t ref_mis = uint32_t(reinterpret_cast<uintptr_t>(ref) & 3);
-        const uint32_t seg0 = ref_mis + uint32_t(row_g0) * uint32_t(W) + uint32_t(x0 + lo_x);  // byte offset from rw
+        const uint32_t seg0 = ref_mis + uint32_t(row_g0) * uint32_t(W) + uint32_t(uni ? ux0 : x0 + lo_x);  // byte offset from rw
         __syncthreads();  // previous band / block done with smem
         // staging from aligned words: copy s, word q = bytes [4q + s, 4q + s + 4)
         // of the row segment = a funnel shift of two aligned words.  Bytes past
@@ -142,11 +153,11 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
             // U words per thread per round, every load of the round issued
             // before any store (the staging is L2-latency-bound otherwise)
             constexpr int U = 4;
-            for (int i0 = tid; i0 < total; i0 += U * T) {
+            for (int i0 = stid; i0 < total; i0 += U * sT) {
                 uint32_t g[U][3], offs[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int i = min(i0 + u * T, total - 1);
+                    const int i = min(i0 + u * sT, total - 1);
                     const int row = __float2int_rz((float(i) + 0.5f) * inv_pw), q = i - row * PW;
                     const uint32_t b0 = seg0 + uint32_t(row) * uint32_t(W);
                     const uint32_t w0 = b0 >> 2, wl = (b0 + uint32_t(rowbytes) - 1) >> 2;
@@ -157,7 +168,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * T;
+                    const int i = i0 + u * sT;
                     if (i >= total) break;
                     const uint32_t off = offs[u], sh = off * 8, g0 = g[u][0], g1 = g[u][1], g2 = g[u][2];
                     // copies s = 0..3: byte offset off + s within (g0, g1, g2)
@@ -173,7 +184,7 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         // IMADs (FMA pipe) and the VIMNMX — the kernel is ALU-pipe-bound
         // (VABSDIFF4 issues at half rate there)
         uint32_t* const rkey = sm + 4 * CW;
-        for (int i = tid; i < bruns * K; i += T) {
+        for (int i = stid; i < bruns * K; i += sT) {
             const int wy = run0 * K + i;
             rkey[i] = wy < WY ? (uint32_t(abs(lo_y + wy)) << 3) | uint32_t(i % K) : kEsDead;
         }
@@ -203,7 +214,8 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
         for (int ti = tid; ti < ntasks; ti += T) {
             if (ti < F) {
                 const int run = __float2int_rz((float(ti) + 0.5f) * inv_wx), col = ti - run * WX;
-                const uint32_t* base = sm + (col & 3) * CW + (run * K) * PW + (col >> 2);
+                const int o = coff + col;
+                const uint32_t* base = sm + (o & 3) * CW + (run * K) * PW + (o >> 2);
                 take(run, col, 0, es_task<BS, K, PWC>(c, base, PW, rkey + run * K, uint32_t(abs(lo_x + col)) << 3));
             } else {
                 // one row k of a leftover K-row task, or of the one-row tail run
@@ -219,7 +231,8 @@ __device__ void es_block(const uint8_t* cur, const uint8_t* ref, int W, int H, i
                     col = j - R * K;
                     k = 0;
                 }
-                const uint32_t* base = sm + (col & 3) * CW + (run * K + k) * PW + (col >> 2);
+                const int o = coff + col;
+                const uint32_t* base = sm + (o & 3) * CW + (run * K + k) * PW + (o >> 2);
                 take(run, col, k, es_task<BS, 1, PWC>(c, base, PW, rkey + run * K + k, uint32_t(abs(lo_x + col)) << 3));
             }
         }
@@ -299,6 +312,75 @@ __global__ void __launch_bounds__(kEsThreads) es_kernel(EsArgs a) {
     }
 }
 
+// Run mode (16x16 blocks, the largest ranges): the list holds runs of 1, 2 or
+// 4 horizontally adjacent estimated blocks of one block row (classify emits
+// them, count in entry bits 12-14).  A pass takes one run: its blocks' union
+// window (the first block's window plus 16 columns per further block) is
+// staged once by the whole CTA — 144 rows x 37 words for one block at S = 64,
+// 144 x 49 for four — and the CTA splits into one group per block.  Staging,
+// which the other CTA on the SM does not hide (config 5: 16 % of the search),
+// is shared by up to four blocks.
+template <int P1, int P2, int P4>
+__global__ void __launch_bounds__(kEsThreads, 2) es_run_kernel(EsArgs a) {
+    constexpr int BS = 16, K = 8;
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ unsigned long long s_best[kEsThreads / 32];
+    __shared__ int s_item;
+    __shared__ int s_res[4][4];
+    const Batch& b = a.b;
+    const int n = *a.nlist;
+    const size_t plane = size_t(b.W) * b.H;
+    const int band_runs = a.band_rows_max / K;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= n) return;
+        const uint2 e = a.list[item];
+        const int h0 = int(e.x & 0xFFF), cnt = int((e.x >> 12) & 7u), v = int((e.x >> 16) & 0x7FFF);
+        const int p = int(e.y & 0xFFFF), seq = int(e.y >> 16);
+        const int T = kEsThreads / cnt, grp = int(threadIdx.x) / T, gtid = int(threadIdx.x) - grp * T;
+        const int h = h0 + grp;
+        const uint8_t* cur = b.luma + (size_t(seq) * b.F + p + b.d) * plane;
+        const uint8_t* ref = b.luma + (size_t(seq) * b.F + p) * plane;
+        // the union of the run's windows (frame columns)
+        const int xa = h0 * BS, xb = (h0 + cnt - 1) * BS;
+        const int ux0 = xa + max(-a.S, -xa), ux1 = xb + min(a.S, b.W - xb - BS) + BS - 1;
+        int dx, dy;
+        uint32_t sad, cmp;
+        unsigned long long* sb = s_best + grp * (T / 32);
+        if (cnt == 4)
+            es_block<BS, K, P4>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, sb, dx, dy, sad, cmp, gtid, T, ux0, ux1 - ux0 + 1);
+        else if (cnt == 2)
+            es_block<BS, K, P2>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, sb, dx, dy, sad, cmp, gtid, T, ux0, ux1 - ux0 + 1);
+        else
+            es_block<BS, K, P1>(cur, ref, b.W, b.H, h * BS, v * BS, a.S, band_runs, sm, sb, dx, dy, sad, cmp, gtid, T, ux0, ux1 - ux0 + 1);
+        if (gtid == 0) {
+            s_res[grp][0] = dx;
+            s_res[grp][1] = dy;
+            s_res[grp][2] = int(sad);
+            s_res[grp][3] = int(cmp);
+        }
+        __syncthreads();
+        if (gtid < 32) {
+            // fused predict_frame + psnr SSE of this group's block at its vector
+            const int lane = gtid;
+            const int rdx = s_res[grp][0], rdy = s_res[grp][1];
+            uint32_t sse = lane < BS ? row_sse_fp(cur, ref, b.W, h * BS, v * BS + lane, BS, rdx, rdy) : 0u;
+            sse = __reduce_add_sync(0xFFFFFFFFu, sse);
+            if (lane == 0) {
+                const size_t pr = size_t(seq) * b.pairs + p;
+                const uint32_t g = uint32_t((pr * b.rows + v) * b.cols + h);
+                const int ty = a.types && a.types[g] == ME_BOUNDARY ? ME_BOUNDARY : ME_OPAQUE;
+                write_rec(a.recs + g, 2 * rdx, 2 * rdy, uint32_t(s_res[grp][2]) * 4u, uint32_t(s_res[grp][3]), 0, 0,
+                          ty, false);
+                if (a.stats) add_stats(a.stats + pr, sse, uint32_t(s_res[grp][3]), 0, ty);
+            }
+        }
+    }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(kEsThreads) es_single_kernel(const uint8_t* cur, const uint8_t* ref,
                                                                int W, int H, int x0, int y0, int S,
@@ -338,9 +420,21 @@ size_t es_smem_bytes(int bs, int S, int W, int H) {
     return size_t(4) * (size_t(srows) * PW + 32) * 4 + size_t(brows) * 4;
 }
 
+// Run mode (es_run_kernel) for 16x16 blocks at the ranges whose one-block window
+// is too large for several per CTA (S > 32): while a four-block union window
+// still leaves two CTAs per SM and the whole window fits in one band.
+bool es_use_runs(const Batch& b, int S) {
+    if (b.bs != 16 || S <= 32 || S > 64) return false;
+    const int WX = min(2 * S + 1, b.W - 16 + 1), WY = min(2 * S + 1, b.H - 16 + 1);
+    const int PW4 = ((WX - 1 + 48) >> 2) + 5;
+    const size_t rows = size_t(WY % 8 == 1 ? WY + 15 : (WY + 7) / 8 * 8 + 15);
+    return size_t(4) * (rows * PW4 + 32) * 4 + size_t(WY + 8) * 4 <= 113 * 1024 && es_band_rows(16, S, b.W, b.H) >= (WY + 7) / 8 * 8;
+}
+
 cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist, int* counter,
-                      me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st) {
+                      me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st, const uint8_t* types) {
     EsArgs ea;
+    ea.types = types;
     ea.b = b;
     ea.S = S;
     ea.list = list;
@@ -349,6 +443,20 @@ cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist
     ea.recs = recs;
     ea.band_rows_max = es_band_rows(b.bs, S, b.W, b.H);
     ea.stats = stats;
+    if (es_use_runs(b, S)) {
+        ea.band_rows_max = es_band_rows(b.bs, S, b.W, b.H);
+        const int WX = min(2 * S + 1, b.W - 16 + 1), WY = min(2 * S + 1, b.H - 16 + 1);
+        const int PW4 = ((WX - 1 + 48) >> 2) + 5;
+        const size_t rows = size_t(WY % 8 == 1 ? WY + 15 : (WY + 7) / 8 * 8 + 15);
+        const size_t smem = size_t(4) * (rows * PW4 + 32) * 4 + size_t(ea.band_rows_max) * 4;
+        void (*kern)(EsArgs) = (S == 64 && WX == 129) ? es_run_kernel<37, 41, 49> : es_run_kernel<0, 0, 0>;
+        cudaError_t e;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))) return e;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEsThreads, smem);
+        kern<<<num_sms * (occ > 0 ? occ : 1), kEsThreads, smem, st>>>(ea);
+        return cudaGetLastError();
+    }
     const size_t smem1 = es_smem_bytes(b.bs, S, b.W, b.H);
     // the row stride of the widest (unclipped) window, fixed for every block
     const int PW = ((min(2 * S + 1, b.W - b.bs + 1) - 1) >> 2) + (b.bs >> 2) + 1;

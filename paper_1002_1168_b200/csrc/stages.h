@@ -40,6 +40,9 @@ struct ClassArgs {
     // them in *nlist_direct — no scan / fill.  Null: the sorted list.
     uint2* list_direct;
     int* nlist_direct;
+    // ... as runs of 1, 2 or 4 horizontally adjacent estimated blocks (16x16
+    // ES at the largest ranges, es_run_kernel): entry {h | count << 12 | v << 16, p | seq << 16}
+    int es_runs;
 };
 
 // wavefront.cu: classify -> per-step histogram -> scan -> fill (the sorted list)
@@ -56,7 +59,11 @@ cudaError_t launch_fill(const ClassArgs& ca, int* cursor, uint2* list, int num_s
 
 // es.cu: full search over the list; single-block full search
 cudaError_t launch_es(const Batch& b, int S, const uint2* list, const int* nlist, int* counter,
-                      me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st);
+                      me_block_rec* recs, me_pair_stats* stats, int num_sms, cudaStream_t st,
+                      const uint8_t* types = nullptr);
+// ES on 16x16 blocks at S > 32 takes runs of adjacent blocks (classify emits
+// them when ClassArgs::es_runs is set; es_run_kernel shares their windows)
+bool es_use_runs(const Batch& b, int S);
 cudaError_t launch_es_single(const uint8_t* cur, const uint8_t* ref, int W, int H, int x0, int y0,
                              int size, int range, int64_t* out, cudaStream_t st);
 

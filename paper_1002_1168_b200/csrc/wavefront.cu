@@ -184,6 +184,26 @@ __global__ void __launch_bounds__(256) classify_kernel(ClassArgs a) {
             }
         }
     next:
+        if (a.list_direct && a.es_runs && NB == 1) {
+            // runs of 4 / 2 horizontally adjacent estimated blocks (aligned lane
+            // quads / pairs of the warp's consecutive strips in one block row),
+            // else single blocks: the entry's first block, count in bits 12-14
+            const unsigned E = __ballot_sync(0xFFFFFFFFu, dval[0]);
+            const uint32_t hx = dent[0].x & 0xFFFu;
+            const unsigned long long rid = (static_cast<unsigned long long>(dent[0].y) << 16) | ((dent[0].x >> 16) & 0x7FFFu);
+            const unsigned long long rid_n = __shfl_down_sync(0xFFFFFFFFu, rid, 1);
+            const uint32_t hx_n = __shfl_down_sync(0xFFFFFFFFu, hx, 1);
+            const unsigned N = __ballot_sync(0xFFFFFFFFu, lane < 31 && dval[0] && rid_n == rid && hx_n == hx + 1);
+            const bool q4 = (lane & 3) == 0 && ((E >> lane) & 0xFu) == 0xFu && ((N >> lane) & 0x7u) == 0x7u;
+            const unsigned Q = __ballot_sync(0xFFFFFFFFu, q4);
+            const bool inq = (Q >> (lane & ~3)) & 1u;
+            const bool p2 = !inq && (lane & 1) == 0 && ((E >> lane) & 3u) == 3u && ((N >> lane) & 1u);
+            const unsigned P = __ballot_sync(0xFFFFFFFFu, p2);
+            const bool inp = (P >> (lane & ~1)) & 1u;
+            const uint32_t cnt = q4 ? 4u : p2 ? 2u : (dval[0] && !inq && !inp) ? 1u : 0u;
+            dval[0] = cnt != 0;
+            dent[0].x = hx | (cnt << 12) | (dent[0].x & 0x7FFF0000u);
+        }
         if (a.list_direct) {  // one list append per warp and block slot
 #pragma unroll
             for (int k = 0; k < NB; ++k) {
